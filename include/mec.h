@@ -1,0 +1,159 @@
+/*
+ * mec.h -- C ABI of libmec.so, the B200 (sm_100a) hot path of MEC
+ * (Cho & Brand, "MEC: Memory-efficient Convolution for Deep Neural Network",
+ *  ICML 2017, arXiv 1706.06873).  "P:<n>" cites line n of the paper text.
+ *
+ * The operation (Sec. 2.1): O = I * K with strides s_h, s_w; zero
+ * padding is assumed already applied to I; o = (i - k) / s + 1 (Eq. 1, floor).
+ * Layouts (Table 1), all row-major:
+ *   I  i_n x i_h x i_w x i_c     (n-h-w-c)
+ *   K  k_h x k_w x i_c x k_c     (read as a (k_h k_w i_c) x k_c matrix, Alg.2 l.7)
+ *   O  i_n x o_h x o_w x k_c     (n-h-w-c, Alg.2 l.27)
+ *   L  i_n x o_w x i_h x k_w x i_c  (MEC's compact lowered tensor, Alg.2 l.2-6)
+ *
+ * Conventions for every entry point:
+ *  - All tensor pointers are DEVICE pointers owned by the caller.  The library
+ *    never frees or retains them past the call; work is enqueued
+ *    asynchronously on `stream` (a cudaStream_t; NULL = legacy default
+ *    stream), so buffers must stay alive until the stream reaches the work.
+ *  - Functions never throw and never abort; they return an mec_status_t.
+ *    On MEC_ERR_CUDA the CUDA error string is available from
+ *    mec_last_error_message() (per-thread).
+ *  - I, O and L must not alias each other.  I and K are read-only.
+ *  - dtype: MEC_DTYPE_BF16 -> I, K, O are bf16 (2 B), fp32 accumulation in
+ *    tensor memory, O rounded to nearest-even.  MEC_DTYPE_TF32 -> I, K, O are
+ *    fp32 (4 B) in memory, multiplied as tf32 (tcgen05 kind::tf32), fp32
+ *    accumulation, O written as fp32.
+ *  - Inputs must be finite: the K-tail of a window reads up to one K-tile of
+ *    neighbouring lowered data, multiplied by zero weight rows.
+ */
+#ifndef MEC_H
+#define MEC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MEC_ABI_VERSION 1
+
+typedef enum {
+  MEC_OK = 0,
+  MEC_ERR_INVALID_ARG = 1, /* extent < 1, stride < 1, i < k, NULL pointer, bad enum */
+  MEC_ERR_UNSUPPORTED = 2, /* forced path infeasible (e.g. Solution A with #O > #L) */
+  MEC_ERR_MISALIGNED = 3,  /* I, K, O, L or workspace not 16-byte aligned */
+  MEC_ERR_CUDA = 4,        /* a CUDA runtime / driver error; see mec_last_error_message() */
+  MEC_ERR_NO_MEMORY = 5    /* workspace too small, or the stream-ordered allocation failed */
+} mec_status_t;
+
+typedef enum {
+  MEC_DTYPE_BF16 = 0,
+  MEC_DTYPE_TF32 = 1
+} mec_dtype_t;
+
+/* Table 1 symbols.  k_c is the number of output channels. */
+typedef struct {
+  int64_t i_n, i_h, i_w, i_c, k_h, k_w, k_c;
+} mec_shape_t;
+
+/* Which of Algorithm 2's two solutions runs.  The paper's letters
+ * are used: Solution A = batch-folded GEMMs (o_h GEMMs of (i_n o_w) rows,
+ * Alg.2 l.9-19); Solution B = per-image GEMMs (i_n o_h GEMMs of o_w rows,
+ * Alg.2 l.20-25).  (BASELINE.json's north_star swaps the two letters.) */
+typedef enum {
+  MEC_PATH_AUTO = 0,       /* Alg.2 l.8: A iff o_w <= T and #O <= #L, else B */
+  MEC_PATH_SOLUTION_A = 1, /* batch-folded */
+  MEC_PATH_SOLUTION_B = 2, /* per-image */
+  MEC_PATH_FUSED = 3       /* lowering fused into the GEMM (L never in HBM); reserved */
+} mec_path_t;
+
+/* How Solution A reaches n-h-w-c (Alg.2 l.13-19). */
+typedef enum {
+  MEC_SOLA_FIX_EPILOGUE = 0, /* GEMM epilogue stores O[n,h] = O_hnwc[h,n] directly (default) */
+  MEC_SOLA_FIX_LITERAL = 1,  /* paper-literal: GEMMs write O in h-n-w-c, "Copy L = O",
+                                then O[n,h,:] = L[h,n,:] (two extra passes over O) */
+  MEC_SOLA_FIX_NONE = 2      /* leave O in h-n-w-c (a following pooling layer may
+                                consume h-n-w-c); O is then o_h x i_n x o_w x k_c */
+} mec_sola_fix_t;
+
+#define MEC_DEFAULT_T 100 /* "we found T around 100 to be a good threshold" */
+
+typedef struct {
+  int path;       /* mec_path_t; MEC_PATH_AUTO by default */
+  int T;          /* threshold of Alg.2 l.8; <= 0 means MEC_DEFAULT_T */
+  int sola_fix;   /* mec_sola_fix_t; used only when Solution A runs */
+  int reserved0;
+  void* workspace;        /* device buffer >= mec_workspace_bytes(); NULL = stream-ordered pool */
+  size_t workspace_bytes;
+  /* Optional cudaEvent_t handles recorded on `stream` at stage boundaries
+   * (NULL entries are skipped): [0] before lowering, [1] after lowering,
+   * [2] after the window GEMMs, [3] after the Solution A format fix (== [2]
+   * when there is none).  For per-stage timing only. */
+  void* stage_events[4];
+  int selected_path; /* OUT: the path that ran (1 = A, 2 = B, 3 = fused) */
+  int reserved1[3];
+} mec_options_t;
+
+/* Fills *opt with defaults (AUTO path, T = 100, epilogue fix, pool workspace). */
+void mec_options_init(mec_options_t* opt);
+
+/* Eq. (1), P:43 with floor (reading Q1).  MEC_ERR_INVALID_ARG on a
+ * bad shape or NULL output pointer. */
+mec_status_t mec_out_dims(const mec_shape_t* s, int s_h, int s_w, int64_t* o_h,
+                          int64_t* o_w);
+
+/* Alg.2 l.8: MEC_PATH_SOLUTION_A iff o_w <= T and
+ * #O <= #L, else MEC_PATH_SOLUTION_B.  T <= 0 means 100.  Host-only; returns
+ * MEC_PATH_AUTO (0) for an invalid shape. */
+mec_path_t mec_select_path(const mec_shape_t* s, int s_h, int s_w, int T);
+
+/* Closed-form element counts: #L_MEC = i_n o_w i_h k_w i_c (Table 1, Alg.2
+ * l.2), #L_im2col = i_n o_h o_w k_h k_w i_c (Eq. 2 with i_c, reading Q2).
+ * Return -1 for an invalid shape. */
+int64_t mec_lowered_elems(const mec_shape_t* s, int s_h, int s_w);
+int64_t mec_im2col_elems(const mec_shape_t* s, int s_h, int s_w);
+
+/* Bytes of device workspace mec_conv_forward_ex needs for this problem:
+ * the pitch-padded lowered tensor L (i_n o_w rows of i_h k_w i_c elements,
+ * row pitch rounded up to 16 B), the prepared weight operand and alignment
+ * slack.  Never an im2col-sized buffer.  0 for an invalid shape/dtype. */
+size_t mec_workspace_bytes(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt);
+
+/* Compact lowering, Alg.2 l.3-6:
+ *   L[n, w, h, 0:k_w, 0:i_c] = I[n, h, s_w w : s_w w + k_w, 0:i_c]
+ * for all n < i_n, w < o_w, h < i_h (every input row, reading Q5).  L is the
+ * DENSE paper layout (#L = i_n o_w i_h k_w i_c elements), a bit-exact copy of
+ * I's elements.  Only the element size of dt matters (2 B bf16, 4 B tf32).
+ * I and L need 16-byte alignment. */
+mec_status_t mec_lower(const void* I, void* L, const mec_shape_t* s, int s_h,
+                       int s_w, mec_dtype_t dt, void* stream);
+
+/* O = MEC(I, K, s) (Algorithm 2): lowering, then the window GEMMs
+ * of the path picked by Alg.2 l.8 with T = 100, then (Solution A) the format
+ * fix, all on `stream`.  O receives i_n x o_h x o_w x k_c in n-h-w-c.  L is
+ * taken from a stream-ordered pool (Alg.2 l.2 allocates L inside MEC). */
+mec_status_t mec_conv_forward(const void* I, const void* K, void* O,
+                              const mec_shape_t* s, int s_h, int s_w,
+                              mec_dtype_t dt, void* stream);
+
+/* As mec_conv_forward, with a forced path / threshold / Solution-A format fix
+ * / caller workspace / stage events (opt may be NULL = defaults). */
+mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O,
+                                 const mec_shape_t* s, int s_h, int s_w,
+                                 mec_dtype_t dt, void* stream,
+                                 mec_options_t* opt);
+
+/* Number of kernel launches the last successful conv / lower call on this
+ * thread enqueued (for the bench's gpu_launches count). */
+int mec_last_launch_count(void);
+
+const char* mec_status_string(mec_status_t st);
+const char* mec_last_error_message(void);
+int mec_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEC_H */

@@ -1,0 +1,329 @@
+// mec_api.cu -- the C ABI of libmec.so (include/mec.h): argument validation,
+// the host plan (Eq.1, Alg.2 l.8, buffer layout), the stream-ordered
+// workspace pool, and the launch sequence of one MEC call:
+//   lower(+weight prep) -> window GEMMs -> [Solution A literal format fix].
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/mec.h"
+#include "mec_internal.h"
+#include "tma_host.h"
+
+namespace mec {
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+mec_status_t cuda_fail(cudaError_t e, const char* where) {
+  snprintf(g_err, sizeof(g_err), "%s: %s (%s)", where, cudaGetErrorName(e),
+           cudaGetErrorString(e));
+  return MEC_ERR_CUDA;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+// One library-owned stream-ordered memory pool per device, with an infinite
+// release threshold so repeated calls reuse the same L workspace.
+constexpr int kMaxDevices = 64;
+cudaMemPool_t g_pools[kMaxDevices] = {};
+std::mutex g_pool_mu;
+
+cudaError_t get_pool(cudaMemPool_t* out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pools[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    e = cudaMemPoolCreate(&g_pools[dev], &props);
+    if (e != cudaSuccess) return e;
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(g_pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = g_pools[dev];
+  return cudaSuccess;
+}
+
+}  // namespace
+
+int num_sms() {
+  static int cached[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  if (cached[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+cudaError_t encode_tiled(CUtensorMap* map, bool tf32, int rank, const void* base,
+                         const uint64_t* dims, const uint64_t* strides_bytes,
+                         const uint32_t* box) {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+  });
+  if (!g_encode) return cudaErrorNotSupported;
+  cuuint64_t d[5];
+  cuuint64_t s[4];
+  cuuint32_t b[5];
+  cuuint32_t es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    es[i] = 1;
+    if (i < rank - 1) s[i] = strides_bytes[i];
+  }
+  CUresult r = g_encode(map, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                        rank, const_cast<void*>(base), d, s, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, Plan* p) {
+  if (!s || !p) return MEC_ERR_INVALID_ARG;
+  if (s->i_n < 1 || s->i_h < 1 || s->i_w < 1 || s->i_c < 1 || s->k_h < 1 || s->k_w < 1 ||
+      s->k_c < 1 || s_h < 1 || s_w < 1 || s->i_h < s->k_h || s->i_w < s->k_w)
+    return MEC_ERR_INVALID_ARG;
+  if (dt != MEC_DTYPE_BF16 && dt != MEC_DTYPE_TF32) return MEC_ERR_INVALID_ARG;
+  std::memset(p, 0, sizeof(*p));
+  p->s = *s;
+  p->s_h = s_h;
+  p->s_w = s_w;
+  p->dt = dt;
+  p->elt = dt == MEC_DTYPE_BF16 ? 2 : 4;
+  p->o_h = (s->i_h - s->k_h) / s_h + 1;  // Eq. (1), floor
+  p->o_w = (s->i_w - s->k_w) / s_w + 1;
+  p->l_cols = s->i_h * s->k_w * s->i_c;
+  p->pitch = round_up(p->l_cols, 16 / p->elt);
+  p->kdim = s->k_h * s->k_w * s->i_c;
+  p->shift = static_cast<int64_t>(s_h) * s->k_w * s->i_c;
+  p->bk = kTileKBytes / p->elt;
+  p->kdim_pad = round_up(p->kdim, p->bk);
+  p->n_tiles_n = static_cast<int>((s->k_c + 255) / 256);
+  p->bn = static_cast<int>(round_up((s->k_c + p->n_tiles_n - 1) / p->n_tiles_n, 16));
+  p->kc_pad = static_cast<int64_t>(p->n_tiles_n) * p->bn;
+  p->n_L = s->i_n * p->o_w * s->i_h * s->k_w * s->i_c;
+  p->n_O = s->i_n * p->o_h * p->o_w * s->k_c;
+  p->bytes_L_pitched = static_cast<size_t>(s->i_n * p->o_w * p->pitch) * p->elt;
+  p->off_kt = static_cast<size_t>(round_up(static_cast<int64_t>(p->bytes_L_pitched), 1024));
+  p->bytes_kt = static_cast<size_t>(p->kc_pad * p->kdim_pad) * p->elt;
+  p->ws_bytes = p->off_kt + p->bytes_kt + 1024;
+  // TMA coordinate / extent limits (int32 coordinates, dims <= 2^32)
+  if (p->l_cols + p->kdim_pad >= (1LL << 31) || s->i_n * p->o_w >= (1LL << 31) ||
+      p->kdim_pad >= (1LL << 31))
+    return MEC_ERR_INVALID_ARG;
+  return MEC_OK;
+}
+
+}  // namespace mec
+
+using mec::Plan;
+
+extern "C" {
+
+void mec_options_init(mec_options_t* opt) {
+  if (!opt) return;
+  std::memset(opt, 0, sizeof(*opt));
+  opt->path = MEC_PATH_AUTO;
+  opt->T = MEC_DEFAULT_T;
+  opt->sola_fix = MEC_SOLA_FIX_EPILOGUE;
+}
+
+int mec_abi_version(void) { return MEC_ABI_VERSION; }
+
+const char* mec_status_string(mec_status_t st) {
+  switch (st) {
+    case MEC_OK: return "MEC_OK";
+    case MEC_ERR_INVALID_ARG: return "MEC_ERR_INVALID_ARG";
+    case MEC_ERR_UNSUPPORTED: return "MEC_ERR_UNSUPPORTED";
+    case MEC_ERR_MISALIGNED: return "MEC_ERR_MISALIGNED";
+    case MEC_ERR_CUDA: return "MEC_ERR_CUDA";
+    case MEC_ERR_NO_MEMORY: return "MEC_ERR_NO_MEMORY";
+  }
+  return "MEC_ERR_UNKNOWN";
+}
+
+const char* mec_last_error_message(void) { return mec::g_err; }
+
+int mec_last_launch_count(void) { return mec::g_launches; }
+
+mec_status_t mec_out_dims(const mec_shape_t* s, int s_h, int s_w, int64_t* o_h, int64_t* o_w) {
+  Plan p;
+  if (!o_h || !o_w) return MEC_ERR_INVALID_ARG;
+  mec_status_t st = mec::make_plan(s, s_h, s_w, MEC_DTYPE_BF16, &p);
+  if (st != MEC_OK) return st;
+  *o_h = p.o_h;
+  *o_w = p.o_w;
+  return MEC_OK;
+}
+
+mec_path_t mec_select_path(const mec_shape_t* s, int s_h, int s_w, int T) {
+  Plan p;
+  if (mec::make_plan(s, s_h, s_w, MEC_DTYPE_BF16, &p) != MEC_OK) return MEC_PATH_AUTO;
+  if (T <= 0) T = MEC_DEFAULT_T;
+  // Alg.2 l.8: "if o_w <= T and |O| <= |L|"
+  return (p.o_w <= T && p.n_O <= p.n_L) ? MEC_PATH_SOLUTION_A : MEC_PATH_SOLUTION_B;
+}
+
+int64_t mec_lowered_elems(const mec_shape_t* s, int s_h, int s_w) {
+  Plan p;
+  if (mec::make_plan(s, s_h, s_w, MEC_DTYPE_BF16, &p) != MEC_OK) return -1;
+  return p.n_L;
+}
+
+int64_t mec_im2col_elems(const mec_shape_t* s, int s_h, int s_w) {
+  Plan p;
+  if (mec::make_plan(s, s_h, s_w, MEC_DTYPE_BF16, &p) != MEC_OK) return -1;
+  return s->i_n * p.o_h * p.o_w * s->k_h * s->k_w * s->i_c;
+}
+
+size_t mec_workspace_bytes(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt) {
+  Plan p;
+  if (mec::make_plan(s, s_h, s_w, dt, &p) != MEC_OK) return 0;
+  return p.ws_bytes;
+}
+
+mec_status_t mec_lower(const void* I, void* L, const mec_shape_t* s, int s_h, int s_w,
+                       mec_dtype_t dt, void* stream) {
+  Plan p;
+  mec_status_t st = mec::make_plan(s, s_h, s_w, dt, &p);
+  if (st != MEC_OK) return st;
+  if (!I || !L) return MEC_ERR_INVALID_ARG;
+  if (!mec::aligned16(I) || !mec::aligned16(L)) return MEC_ERR_MISALIGNED;
+  int launches = 0;
+  cudaError_t e = mec::launch_lower(p, I, L, p.l_cols, nullptr, nullptr,
+                                    static_cast<cudaStream_t>(stream), &launches);
+  if (e != cudaSuccess) return mec::cuda_fail(e, "mec_lower");
+  mec::g_launches = launches;
+  return MEC_OK;
+}
+
+mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const mec_shape_t* s,
+                                 int s_h, int s_w, mec_dtype_t dt, void* stream,
+                                 mec_options_t* opt) {
+  mec_options_t def;
+  if (!opt) {
+    mec_options_init(&def);
+    opt = &def;
+  }
+  Plan p;
+  mec_status_t st = mec::make_plan(s, s_h, s_w, dt, &p);
+  if (st != MEC_OK) return st;
+  if (!I || !K || !O) return MEC_ERR_INVALID_ARG;
+  if (!mec::aligned16(I) || !mec::aligned16(K) || !mec::aligned16(O)) return MEC_ERR_MISALIGNED;
+  if (opt->path < MEC_PATH_AUTO || opt->path > MEC_PATH_FUSED) return MEC_ERR_INVALID_ARG;
+  if (opt->sola_fix < MEC_SOLA_FIX_EPILOGUE || opt->sola_fix > MEC_SOLA_FIX_NONE)
+    return MEC_ERR_INVALID_ARG;
+  const int T = opt->T > 0 ? opt->T : MEC_DEFAULT_T;
+  int path = opt->path;
+  if (path == MEC_PATH_AUTO) path = mec_select_path(s, s_h, s_w, T);
+  if (path == MEC_PATH_FUSED) return MEC_ERR_UNSUPPORTED;
+  // Solution A's literal format fix repurposes L as auxiliary space,
+  // which requires |L| >= |O|.
+  if (path == MEC_PATH_SOLUTION_A && opt->sola_fix == MEC_SOLA_FIX_LITERAL && p.n_O > p.n_L)
+    return MEC_ERR_UNSUPPORTED;
+
+  cudaStream_t stream_ = static_cast<cudaStream_t>(stream);
+  void* ws = opt->workspace;
+  bool pooled = false;
+  if (ws) {
+    if (!mec::aligned16(ws)) return MEC_ERR_MISALIGNED;
+    if (opt->workspace_bytes < p.ws_bytes) return MEC_ERR_NO_MEMORY;
+  } else {
+    cudaMemPool_t pool;
+    cudaError_t e = mec::get_pool(&pool);
+    if (e != cudaSuccess) return mec::cuda_fail(e, "mec pool");
+    e = cudaMallocFromPoolAsync(&ws, p.ws_bytes, pool, stream_);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      snprintf(mec::g_err, sizeof(mec::g_err), "workspace allocation of %zu bytes failed",
+               p.ws_bytes);
+      return MEC_ERR_NO_MEMORY;
+    }
+    pooled = true;
+  }
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(ws) + 1023) & ~static_cast<uintptr_t>(1023));
+  void* L = base;
+  void* Kt = base + p.off_kt;
+
+  auto rec = [&](int i) {
+    if (opt->stage_events[i]) cudaEventRecord(static_cast<cudaEvent_t>(opt->stage_events[i]), stream_);
+  };
+  int launches = 0;
+  cudaError_t e = cudaSuccess;
+  rec(0);
+  // Alg.2 l.2-7: lowering into the pitch-padded L, and K as a (k_h k_w i_c) x k_c matrix
+  e = mec::launch_lower(p, I, L, p.pitch, K, Kt, stream_, &launches);
+  if (e != cudaSuccess) goto fail;
+  rec(1);
+  {
+    mec::GemmArgs ga{};
+    ga.L = L;
+    ga.Kt = Kt;
+    ga.O = O;
+    if (path == MEC_PATH_SOLUTION_A) {  // l.9: L as (i_n o_w) x (i_h k_w i_c)
+      ga.groups = 1;
+      ga.rows = s->i_n * p.o_w;
+      ga.out_hnwc = opt->sola_fix != MEC_SOLA_FIX_EPILOGUE;
+    } else {  // l.21: L as i_n matrices of o_w x (i_h k_w i_c)
+      ga.groups = s->i_n;
+      ga.rows = p.o_w;
+      ga.out_hnwc = false;
+    }
+    e = mec::launch_window_gemm(p, ga, stream_, &launches);
+    if (e != cudaSuccess) goto fail;
+  }
+  rec(2);
+  if (path == MEC_PATH_SOLUTION_A && opt->sola_fix == MEC_SOLA_FIX_LITERAL) {
+    e = mec::launch_sola_copy(p, O, L, stream_, &launches);  // l.13 Copy L = O
+    if (e != cudaSuccess) goto fail;
+    e = mec::launch_sola_transpose(p, L, O, stream_, &launches);  // l.14-19
+    if (e != cudaSuccess) goto fail;
+  }
+  rec(3);
+  if (pooled) cudaFreeAsync(ws, stream_);
+  opt->selected_path = path;
+  mec::g_launches = launches;
+  return MEC_OK;
+fail:
+  if (pooled) cudaFreeAsync(ws, stream_);
+  return mec::cuda_fail(e, "mec_conv_forward");
+}
+
+mec_status_t mec_conv_forward(const void* I, const void* K, void* O, const mec_shape_t* s,
+                              int s_h, int s_w, mec_dtype_t dt, void* stream) {
+  return mec_conv_forward_ex(I, K, O, s, s_h, s_w, dt, stream, nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// mec_internal.h -- host-side plan of one MEC call and the kernel launchers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/mec.h"
+
+namespace mec {
+
+constexpr int kBM = 128;           // UMMA_M (rows of a window tile; cta_group::1)
+constexpr int kTileKBytes = 128;   // one K-tile row = one 128-byte swizzle row
+constexpr int kSmemAlign = 1024;   // SWIZZLE_128B atoms need 1024-byte alignment
+
+// Everything derived from (shape, strides, dtype, path) -- Eq.1, the T rule
+// of Alg.2 l.8, the window geometry of Alg.2 l.9-12 / l.21-25 and the device
+// buffer layout.  Plain host arithmetic.
+struct Plan {
+  mec_shape_t s;
+  int s_h, s_w;
+  mec_dtype_t dt;
+  int elt;               // bytes per element (2 bf16, 4 tf32/fp32)
+  int64_t o_h, o_w;      // Eq. (1)
+  int64_t l_cols;        // i_h k_w i_c: one row of L (Alg.2 l.9 / l.21 "i_h k_w i_c")
+  int64_t pitch;         // l_cols rounded up to 16 B (TMA stride rule), elements
+  int64_t kdim;          // k_h k_w i_c: GEMM reduction length
+  int64_t shift;         // s_h k_w i_c: column offset between output rows
+  int bk;                // K-tile in elements (128 B / elt)
+  int64_t kdim_pad;      // kdim rounded up to bk
+  int n_tiles_n;         // ceil(k_c / 256)
+  int bn;                // N tile (multiple of 16, <= 256)
+  int64_t kc_pad;        // n_tiles_n * bn
+  int64_t n_L, n_O;      // #L (dense) and #O, elements
+  size_t bytes_L_pitched;  // i_n o_w pitch elt
+  size_t off_kt;           // workspace offset of the prepared weight operand
+  size_t bytes_kt;         // kc_pad kdim_pad elt
+  size_t ws_bytes;         // total workspace (incl. alignment slack)
+};
+
+// Returns MEC_OK and fills *p, or MEC_ERR_INVALID_ARG.
+mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, Plan* p);
+
+// ---- kernels (each returns cudaGetLastError() of its launch) ----
+
+// Lowering (Alg.2 l.3-6) into L with row pitch `pitch` elements; optionally,
+// in the same launch, the weight operand Kt[kc_pad][kdim_pad] = K_mat^T,
+// zero padded (Alg.2 l.7).  Kt may be null (mec_lower).
+cudaError_t launch_lower(const Plan& p, const void* I, void* L, int64_t pitch, const void* K,
+                         void* Kt, cudaStream_t st, int* launches);
+
+// Window GEMMs (Alg.2 l.10-12 or l.23-25) on tcgen05.  `groups` x `rows`
+// is the row tiling: Solution A = 1 x (i_n o_w), Solution B = i_n x o_w.
+// out_hnwc: store O in h-n-w-c (Alg.2 l.10's "O as o_h x i_n o_w k_c")
+// instead of n-h-w-c.
+struct GemmArgs {
+  const void* L;
+  const void* Kt;
+  void* O;
+  int64_t groups, rows;
+  bool out_hnwc;
+};
+cudaError_t launch_window_gemm(const Plan& p, const GemmArgs& a, cudaStream_t st, int* launches);
+
+// Solution A format fix, paper-literal (Alg.2 l.13-19): "Copy L = O" and the
+// block transpose O[n,h,:] = L[h,n,:].
+cudaError_t launch_sola_copy(const Plan& p, const void* O, void* Laux, cudaStream_t st,
+                             int* launches);
+cudaError_t launch_sola_transpose(const Plan& p, const void* Laux, void* O, cudaStream_t st,
+                                  int* launches);
+
+int num_sms();
+
+}  // namespace mec

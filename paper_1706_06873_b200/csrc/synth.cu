@@ -1,0 +1,82 @@
+// synth.cu -- device evaluation of the counter-based synthetic input
+// generator (bench / test helper; not part of the MEC method).  Same formula
+// as the host generator synth/__init__.py (see include/mec_synth.h); a GPU
+// test checks the two bit for bit.  Also the L2-flush helper of the bench.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/mec_synth.h"
+#include "mec_internal.h"
+
+namespace mec {
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float synth_value(uint64_t z, int kind) {
+  if (kind == MEC_SYNTH_GRID8) return static_cast<float>(static_cast<int8_t>(z >> 56)) / 128.0f;
+  if (kind == MEC_SYNTH_GRID11)
+    return static_cast<float>(static_cast<int64_t>(z >> 53) - 1024) / 1024.0f;
+  return static_cast<float>(static_cast<int64_t>(z >> 40) - (1ll << 23)) / 8388608.0f;
+}
+
+template <typename T>
+__global__ void synth_kernel(T* dst, int64_t count, uint64_t seed, int tensor_id,
+                             uint64_t offset, int kind) {
+  const uint64_t base = seed ^ (static_cast<uint64_t>(tensor_id) << 56);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += stride) {
+    const float v = synth_value(splitmix64(base ^ (offset + static_cast<uint64_t>(i))), kind);
+    if constexpr (sizeof(T) == 2)
+      dst[i] = __float2bfloat16_rn(v);
+    else
+      dst[i] = v;
+  }
+}
+
+__global__ void flush_kernel(uint4* dst, int64_t n16, uint32_t salt) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += stride)
+    dst[i] = make_uint4(salt, static_cast<uint32_t>(i), salt, 0u);
+}
+
+}  // namespace
+}  // namespace mec
+
+extern "C" mec_status_t mec_synth_fill(void* dst, int64_t count, uint64_t seed, int tensor_id,
+                                       uint64_t index_offset, int kind, mec_dtype_t out_dtype,
+                                       void* stream) {
+  if (dst == nullptr || count < 0 || kind < 0 || kind > 2 ||
+      (out_dtype != MEC_DTYPE_BF16 && out_dtype != MEC_DTYPE_TF32))
+    return MEC_ERR_INVALID_ARG;
+  if (count == 0) return MEC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t grid = std::min<int64_t>((count + 255) / 256, 16LL * mec::num_sms());
+  if (out_dtype == MEC_DTYPE_BF16)
+    mec::synth_kernel<__nv_bfloat16><<<static_cast<unsigned>(grid), 256, 0, st>>>(
+        static_cast<__nv_bfloat16*>(dst), count, seed, tensor_id, index_offset, kind);
+  else
+    mec::synth_kernel<float><<<static_cast<unsigned>(grid), 256, 0, st>>>(
+        static_cast<float*>(dst), count, seed, tensor_id, index_offset, kind);
+  return cudaGetLastError() == cudaSuccess ? MEC_OK : MEC_ERR_CUDA;
+}
+
+extern "C" mec_status_t mec_l2_flush(void* scratch, size_t bytes, void* stream) {
+  static uint32_t salt = 1;
+  if (scratch == nullptr) return MEC_ERR_INVALID_ARG;
+  const int64_t n16 = static_cast<int64_t>(bytes / 16);
+  if (n16 == 0) return MEC_OK;
+  const int64_t grid = std::min<int64_t>((n16 + 255) / 256, 8LL * mec::num_sms());
+  mec::flush_kernel<<<static_cast<unsigned>(grid), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint4*>(scratch), n16, salt++);
+  return cudaGetLastError() == cudaSuccess ? MEC_OK : MEC_ERR_CUDA;
+}

@@ -1,0 +1,19 @@
+// tma_host.h -- host-side TMA tensor-map encoding through the driver entry
+// point (no link-time dependency on libcuda; the runtime resolves it).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mec {
+
+// Tiled tensor map, 128-byte swizzle, zero OOB fill, 256-byte L2 promotion.
+// Element type BFLOAT16 (tf32 == false) or FLOAT32 (tf32 == true; the tensor
+// core reads fp32 storage as tf32).  Returns cudaErrorInvalidValue if the
+// driver rejects the parameters.
+cudaError_t encode_tiled(CUtensorMap* map, bool tf32, int rank, const void* base,
+                         const uint64_t* dims, const uint64_t* strides_bytes,
+                         const uint32_t* box);
+
+}  // namespace mec

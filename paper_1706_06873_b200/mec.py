@@ -1,0 +1,143 @@
+"""Python binding of the MEC C ABI (include/mec.h) -- argument marshalling only.
+
+Every step of the computation runs in libmec.so's CUDA kernels on the
+caller's current torch CUDA stream.  torch supplies device memory and the
+stream; nothing here computes.  Inputs must be CUDA tensors: there is no CPU
+fallback, and a missing library raises.
+
+Layouts follow the paper's Table 1: I (i_n, i_h, i_w, i_c) NHWC,
+K (k_h, k_w, i_c, k_c), O (i_n, o_h, o_w, k_c), L (i_n, o_w, i_h, k_w, i_c).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import (MEC_DTYPE_BF16, MEC_DTYPE_TF32, MEC_PATH_AUTO, MEC_PATH_FUSED,  # noqa: F401
+                   MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B, MEC_SOLA_FIX_EPILOGUE,
+                   MEC_SOLA_FIX_LITERAL, MEC_SOLA_FIX_NONE, MEC_DEFAULT_T, MecError)
+
+PATH_NAMES = {MEC_PATH_SOLUTION_A: "solution_A_batch_folded", MEC_PATH_SOLUTION_B: "solution_B_per_image",
+              MEC_PATH_FUSED: "fused"}
+
+
+def _shape(i_n, i_h, i_w, i_c, k_h, k_w, k_c) -> _lib.MecShape:
+    return _lib.MecShape(int(i_n), int(i_h), int(i_w), int(i_c), int(k_h), int(k_w), int(k_c))
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.bfloat16:
+        return MEC_DTYPE_BF16
+    if dt == torch.float32:
+        return MEC_DTYPE_TF32
+    raise TypeError(f"MEC supports bfloat16 and float32 (tf32 math), got {dt}")
+
+
+def _stream(t: torch.Tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _cuda(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (MEC has no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def out_dims(i_h, i_w, k_h, k_w, s_h, s_w):
+    """Eq. (1), P:43 (floor)."""
+    oh, ow = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.lib().mec_out_dims(ctypes.byref(_shape(1, i_h, i_w, 1, k_h, k_w, 1)), s_h, s_w,
+                                       ctypes.byref(oh), ctypes.byref(ow)), "mec_out_dims")
+    return oh.value, ow.value
+
+
+def select_path(shape, s_h, s_w, T: int = MEC_DEFAULT_T) -> int:
+    """Alg.2 l.8: MEC_PATH_SOLUTION_A or MEC_PATH_SOLUTION_B.  shape = 7-tuple."""
+    r = _lib.lib().mec_select_path(ctypes.byref(_shape(*shape)), s_h, s_w, T)
+    if r == MEC_PATH_AUTO:
+        raise ValueError("invalid shape")
+    return r
+
+
+def lowered_elems(shape, s_h, s_w) -> int:
+    return _lib.lib().mec_lowered_elems(ctypes.byref(_shape(*shape)), s_h, s_w)
+
+
+def im2col_elems(shape, s_h, s_w) -> int:
+    return _lib.lib().mec_im2col_elems(ctypes.byref(_shape(*shape)), s_h, s_w)
+
+
+def workspace_bytes(shape, s_h, s_w, dtype: torch.dtype) -> int:
+    return _lib.lib().mec_workspace_bytes(ctypes.byref(_shape(*shape)), s_h, s_w, dtype_code(dtype))
+
+
+def lower(I: torch.Tensor, k_h: int, k_w: int, s_h: int, s_w: int, out: torch.Tensor | None = None):
+    """mec_lower: L = compact lowering of I (Alg.2 l.3-6), dense (i_n, o_w, i_h, k_w, i_c)."""
+    _cuda(I, "I")
+    i_n, i_h, i_w, i_c = I.shape
+    o_h, o_w = out_dims(i_h, i_w, k_h, k_w, s_h, s_w)
+    if out is None:
+        out = torch.empty((i_n, o_w, i_h, k_w, i_c), dtype=I.dtype, device=I.device)
+    _cuda(out, "L")
+    assert out.dtype == I.dtype and out.numel() == i_n * o_w * i_h * k_w * i_c
+    _lib.check(_lib.lib().mec_lower(I.data_ptr(), out.data_ptr(),
+                                    ctypes.byref(_shape(i_n, i_h, i_w, i_c, k_h, k_w, 1)),
+                                    s_h, s_w, dtype_code(I.dtype), _stream(I)), "mec_lower")
+    return out
+
+
+def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torch.Tensor | None = None,
+                 path: int = MEC_PATH_AUTO, T: int = MEC_DEFAULT_T, sola_fix: int = MEC_SOLA_FIX_EPILOGUE,
+                 workspace: torch.Tensor | None = None, stage_events=None, return_path: bool = False):
+    """mec_conv_forward_ex: O = MEC(I, K, s) (Algorithm 2), O in n-h-w-c
+    (or h-n-w-c with sola_fix=MEC_SOLA_FIX_NONE when Solution A runs)."""
+    _cuda(I, "I")
+    _cuda(K, "K")
+    if K.dtype != I.dtype:
+        raise TypeError("I and K must have the same dtype")
+    i_n, i_h, i_w, i_c = I.shape
+    k_h, k_w, k_ci, k_c = K.shape
+    if k_ci != i_c:
+        raise ValueError("K's third extent must equal i_c (Table 1)")
+    o_h, o_w = out_dims(i_h, i_w, k_h, k_w, s_h, s_w)
+    if out is None:
+        out = torch.empty((i_n, o_h, o_w, k_c), dtype=I.dtype, device=I.device)
+    _cuda(out, "O")
+    assert out.dtype == I.dtype and out.numel() == i_n * o_h * o_w * k_c
+    opt = _lib.MecOptions()
+    _lib.lib().mec_options_init(ctypes.byref(opt))
+    opt.path, opt.T, opt.sola_fix = int(path), int(T), int(sola_fix)
+    if workspace is not None:
+        _cuda(workspace, "workspace")
+        opt.workspace = workspace.data_ptr()
+        opt.workspace_bytes = workspace.numel() * workspace.element_size()
+    if stage_events is not None:
+        for i, ev in enumerate(stage_events[:4]):
+            opt.stage_events[i] = ev.cuda_event if ev is not None else None
+    st = _lib.lib().mec_conv_forward_ex(I.data_ptr(), K.data_ptr(), out.data_ptr(),
+                                        ctypes.byref(_shape(i_n, i_h, i_w, i_c, k_h, k_w, k_c)),
+                                        s_h, s_w, dtype_code(I.dtype), _stream(I), ctypes.byref(opt))
+    _lib.check(st, "mec_conv_forward")
+    return (out, opt.selected_path) if return_path else out
+
+
+def last_launch_count() -> int:
+    return _lib.lib().mec_last_launch_count()
+
+
+def synth_fill(t: torch.Tensor, seed: int, tensor_id: int, kind: int, index_offset: int = 0) -> torch.Tensor:
+    """Device-side counter-based generator (include/mec_synth.h) into tensor t."""
+    _cuda(t, "t")
+    _lib.check(_lib.lib().mec_synth_fill(t.data_ptr(), t.numel(), seed, tensor_id, index_offset, kind,
+                                         dtype_code(t.dtype), _stream(t)), "mec_synth_fill")
+    return t
+
+
+def l2_flush(scratch: torch.Tensor) -> None:
+    _cuda(scratch, "scratch")
+    _lib.check(_lib.lib().mec_l2_flush(scratch.data_ptr(), scratch.numel() * scratch.element_size(),
+                                       _stream(scratch)), "mec_l2_flush")

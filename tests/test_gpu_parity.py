@@ -1,0 +1,263 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Inputs come from the counter-based generator (synth/), evaluated on the host
+for the oracle and uploaded for the GPU, so both sides see identical values.
+Bars (BASELINE.json north_star):
+  L                : bit-exact
+  O, bf16          : max|O - O_ref| <= 2e-2 * max|O_ref|
+  O, fp32 / tf32   : max|O - O_ref| <= 1e-3 * sqrt(k_h k_w i_c) * max|O_ref|
+On the GRID kinds the inputs are exact in bf16 / tf32, so the GPU's only
+error is fp32 accumulation order (+ the bf16 rounding of O); the tests also
+check that much tighter bound.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_1706_06873_b200 import mec
+from paper_1706_06873_b200._lib import (MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B, MEC_SOLA_FIX_EPILOGUE,
+                                        MEC_SOLA_FIX_LITERAL, MEC_SOLA_FIX_NONE, MecError)
+
+pytestmark = pytest.mark.gpu
+
+TDT = {"bf16": torch.bfloat16, "tf32": torch.float32, "fp32": torch.float32}
+
+
+def make_inputs(shape, dtype, seed, kind=None, n_begin=0):
+    i_n, i_h, i_w, i_c, k_h, k_w, k_c = shape
+    if kind is None:
+        kind = synth.KIND_GRID8 if dtype == "bf16" else synth.KIND_GRID11
+    cfg = dict(i_h=i_h, i_w=i_w, i_c=i_c, k_h=k_h, k_w=k_w, k_c=k_c)
+    I = synth.input_images(cfg, n_begin, i_n, kind, seed)
+    K = synth.kernel_tensor(cfg, kind, seed)
+    return I, K
+
+
+def to_dev(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda").to(TDT[dtype])
+
+
+def tol(dtype, kdim, ref):
+    m = float(np.abs(ref).max()) if ref.size else 0.0
+    return (2e-2 if dtype == "bf16" else 1e-3 * math.sqrt(kdim)) * max(m, 1e-30)
+
+
+def check_O(O_gpu, ref, dtype, kdim, tight=True):
+    got = O_gpu.float().cpu().numpy().astype(np.float64)
+    assert got.shape == ref.shape
+    err = float(np.abs(got - ref).max())
+    bar = tol(dtype, kdim, ref)
+    assert err <= bar, f"max abs err {err} > {bar}"
+    if tight:
+        # exact-grid inputs: fp32 accumulation error << bar; bf16 adds one rounding of O
+        m = float(np.abs(ref).max())
+        tight_bar = (2.0 ** -8 if dtype == "bf16" else 1e-5) * m + 1e-6
+        assert err <= tight_bar, f"max abs err {err} > tight {tight_bar}"
+    return err
+
+
+SMALL = [
+    # (i_n, i_h, i_w, i_c, k_h, k_w, k_c), s_h, s_w
+    ((1, 7, 7, 1, 3, 3, 1), 1, 1),        # C0 shapes
+    ((2, 9, 11, 3, 3, 5, 8), 1, 2),       # tiny, k_c 8
+    ((3, 20, 17, 5, 4, 3, 24), 2, 1),     # k_c not multiple of 16, non-divisible stride
+    ((2, 30, 30, 16, 3, 3, 40), 1, 1),
+    ((4, 16, 40, 8, 5, 5, 64), 3, 2),     # s_h does not divide i_h - k_h
+    ((2, 12, 12, 7, 2, 2, 17), 3, 3),     # s > k (unused input rows, reading Q5)
+    ((1, 60, 70, 4, 1, 1, 32), 1, 1),     # 1x1
+    ((2, 8, 9, 6, 8, 9, 48), 1, 1),       # k == i: o = 1
+]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("case", range(len(SMALL)))
+def test_small_shapes_both_solutions(cuda_ok, case, dtype):
+    shape, s_h, s_w = SMALL[case]
+    I, K = make_inputs(shape, dtype, seed=1000 + case)
+    ref = oracle.direct_conv(I, K, s_h, s_w)
+    kdim = shape[4] * shape[5] * shape[3]
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    outs = {}
+    for path in (MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B):
+        O = mec.conv_forward(Id, Kd, s_h, s_w, path=path)
+        torch.cuda.synchronize()
+        check_O(O, ref, dtype, kdim)
+        outs[path] = O
+    # Both solutions share the mainloop: identical arithmetic per output element
+    assert torch.equal(outs[MEC_PATH_SOLUTION_A], outs[MEC_PATH_SOLUTION_B])
+
+
+def test_worked_example_ramp_exact(cuda_ok):
+    # C0 (Fig. 1/2): ramp I[h,w] = 7h+w, K = ones -> O = 9(7h+w) + 72, exact in tf32/fp32
+    I = np.array([[7 * h + w for w in range(7)] for h in range(7)], dtype=np.float32).reshape(1, 7, 7, 1)
+    K = np.ones((3, 3, 1, 1), dtype=np.float32)
+    expect = np.array([[9 * (7 * h + w) + 72 for w in range(5)] for h in range(5)], dtype=np.float32)
+    for path in (0, MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B):
+        O, chosen = mec.conv_forward(to_dev(I, "tf32"), to_dev(K, "tf32"), 1, 1, path=path, return_path=True)
+        np.testing.assert_array_equal(O.cpu().numpy()[0, :, :, 0], expect)
+        assert chosen == (path or MEC_PATH_SOLUTION_A)  # Alg.2 l.8: o_w 5 <= 100, #O 25 <= #L 105
+    L = mec.lower(to_dev(I, "tf32"), 3, 3, 1, 1)
+    assert tuple(L.shape) == (1, 5, 7, 3, 1)  # 5 x 21
+    np.testing.assert_array_equal(L.cpu().numpy().reshape(5, 21)[1], I[0, :, 1:4, 0].reshape(-1))
+
+
+@pytest.mark.parametrize("fix", [MEC_SOLA_FIX_EPILOGUE, MEC_SOLA_FIX_LITERAL, MEC_SOLA_FIX_NONE])
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_solution_A_format_fix_modes(cuda_ok, fix, dtype):
+    shape, s = (5, 23, 21, 6, 3, 3, 24), 2
+    I, K = make_inputs(shape, dtype, seed=77)
+    ref = oracle.direct_conv(I, K, s, s)
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    O = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_SOLUTION_A, sola_fix=fix)
+    torch.cuda.synchronize()
+    if fix == MEC_SOLA_FIX_NONE:
+        # h-n-w-c, the direct extension's format
+        O = O.reshape(ref.shape[1], ref.shape[0], ref.shape[2], ref.shape[3]).permute(1, 0, 2, 3)
+    check_O(O, ref, dtype, 54)
+    base = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_SOLUTION_A)
+    if fix != MEC_SOLA_FIX_NONE:
+        assert torch.equal(O, base)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("name", ["cv1", "cv3", "cv5", "cv6", "cv9", "cv12", "cv7", "cv10"])
+def test_table2_layers_small_batch(cuda_ok, name, dtype):
+    """Every Table 2 layer shape at batch 2: spans many tiles, ragged M tails,
+    Kdim tails (363, 147, 27), k_c = 512 (two N tiles), i_c = 3 lowering."""
+    i_h, i_w, i_c, k_h, k_w, k_c, s = synth.TABLE2[name]
+    shape = (2, i_h, i_w, i_c, k_h, k_w, k_c)
+    I, K = make_inputs(shape, dtype, seed=2000 + int(name[2:]))
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    O_auto = mec.conv_forward(Id, Kd, s, s)
+    other = (MEC_PATH_SOLUTION_B if mec.select_path(shape, s, s) == MEC_PATH_SOLUTION_A
+             else MEC_PATH_SOLUTION_A)
+    O_other = mec.conv_forward(Id, Kd, s, s, path=other)
+    torch.cuda.synchronize()
+    check_O(O_auto, ref, dtype, k_h * k_w * i_c)
+    assert torch.equal(O_auto, O_other)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_full24_values_within_north_star_tolerance(cuda_ok, dtype):
+    # realistic (non-grid) fp32 values: tf32 / bf16 input rounding is now part of the error
+    shape, s = (2, 56, 56, 64, 3, 3, 64), 1
+    I, K = make_inputs(shape, "tf32", seed=5, kind=synth.KIND_FULL24)
+    ref_vals_I = I if dtype == "tf32" else torch.from_numpy(I).to(torch.bfloat16).float().numpy()
+    ref_vals_K = K if dtype == "tf32" else torch.from_numpy(K).to(torch.bfloat16).float().numpy()
+    ref = oracle.direct_conv(ref_vals_I, ref_vals_K, s, s, n_threads=8)
+    O = mec.conv_forward(to_dev(I, dtype), to_dev(K, dtype), s, s)
+    check_O(O, ref, dtype, 576, tight=False)
+
+
+# ------------------------------------------------------------------ lowering
+
+LOWER_CASES = [
+    ((2, 227, 227, 3, 11, 11, 1), 4, 4),   # cv1: 66-byte strips, unaligned segments
+    ((3, 56, 56, 64, 3, 3, 1), 1, 1),      # cv9: aligned fast path
+    ((2, 231, 231, 3, 11, 11, 1), 4, 4),   # cv2
+    ((2, 224, 224, 64, 7, 7, 1), 2, 2),    # cv4: unused last input row (Q5)
+    ((1, 7, 7, 1, 3, 3, 1), 1, 1),         # C0
+    ((2, 12, 12, 7, 2, 2, 1), 3, 3),       # s > k
+    ((2, 13, 9, 5, 1, 1, 1), 1, 1),        # 1x1
+]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("case", range(len(LOWER_CASES)))
+def test_lowering_bit_exact(cuda_ok, case, dtype):
+    shape, s_h, s_w = LOWER_CASES[case]
+    i_n, i_h, i_w, i_c, k_h, k_w, _ = shape
+    # arbitrary bit patterns (incl. NaN/Inf encodings): the lowering is a pure copy
+    rng = np.random.default_rng(case)
+    if dtype == "bf16":
+        bits = rng.integers(0, 2**16, (i_n, i_h, i_w, i_c), dtype=np.uint16)
+        Id = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.bfloat16)
+    else:
+        bits = rng.integers(0, 2**32, (i_n, i_h, i_w, i_c), dtype=np.uint32)
+        Id = torch.from_numpy(bits.view(np.int32)).cuda().view(torch.float32)
+    L = mec.lower(Id, k_h, k_w, s_h, s_w)
+    ref = oracle.lower(bits, k_h, k_w, s_h, s_w)
+    got = L.cpu().view(torch.int16 if dtype == "bf16" else torch.int32).numpy()
+    np.testing.assert_array_equal(got.view(ref.dtype), ref)
+
+
+def test_lowering_full_C1_batch_bit_exact(cuda_ok):
+    c = synth.config("C1")
+    I, _ = make_inputs((c["i_n"], c["i_h"], c["i_w"], c["i_c"], c["k_h"], c["k_w"], c["k_c"]), "bf16", seed=1)
+    Id = to_dev(I, "bf16")
+    L = mec.lower(Id, c["k_h"], c["k_w"], c["s_h"], c["s_w"])
+    bits = Id.view(torch.int16).cpu().numpy()
+    ref = oracle.lower(bits, c["k_h"], c["k_w"], c["s_h"], c["s_w"])
+    np.testing.assert_array_equal(L.view(torch.int16).cpu().numpy(), ref)
+
+
+# -------------------------------------------- BASELINE configs at full size
+
+def sampled_parity(cfg_name, dtype, images, path=0):
+    c = synth.config(cfg_name)
+    shape = (c["i_n"], c["i_h"], c["i_w"], c["i_c"], c["k_h"], c["k_w"], c["k_c"])
+    seed = synth.SEED_BASE + c["index"]
+    kind = synth.KIND_GRID8 if dtype == "bf16" else synth.KIND_GRID11
+    # the full batch generated on the device (bench's launch configuration) ...
+    Id = torch.empty(shape[:4], dtype=TDT[dtype], device="cuda")
+    Kd = torch.empty((c["k_h"], c["k_w"], c["i_c"], c["k_c"]), dtype=TDT[dtype], device="cuda")
+    mec.synth_fill(Id, seed, synth.TENSOR_I, kind)
+    mec.synth_fill(Kd, seed, synth.TENSOR_K, kind)
+    O = mec.conv_forward(Id, Kd, c["s_h"], c["s_w"], path=path)
+    torch.cuda.synchronize()
+    # ... and the sampled images regenerated on the host for the oracle
+    K = synth.kernel_tensor(c, kind, seed)
+    np.testing.assert_array_equal(Kd.float().cpu().numpy(), K)
+    for n in images:
+        I = synth.input_images(c, n, 1, kind, seed)
+        ref = oracle.direct_conv(I, K, c["s_h"], c["s_w"], n_threads=8)
+        check_O(O[n:n + 1], ref, dtype, c["k_h"] * c["k_w"] * c["i_c"])
+
+
+def test_C1_alexnet_conv1_full_batch_sampled(cuda_ok):
+    sampled_parity("C1", "bf16", [0, 17, 31])
+
+
+@pytest.mark.parametrize("path", [MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B])
+def test_C3_resnet50_stage2_full_batch_sampled(cuda_ok, path):
+    sampled_parity("C3", "bf16", [0, 128, 255], path=path)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_C2_vgg_conv1_2_full_batch_sampled(cuda_ok, dtype):
+    sampled_parity("C2" if dtype == "bf16" else "C2_tf32", dtype, [0, 63])
+
+
+# ------------------------------------------------------------- generator
+
+@pytest.mark.parametrize("kind", [synth.KIND_GRID8, synth.KIND_GRID11, synth.KIND_FULL24])
+def test_device_generator_matches_host(cuda_ok, kind):
+    t = torch.empty(100003, dtype=torch.float32, device="cuda")
+    mec.synth_fill(t, 12345, 1, kind, index_offset=777)
+    np.testing.assert_array_equal(t.cpu().numpy(), synth.draw(100003, 12345, 1, kind, 777))
+    if kind == synth.KIND_GRID8:
+        tb = torch.empty(1000, dtype=torch.bfloat16, device="cuda")
+        mec.synth_fill(tb, 12345, 1, kind, index_offset=777)
+        np.testing.assert_array_equal(tb.float().cpu().numpy(), synth.draw(1000, 12345, 1, kind, 777))
+
+
+# ---------------------------------------------------------------- errors
+
+def test_error_paths_on_device(cuda_ok):
+    I = torch.zeros(1, 7, 7, 1, device="cuda")
+    K = torch.zeros(3, 3, 1, 1, device="cuda")
+    with pytest.raises(MecError):  # misaligned I
+        mec.conv_forward(torch.zeros(50, device="cuda")[1:50].view(1, 7, 7, 1), K, 1, 1)
+    with pytest.raises(ValueError):  # i < k
+        mec.conv_forward(torch.zeros(1, 2, 7, 1, device="cuda"), K, 1, 1)
+    ws = torch.empty(mec.workspace_bytes((1, 7, 7, 1, 3, 3, 1), 1, 1, torch.float32), dtype=torch.uint8,
+                     device="cuda")
+    O = mec.conv_forward(I, K, 1, 1, workspace=ws)
+    assert float(O.abs().max()) == 0.0
+    with pytest.raises(MecError):
+        mec.conv_forward(I, K, 1, 1, workspace=ws[: ws.numel() // 2])
