@@ -44,21 +44,27 @@ struct LowerParams {
   const unsigned char* K;
   unsigned char* Kt;
   int64_t kdim, k_c, kdim_pad, kc_pad;
+  int n_var, delta_step;
   bool aligned;   // fast path: every strip and segment 16-byte aligned
 };
 
 template <typename T>
 __device__ __forceinline__ void prep_weight_tile(const LowerParams& p, int64_t tile) {
-  // Kt[c][j] = K[j][c] for j < kdim, c < k_c; zero elsewhere.  32x32 tiles.
+  // Kt[v][c][j] = K[j - v*delta_step][c] where 0 <= j - v*delta_step < kdim
+  // and c < k_c; zero elsewhere.  32x32 tiles transposed through smem.
   __shared__ T tbuf[32][33];
   const int64_t tiles_j = (p.kdim_pad + 31) / 32;
+  const int64_t tiles_c = (p.kc_pad + 31) / 32;
+  const int64_t v = tile / (tiles_j * tiles_c);
+  tile -= v * tiles_j * tiles_c;
   const int64_t jt = tile % tiles_j, ct = tile / tiles_j;
+  const int64_t delta = v * p.delta_step;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
   const T* K = reinterpret_cast<const T*>(p.K);
-  T* Kt = reinterpret_cast<T*>(p.Kt);
+  T* Kt = reinterpret_cast<T*>(p.Kt) + v * p.kc_pad * p.kdim_pad;
   for (int r = ty; r < 32; r += 8) {
-    const int64_t j = jt * 32 + r, c = ct * 32 + tx;
-    tbuf[r][tx] = (j < p.kdim && c < p.k_c) ? K[j * p.k_c + c] : T(0);
+    const int64_t j = jt * 32 + r - delta, c = ct * 32 + tx;
+    tbuf[r][tx] = (j >= 0 && j < p.kdim && c < p.k_c) ? K[j * p.k_c + c] : T(0);
   }
   __syncthreads();
   for (int r = ty; r < 32; r += 8) {
@@ -74,7 +80,7 @@ __global__ void __launch_bounds__(256) lower_kernel(const LowerParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
 
   if (blockIdx.x >= p.n_lower_blocks) {
-    const int64_t n_tiles = ((p.kdim_pad + 31) / 32) * ((p.kc_pad + 31) / 32);
+    const int64_t n_tiles = p.n_var * ((p.kdim_pad + 31) / 32) * ((p.kc_pad + 31) / 32);
     for (int64_t t = blockIdx.x - p.n_lower_blocks; t < n_tiles;
          t += gridDim.x - p.n_lower_blocks)
       prep_weight_tile<T>(p, t);
@@ -184,6 +190,8 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   p.k_c = s.k_c;
   p.kdim_pad = pl.kdim_pad;
   p.kc_pad = pl.kc_pad;
+  p.n_var = pl.n_var;
+  p.delta_step = pl.delta_step;
 
   // Rows per CTA: stage at most ~24 KB of input and aim for >= ~4 CTAs per SM.
   const int64_t row_bytes = p.iwc * pl.elt;
@@ -205,7 +213,7 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   const size_t smem = static_cast<size_t>(hb * row_bytes) + 32;
   int64_t prep_blocks = 0;
   if (Kt != nullptr) {
-    const int64_t tiles = ((pl.kdim_pad + 31) / 32) * ((pl.kc_pad + 31) / 32);
+    const int64_t tiles = pl.n_var * ((pl.kdim_pad + 31) / 32) * ((pl.kc_pad + 31) / 32);
     prep_blocks = std::min<int64_t>(tiles, 2LL * num_sms());
   }
   const int64_t grid = p.n_lower_blocks + prep_blocks;

@@ -128,7 +128,15 @@ mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, P
   p->kdim = s->k_h * s->k_w * s->i_c;
   p->shift = static_cast<int64_t>(s_h) * s->k_w * s->i_c;
   p->bk = kTileKBytes / p->elt;
-  p->kdim_pad = round_up(p->kdim, p->bk);
+  p->vec = 16 / p->elt;
+  {
+    int64_t a = p->shift % p->vec, b = p->vec;  // gcd(shift, vec)
+    while (a) { int64_t t = b % a; b = a; a = t; }
+    p->delta_step = static_cast<int>(b);
+  }
+  p->n_var = p->vec / p->delta_step;
+  p->kdim_pad = round_up(p->kdim + (p->vec - p->delta_step), p->bk);
+  if (p->n_var == 1) p->kdim_pad = round_up(p->kdim, p->bk);
   p->n_tiles_n = static_cast<int>((s->k_c + 255) / 256);
   p->bn = static_cast<int>(round_up((s->k_c + p->n_tiles_n - 1) / p->n_tiles_n, 16));
   p->kc_pad = static_cast<int64_t>(p->n_tiles_n) * p->bn;
@@ -136,7 +144,7 @@ mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, P
   p->n_O = s->i_n * p->o_h * p->o_w * s->k_c;
   p->bytes_L_pitched = static_cast<size_t>(s->i_n * p->o_w * p->pitch) * p->elt;
   p->off_kt = static_cast<size_t>(round_up(static_cast<int64_t>(p->bytes_L_pitched), 1024));
-  p->bytes_kt = static_cast<size_t>(p->kc_pad * p->kdim_pad) * p->elt;
+  p->bytes_kt = static_cast<size_t>(p->n_var * p->kc_pad * p->kdim_pad) * p->elt;
   p->ws_bytes = p->off_kt + p->bytes_kt + 1024;
   // TMA coordinate / extent limits (int32 coordinates, dims <= 2^32)
   if (p->l_cols + p->kdim_pad >= (1LL << 31) || s->i_n * p->o_w >= (1LL << 31) ||

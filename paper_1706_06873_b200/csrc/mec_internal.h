@@ -26,14 +26,23 @@ struct Plan {
   int64_t kdim;          // k_h k_w i_c: GEMM reduction length
   int64_t shift;         // s_h k_w i_c: column offset between output rows
   int bk;                // K-tile in elements (128 B / elt)
-  int64_t kdim_pad;      // kdim rounded up to bk
+  // TMA needs every box to start 16-byte aligned in dim 0, but window h starts
+  // at column h*shift.  The box therefore starts at the aligned column
+  // x = h*shift - delta, delta = (h*shift) mod vec (vec = 16/elt), and the
+  // B operand used for that window is K_mat shifted down by delta rows
+  // (zero rows above).  delta takes n_var = vec / gcd(shift, vec) values,
+  // multiples of delta_step = gcd(shift, vec); Kt holds one copy per value.
+  int vec;               // elements per 16 bytes
+  int delta_step;        // gcd(shift, vec)
+  int n_var;             // number of shifted weight copies
+  int64_t kdim_pad;      // (kdim + max delta) rounded up to bk
   int n_tiles_n;         // ceil(k_c / 256)
   int bn;                // N tile (multiple of 16, <= 256)
   int64_t kc_pad;        // n_tiles_n * bn
   int64_t n_L, n_O;      // #L (dense) and #O, elements
   size_t bytes_L_pitched;  // i_n o_w pitch elt
   size_t off_kt;           // workspace offset of the prepared weight operand
-  size_t bytes_kt;         // kc_pad kdim_pad elt
+  size_t bytes_kt;         // n_var kc_pad kdim_pad elt
   size_t ws_bytes;         // total workspace (incl. alignment slack)
 };
 
@@ -43,8 +52,10 @@ mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, P
 // ---- kernels (each returns cudaGetLastError() of its launch) ----
 
 // Lowering (Alg.2 l.3-6) into L with row pitch `pitch` elements; optionally,
-// in the same launch, the weight operand Kt[kc_pad][kdim_pad] = K_mat^T,
-// zero padded (Alg.2 l.7).  Kt may be null (mec_lower).
+// in the same launch, the weight operand (Alg.2 l.7, K as a (k_h k_w i_c) x
+// k_c matrix), transposed to K-major and shifted:
+//   Kt[v][c][j] = K_mat[j - v*delta_step][c]  (0 outside, v < n_var).
+// Kt may be null (mec_lower).
 cudaError_t launch_lower(const Plan& p, const void* I, void* L, int64_t pitch, const void* K,
                          void* Kt, cudaStream_t st, int* launches);
 

@@ -36,10 +36,15 @@
 // CTAs in flight at any time work on neighbouring windows of the same L rows,
 // which overlap k_h/s_h-fold, so the re-reads hit L2.
 //
-// K-tail: kdim is padded to a multiple of the K-tile (64 bf16 / 32 fp32).
-// The last window tile reads up to one K-tile past the window (neighbouring,
-// finite lowered data, or TMA zero fill past the row end); Kt's padded rows
-// are zero, so those columns contribute exactly 0 (inputs must be finite).
+// TMA alignment: a box must start 16-byte aligned in dim 0, but window h
+// starts at column h*shift (shift = s_h k_w i_c, e.g. 132 bf16 = 264 B for
+// AlexNet conv1).  The box starts at x = h*shift - delta instead, delta =
+// (h*shift) mod (16/elt), and the MMA uses a copy of K_mat shifted down by
+// delta rows (Kt variant delta/delta_step; built by the lowering launch).
+// K-tail: the reduction is padded to a multiple of the K-tile (64 bf16 / 32
+// fp32).  Columns of the box outside [delta, delta + kdim) (neighbouring,
+// finite lowered data, or TMA zero fill past the row end) meet zero rows of
+// Kt, so they contribute exactly 0 (inputs must be finite).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -63,6 +68,8 @@ struct GemmParams {
   int64_t o_h, o_w, i_n, k_c;
   int64_t rows, groups, n_mt;
   int64_t shift;
+  int vec, delta_step;
+  int64_t kc_pad;
   int bk;
   int nk;           // K-tiles per window
   int bn, n_tiles_n;
@@ -143,10 +150,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
         const TileCoord c = decode_tile(p, t);
-        const int32_t x0 = static_cast<int32_t>(c.h * p.shift);
+        // window start h*shift, rounded down to a 16-byte boundary (TMA rule);
+        // the delta-shifted weight copy absorbs the difference
+        const int64_t xw = c.h * p.shift;
+        const int64_t delta = xw % p.vec;
+        const int32_t x0 = static_cast<int32_t>(xw - delta);
         const int32_t y0 = static_cast<int32_t>(c.mt * kBM);
         const int32_t z0 = static_cast<int32_t>(c.g);
-        const int32_t n0 = static_cast<int32_t>(c.nt * p.bn);
+        const int32_t n0 = static_cast<int32_t>((delta / p.delta_step) * p.kc_pad + c.nt * p.bn);
         for (int kt = 0; kt < p.nk; ++kt) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[stage], kATileBytes + b_tile_bytes);
@@ -293,10 +304,10 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
     cudaError_t e = encode_tiled(&tmA, tf32, 3, a.L, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
-  // B: the prepared weight operand Kt, kc_pad x kdim_pad, K-major.
+  // B: the prepared weight operand Kt, n_var x kc_pad rows of kdim_pad, K-major.
   {
     const uint64_t dims[2] = {static_cast<uint64_t>(pl.kdim_pad),
-                              static_cast<uint64_t>(pl.kc_pad)};
+                              static_cast<uint64_t>(pl.n_var * pl.kc_pad)};
     const uint64_t strides[1] = {static_cast<uint64_t>(pl.kdim_pad) * pl.elt};
     const uint32_t box[2] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(pl.bn)};
     cudaError_t e = encode_tiled(&tmB, tf32, 2, a.Kt, dims, strides, box);
@@ -313,6 +324,9 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   p.groups = a.groups;
   p.n_mt = (a.rows + kBM - 1) / kBM;
   p.shift = pl.shift;
+  p.vec = pl.vec;
+  p.delta_step = pl.delta_step;
+  p.kc_pad = pl.kc_pad;
   p.bk = pl.bk;
   p.nk = static_cast<int>(pl.kdim_pad / pl.bk);
   p.bn = pl.bn;
