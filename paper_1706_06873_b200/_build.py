@@ -45,15 +45,30 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, extra_flags=(), so_path: str | None = None,
+          build_dir: str | None = None) -> str:
+    """Compile csrc/*.cu into libmec.so (or `so_path`, e.g. a -DMEC_TRACE build)."""
+    global SO, BUILD
+    so_target = so_path or SO
+    bdir = build_dir or BUILD
+    if so_path is None and not force and up_to_date():
         return SO
+    SO_saved, BUILD_saved = SO, BUILD
+    SO, BUILD = so_target, bdir
+    try:
+        return _build(verbose, list(extra_flags))
+    finally:
+        SO, BUILD = SO_saved, BUILD_saved
+
+
+def _build(verbose, extra_flags):
     os.makedirs(BUILD, exist_ok=True)
     objs = []
     log = []
     for src in _sources():
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        cmd = [nvcc(), *NVCC_FLAGS, *extra_flags, "-I", os.path.join(ROOT, "include"), "-c", src,
+               "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:

@@ -7,18 +7,23 @@
 // B200 design: one CTA owns a band of HB input rows of one image.  It stages
 // I[n, h0:h0+HB, :, :] (contiguous in NHWC) into shared memory
 // with 128-bit coalesced loads -- every input byte is read from HBM once --
-// and then, for every output column w, writes the contiguous L segment
-// L[n, w, h0:h0+HB, :, :] (HB strips of k_w i_c elements, which are
-// adjacent in L) with 128-bit coalesced stores, gathering the strips
-// from shared memory.  Segments that do not start 16-byte aligned get a
-// scalar head/tail.  When every strip offset is 16-byte aligned (i_c elt a
-// multiple of 16, e.g. i_c = 64 bf16) the gather is one 128-bit LDS per
-// store.
+// then, for every output column w, writes the contiguous L segment
+// L[n, w, h0:h0+HB, :, :] (HB strips of k_w i_c elements, adjacent in L)
+// with 128-bit stores.  One warp per segment; a lane assembles one 16-byte
+// output granule:
+//   * aligned fast path (i_c elt a multiple of 16, e.g. i_c = 64 bf16):
+//     one LDS.128 per STG.128;
+//   * general path (e.g. i_c = 3): a granule inside one strip is a run of
+//     contiguous smem elements at any alignment -> aligned 32-bit LDS +
+//     funnel shifts; a granule straddling two strips falls back to element
+//     loads.  All index math is 32-bit, one division per granule.
+// HB is a multiple of 16/gcd(kwc elt,16) where possible so every segment of
+// the pitch-padded conv-path L starts 16-byte aligned.
 //
 // The same launch also builds the GEMM's weight operand (Alg.2 l.7, "K as
-// k_h k_w i_c x k_c matrix"): Kt = K_mat^T, k_c_pad x kdim_pad, zero padded,
-// K-major for tcgen05 -- 32x32 tiles transposed through shared memory by the
-// CTAs after the lowering CTAs.
+// k_h k_w i_c x k_c matrix"), K-major and delta-shifted (see mec_internal.h),
+// with 32x32 tiles transposed through shared memory by the CTAs after the
+// lowering CTAs.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,11 +38,15 @@ struct LowerParams {
   const unsigned char* I;
   const unsigned char* I_end;
   unsigned char* L;
-  int64_t i_h, i_w, i_c, k_w, s_w, o_w;
-  int64_t iwc;    // i_w i_c   (one input row, elements)
-  int64_t kwc;    // k_w i_c   (one strip, elements)
+  int64_t i_h;
   int64_t pitch;  // L row pitch, elements
+  int64_t o_w;
+  uint32_t iwc;   // i_w i_c   (one input row, elements)
+  uint32_t kwc;   // k_w i_c   (one strip, elements)
+  uint32_t wstep; // s_w i_c   (strip start advance per output column)
+  uint32_t kwc_magic;  // floor(2^32 / kwc) + 1: e / kwc == umulhi(e, magic) for e < 2^20
   int hb;         // input rows per CTA
+  uint32_t table_off;  // smem byte offset of the word table (general path)
   int bands;      // ceil(i_h / hb)
   int64_t n_lower_blocks;
   // weight operand
@@ -76,7 +85,7 @@ __device__ __forceinline__ void prep_weight_tile(const LowerParams& p, int64_t t
 
 template <typename T>
 __global__ void __launch_bounds__(256) lower_kernel(const LowerParams p) {
-  constexpr int VEC = 16 / sizeof(T);
+  constexpr uint32_t VEC = 16 / sizeof(T);
   extern __shared__ __align__(16) unsigned char smem[];
 
   if (blockIdx.x >= p.n_lower_blocks) {
@@ -88,81 +97,151 @@ __global__ void __launch_bounds__(256) lower_kernel(const LowerParams p) {
   }
 
   const int64_t n = blockIdx.x / p.bands;
-  const int64_t h0 = (blockIdx.x % p.bands) * p.hb;
-  const int64_t rows = min(static_cast<int64_t>(p.hb), p.i_h - h0);
+  const int64_t h0 = (blockIdx.x % p.bands) * static_cast<int64_t>(p.hb);
+  const uint32_t rows = static_cast<uint32_t>(min(static_cast<int64_t>(p.hb), p.i_h - h0));
 
   // ---- stage I[n, h0:h0+rows, :, :] in shared memory (128-bit loads) ----
   const unsigned char* a0 = p.I + ((n * p.i_h + h0) * p.iwc) * sizeof(T);
   const unsigned char* ab = reinterpret_cast<const unsigned char*>(
       reinterpret_cast<uintptr_t>(a0) & ~static_cast<uintptr_t>(15));
-  const int shift_elems = static_cast<int>((a0 - ab) / sizeof(T));
-  const int64_t nbytes = (a0 - ab) + rows * p.iwc * sizeof(T);
-  const int64_t n16 = (nbytes + 15) / 16;
-  for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) {
-    const unsigned char* g = ab + 16 * i;
+  const uint32_t shift_elems = static_cast<uint32_t>((a0 - ab) / sizeof(T));
+  const uint32_t nbytes = static_cast<uint32_t>(a0 - ab) + rows * p.iwc * sizeof(T);
+  const uint32_t n16 = (nbytes + 15) / 16;
+  for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
+    const unsigned char* g = ab + 16 * static_cast<size_t>(i);
     if (g + 16 <= p.I_end) {
       *reinterpret_cast<uint4*>(smem + 16 * i) = __ldg(reinterpret_cast<const uint4*>(g));
     } else {
-      for (int b = 0; b < VEC; ++b) {
+      for (uint32_t b = 0; b < VEC; ++b) {
         const unsigned char* ge = g + b * sizeof(T);
         if (ge < p.I_end)
           reinterpret_cast<T*>(smem + 16 * i)[b] = *reinterpret_cast<const T*>(ge);
       }
     }
   }
+  // zero the slack past the staged bytes so table reads past a row end are defined
+  if (threadIdx.x < 3) reinterpret_cast<uint4*>(smem + 16 * n16)[threadIdx.x] = make_uint4(0, 0, 0, 0);
   __syncthreads();
 
   const T* srow = reinterpret_cast<const T*>(smem) + shift_elems;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  const int64_t seg_len = rows * p.kwc;  // elements of L[n, w, h0:h0+rows, :, :]
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  (void)warp;
+  (void)lane;
+  (void)nwarps;
+  const uint32_t seg_len = rows * p.kwc;  // elements of L[n, w, h0:h0+rows, :, :]
 
   if (p.aligned) {
-    // every strip starts 16-byte aligned in both smem and L: 1 LDS.128 per STG.128
-    const int64_t vec_per_strip = p.kwc / VEC;
-    const int64_t n_vec = rows * vec_per_strip;
-    for (int64_t w = warp; w < p.o_w; w += nwarps) {
+    // every strip starts 16-byte aligned in both smem and L: 1 LDS.128 per STG.128;
+    // (w, vector) flattened over the CTA
+    const uint32_t vps = p.kwc / VEC;  // vectors per strip
+    const uint32_t n_vec = rows * vps;
+    const uint32_t total = n_vec * static_cast<uint32_t>(p.o_w);
+    for (uint32_t idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      const uint32_t w = idx / n_vec, v = idx - w * n_vec;
+      const uint32_t hh = v / vps, r = (v - hh * vps) * VEC;
       T* dst = reinterpret_cast<T*>(p.L) + (n * p.o_w + w) * p.pitch + h0 * p.kwc;
-      const T* src = srow + p.s_w * w * p.i_c;
-      for (int64_t v = lane; v < n_vec; v += 32) {
-        const int64_t hh = v / vec_per_strip, r = (v - hh * vec_per_strip) * VEC;
-        const uint4 val = *reinterpret_cast<const uint4*>(src + hh * p.iwc + r);
-        *reinterpret_cast<uint4*>(dst + hh * p.kwc + r) = val;
+      *reinterpret_cast<uint4*>(dst + hh * p.kwc + r) =
+          *reinterpret_cast<const uint4*>(srow + w * p.wstep + hh * p.iwc + r);
+    }
+    return;
+  }
+
+  // general path (strips not 16-byte aligned, e.g. i_c = 3).  When every
+  // segment starts 4-byte aligned (pitch-padded conv-path L), each 4-byte
+  // output word j of a segment is byte_perm(W[a_j], W[b_j], sel_j) of two
+  // aligned 32-bit words of the staged rows, with (a_j, b_j, sel_j) the same
+  // for every w up to the word shift w*wstep*elt/4 (two tables: that shift's
+  // 2-byte remainder).  Per word: table LDS + 2 LDS + PRMT + STG, consecutive
+  // lanes on consecutive words (conflict-free, coalesced).
+  const uint32_t seg_bytes = seg_len * sizeof(T);
+  const bool word_ok = (p.pitch * sizeof(T)) % 4 == 0 &&
+                       ((reinterpret_cast<uintptr_t>(p.L) + h0 * p.kwc * sizeof(T)) & 3) == 0;
+  if (word_ok) {
+    const uint32_t seg_words = (seg_bytes + 3) / 4;
+    uint32_t* table = reinterpret_cast<uint32_t*>(smem + p.table_off);
+    const uint32_t sbyte0 = shift_elems * sizeof(T);
+    for (uint32_t t = threadIdx.x; t < 2 * seg_words; t += blockDim.x) {
+      const uint32_t par = t / seg_words, j = t - par * seg_words;
+      uint32_t wa, wb, sel;
+      if constexpr (sizeof(T) == 4) {
+        const uint32_t hh = p.kwc_magic ? __umulhi(j, p.kwc_magic) : j;
+        const uint32_t r = j - hh * p.kwc;
+        wa = (sbyte0 + (hh * p.iwc + r) * 4) >> 2;
+        wb = wa;
+        sel = 0;  // 0x3210
+      } else {
+        const uint32_t e0 = 2 * j, e1 = 2 * j + 1 < seg_len ? 2 * j + 1 : 2 * j;
+        const uint32_t h0e = p.kwc_magic ? __umulhi(e0, p.kwc_magic) : e0;
+        const uint32_t h1e = p.kwc_magic ? __umulhi(e1, p.kwc_magic) : e1;
+        const uint32_t b0 = sbyte0 + (h0e * p.iwc + e0 - h0e * p.kwc) * 2 + par * 2;
+        const uint32_t b1 = sbyte0 + (h1e * p.iwc + e1 - h1e * p.kwc) * 2 + par * 2;
+        wa = b0 >> 2;
+        wb = b1 >> 2;
+        sel = ((b0 >> 1) & 1u) | (((b1 >> 1) & 1u) << 1);
+      }
+      table[t] = wa | (wb << 15) | (sel << 30);
+    }
+    __syncthreads();
+    const uint32_t* W = reinterpret_cast<const uint32_t*>(smem);
+    const bool odd_tail = (seg_bytes & 3u) != 0;  // last word holds one 2-byte element
+    const uint32_t full_words = odd_tail ? seg_words - 1 : seg_words;
+    // one warp per w: the segment pointer and table parity are hoisted, the
+    // inner loop is table LDS + 2 LDS + PRMT + STG per word
+    for (uint32_t w = warp; w < p.o_w; w += nwarps) {
+      const uint32_t wbyte = w * p.wstep * static_cast<uint32_t>(sizeof(T));
+      const uint32_t* tab = table + ((wbyte >> 1) & 1u) * seg_words;
+      const uint32_t* Wb = W + (wbyte >> 2);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(
+          p.L + (((n * p.o_w + w) * p.pitch + h0 * p.kwc) * sizeof(T)));
+      for (uint32_t j = lane; j < full_words; j += 32) {
+        const uint32_t entry = tab[j];
+        const uint32_t x = Wb[entry & 0x7FFFu];
+        if constexpr (sizeof(T) == 4) {
+          dst[j] = x;
+        } else {
+          const uint32_t y = Wb[(entry >> 15) & 0x7FFFu];
+          const uint32_t selector = ((entry >> 30) & 1u ? 0x0032u : 0x0010u) |
+                                    ((entry >> 31) ? 0x7600u : 0x5400u);
+          dst[j] = __byte_perm(x, y, selector);
+        }
+      }
+      if (odd_tail && lane == 0) {
+        const uint32_t entry = tab[seg_words - 1];
+        const uint32_t x = Wb[entry & 0x7FFFu];
+        const uint32_t lo = ((entry >> 30) & 1u) ? (x >> 16) : (x & 0xFFFFu);
+        reinterpret_cast<uint16_t*>(dst)[2 * (seg_words - 1)] = static_cast<uint16_t>(lo);
       }
     }
     return;
   }
 
-  // general path: 16-byte granules of each L segment, gathered element-wise
-  for (int64_t w = warp; w < p.o_w; w += nwarps) {
+  // non-uniform segment alignment (dense L with an odd pitch, mec_lower):
+  // element-wise, one warp per segment
+  for (uint32_t w = warp; w < p.o_w; w += nwarps) {
     T* seg = reinterpret_cast<T*>(p.L) + (n * p.o_w + w) * p.pitch + h0 * p.kwc;
-    const T* src = srow + p.s_w * w * p.i_c;
-    const int head = static_cast<int>((reinterpret_cast<uintptr_t>(seg) & 15) / sizeof(T));
-    T* gbase = seg - head;  // 16-byte aligned
-    const int64_t n_gran = (head + seg_len + VEC - 1) / VEC;
-    for (int64_t gi = lane; gi < n_gran; gi += 32) {
-      const int64_t e0 = gi * VEC - head;  // segment element of the granule's first slot
-      int64_t hh = (e0 >= 0) ? e0 / p.kwc : 0;
-      int64_t r = (e0 >= 0) ? e0 - hh * p.kwc : 0;
-      if (e0 >= 0 && e0 + VEC <= seg_len) {
-        union {
-          uint4 v;
-          T e[VEC];
-        } u;
-#pragma unroll
-        for (int b = 0; b < VEC; ++b) {
-          u.e[b] = src[hh * p.iwc + r];
-          if (++r == p.kwc) { r = 0; ++hh; }
-        }
-        *reinterpret_cast<uint4*>(gbase + gi * VEC) = u.v;
-      } else {
-        for (int b = 0; b < VEC; ++b) {
-          const int64_t e = e0 + b;
-          if (e < 0 || e >= seg_len) continue;
-          const int64_t h2 = e / p.kwc, r2 = e - h2 * p.kwc;
-          gbase[gi * VEC + b] = src[h2 * p.iwc + r2];
-        }
-      }
+    for (uint32_t e = lane; e < seg_len; e += 32) {
+      const uint32_t h2 = p.kwc_magic ? __umulhi(e, p.kwc_magic) : e;
+      const uint32_t r2 = e - h2 * p.kwc;
+      seg[e] = srow[h2 * p.iwc + w * p.wstep + r2];
     }
+  }
+}
+
+// Direct fallback for input rows too wide to stage in shared memory: every
+// thread copies one L element from global.  (Not used by any BASELINE config.)
+template <typename T>
+__global__ void __launch_bounds__(256) lower_direct_kernel(const T* __restrict__ I, T* __restrict__ L,
+                                                           int64_t i_n, int64_t i_h, int64_t i_w,
+                                                           int64_t i_c, int64_t k_w, int64_t s_w,
+                                                           int64_t o_w, int64_t pitch) {
+  const int64_t kwc = k_w * i_c, row = i_h * kwc;
+  const int64_t total = i_n * o_w * row;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t nw = e / row, rem = e - nw * row;
+    const int64_t n = nw / o_w, w = nw - n * o_w;
+    const int64_t h = rem / kwc, r = rem - h * kwc;
+    L[nw * pitch + rem] = I[((n * i_h + h) * i_w + s_w * w) * i_c + r];
   }
 }
 
@@ -176,14 +255,12 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   p.I_end = p.I + static_cast<size_t>(s.i_n * s.i_h * s.i_w * s.i_c) * pl.elt;
   p.L = static_cast<unsigned char*>(L);
   p.i_h = s.i_h;
-  p.i_w = s.i_w;
-  p.i_c = s.i_c;
-  p.k_w = s.k_w;
-  p.s_w = pl.s_w;
   p.o_w = pl.o_w;
-  p.iwc = s.i_w * s.i_c;
-  p.kwc = s.k_w * s.i_c;
   p.pitch = pitch;
+  p.iwc = static_cast<uint32_t>(s.i_w * s.i_c);
+  p.kwc = static_cast<uint32_t>(s.k_w * s.i_c);
+  p.wstep = static_cast<uint32_t>(pl.s_w * s.i_c);
+  p.kwc_magic = p.kwc > 1 ? static_cast<uint32_t>((1ull << 32) / p.kwc + 1) : 0u;  // 0: kwc == 1
   p.K = static_cast<const unsigned char*>(K);
   p.Kt = static_cast<unsigned char*>(Kt);
   p.kdim = pl.kdim;
@@ -193,29 +270,68 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   p.n_var = pl.n_var;
   p.delta_step = pl.delta_step;
 
-  // Rows per CTA: stage at most ~24 KB of input and aim for >= ~4 CTAs per SM.
-  const int64_t row_bytes = p.iwc * pl.elt;
-  const int64_t max_rows_smem = std::max<int64_t>(1, (24 * 1024) / row_bytes);
-  const int64_t want_blocks = 4LL * num_sms();
-  int64_t hb = std::min<int64_t>(s.i_h, max_rows_smem);
-  while (hb > 1 && s.i_n * ((s.i_h + hb - 1) / hb) < want_blocks) hb = (hb + 1) / 2;
-  // keep each band's L segment 16-byte aligned where the strip length allows it
-  p.hb = static_cast<int>(hb);
-  p.bands = static_cast<int>((s.i_h + hb - 1) / hb);
-  p.n_lower_blocks = s.i_n * p.bands;
-
-  const int vec = 16 / pl.elt;
-  const bool base_ok = (reinterpret_cast<uintptr_t>(I) % 16 == 0) &&
-                       (reinterpret_cast<uintptr_t>(L) % 16 == 0);
-  p.aligned = base_ok && (p.kwc % vec == 0) && ((pl.s_w * s.i_c) % vec == 0) &&
-              (p.iwc % vec == 0) && (pitch % vec == 0);
-
-  const size_t smem = static_cast<size_t>(hb * row_bytes) + 32;
   int64_t prep_blocks = 0;
   if (Kt != nullptr) {
     const int64_t tiles = pl.n_var * ((pl.kdim_pad + 31) / 32) * ((pl.kc_pad + 31) / 32);
     prep_blocks = std::min<int64_t>(tiles, 2LL * num_sms());
   }
+
+  const int64_t row_bytes = static_cast<int64_t>(p.iwc) * pl.elt;
+  const int64_t max_smem = 96 * 1024;
+  const bool use_smem = row_bytes + 64 <= max_smem && s.k_w * s.i_c < (1 << 20) && p.iwc < (1u << 24);
+  if (!use_smem) {
+    // weight prep still needs the main kernel's prep blocks: run them with a 1-band grid
+    if (Kt != nullptr) {
+      LowerParams q = p;
+      q.n_lower_blocks = 0;
+      if (pl.elt == 2)
+        lower_kernel<uint16_t><<<static_cast<unsigned>(prep_blocks), 256, 64, st>>>(q);
+      else
+        lower_kernel<uint32_t><<<static_cast<unsigned>(prep_blocks), 256, 64, st>>>(q);
+      if (launches) ++*launches;
+    }
+    const int64_t total = s.i_n * pl.o_w * pl.l_cols;
+    const int64_t grid = std::min<int64_t>((total + 255) / 256, 32LL * num_sms());
+    if (pl.elt == 2)
+      lower_direct_kernel<uint16_t><<<static_cast<unsigned>(grid), 256, 0, st>>>(
+          static_cast<const uint16_t*>(I), static_cast<uint16_t*>(L), s.i_n, s.i_h, s.i_w, s.i_c,
+          s.k_w, pl.s_w, pl.o_w, pitch);
+    else
+      lower_direct_kernel<uint32_t><<<static_cast<unsigned>(grid), 256, 0, st>>>(
+          static_cast<const uint32_t*>(I), static_cast<uint32_t*>(L), s.i_n, s.i_h, s.i_w, s.i_c,
+          s.k_w, pl.s_w, pl.o_w, pitch);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
+
+  // Rows per CTA: stage <= ~24 KB of input (several CTAs per SM), enough CTAs
+  // for >= ~4 per SM, and HB a multiple of the alignment period so segments of
+  // a 16-byte-pitched L start 16-byte aligned.
+  const int vec = 16 / pl.elt;
+  int64_t period = 1;
+  while ((period * p.kwc) % vec != 0) ++period;  // <= vec
+  const int64_t max_rows_smem = std::max<int64_t>(1, (24 * 1024) / row_bytes);
+  const int64_t want_blocks = 4LL * num_sms();
+  int64_t hb = std::min<int64_t>(s.i_h, max_rows_smem);
+  while (hb > period && s.i_n * ((s.i_h + hb - 1) / hb) < want_blocks) hb = (hb + 1) / 2;
+  if (hb > period && hb < s.i_h) hb = hb / period * period;
+  // the general path divides e < hb*kwc by kwc with a 32-bit magic multiply,
+  // exact while hb*kwc*kwc < 2^32
+  while (hb > 1 && static_cast<uint64_t>(hb) * p.kwc * p.kwc >= (1ull << 32)) hb = (hb + 1) / 2;
+  hb = std::max<int64_t>(1, hb);
+  p.hb = static_cast<int>(hb);
+  p.bands = static_cast<int>((s.i_h + hb - 1) / hb);
+  p.n_lower_blocks = s.i_n * p.bands;
+
+  const bool base_ok = (reinterpret_cast<uintptr_t>(I) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(L) % 16 == 0);
+  p.aligned = base_ok && (p.kwc % vec == 0) && (p.wstep % vec == 0) && (p.iwc % vec == 0) &&
+              (pitch % vec == 0);
+
+  const size_t staged = static_cast<size_t>(hb * row_bytes) + 96;
+  p.table_off = static_cast<uint32_t>((staged + 15) / 16 * 16);
+  const size_t seg_words = (static_cast<size_t>(hb) * p.kwc * pl.elt + 3) / 4;
+  const size_t smem = p.table_off + (p.aligned ? 0 : 2 * seg_words * 4);
   const int64_t grid = p.n_lower_blocks + prep_blocks;
   if (grid > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
   if (pl.elt == 2) {

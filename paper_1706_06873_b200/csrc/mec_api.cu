@@ -80,9 +80,29 @@ int num_sms() {
   return cached[dev];
 }
 
+static cudaError_t encode_impl(CUtensorMap* map, bool tf32, int rank, const void* base,
+                               const uint64_t* dims, const uint64_t* strides_bytes,
+                               const uint32_t* box, CUtensorMapSwizzle swz);
+
 cudaError_t encode_tiled(CUtensorMap* map, bool tf32, int rank, const void* base,
                          const uint64_t* dims, const uint64_t* strides_bytes,
                          const uint32_t* box) {
+  return encode_impl(map, tf32, rank, base, dims, strides_bytes, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+cudaError_t encode_tiled_swz(CUtensorMap* map, bool tf32, int rank, const void* base,
+                             const uint64_t* dims, const uint64_t* strides_bytes,
+                             const uint32_t* box, int swizzle_bytes) {
+  const CUtensorMapSwizzle swz = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                 : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                       : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return encode_impl(map, tf32, rank, base, dims, strides_bytes, box, swz);
+}
+
+static cudaError_t encode_impl(CUtensorMap* map, bool tf32, int rank, const void* base,
+                               const uint64_t* dims, const uint64_t* strides_bytes,
+                               const uint32_t* box, CUtensorMapSwizzle swz) {
   std::call_once(g_encode_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -104,7 +124,7 @@ cudaError_t encode_tiled(CUtensorMap* map, bool tf32, int rank, const void* base
   }
   CUresult r = g_encode(map, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                         rank, const_cast<void*>(base), d, s, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -301,12 +321,10 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
     ga.Kt = Kt;
     ga.O = O;
     if (path == MEC_PATH_SOLUTION_A) {  // l.9: L as (i_n o_w) x (i_h k_w i_c)
-      ga.groups = 1;
-      ga.rows = s->i_n * p.o_w;
+      ga.batch_folded = true;
       ga.out_hnwc = opt->sola_fix != MEC_SOLA_FIX_EPILOGUE;
     } else {  // l.21: L as i_n matrices of o_w x (i_h k_w i_c)
-      ga.groups = s->i_n;
-      ga.rows = p.o_w;
+      ga.batch_folded = false;
       ga.out_hnwc = false;
     }
     e = mec::launch_window_gemm(p, ga, stream_, &launches);

@@ -59,15 +59,15 @@ mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, P
 cudaError_t launch_lower(const Plan& p, const void* I, void* L, int64_t pitch, const void* K,
                          void* Kt, cudaStream_t st, int* launches);
 
-// Window GEMMs (Alg.2 l.10-12 or l.23-25) on tcgen05.  `groups` x `rows`
-// is the row tiling: Solution A = 1 x (i_n o_w), Solution B = i_n x o_w.
-// out_hnwc: store O in h-n-w-c (Alg.2 l.10's "O as o_h x i_n o_w k_c")
-// instead of n-h-w-c.
+// Window GEMMs (Alg.2 l.10-12 or l.23-25) on tcgen05.  batch_folded:
+// Solution A (rows of several images share one 128-row tile); otherwise
+// Solution B (a tile never mixes images).  out_hnwc: store O in h-n-w-c
+// (Alg.2 l.10's "O as o_h x i_n o_w k_c") instead of n-h-w-c.
 struct GemmArgs {
   const void* L;
   const void* Kt;
   void* O;
-  int64_t groups, rows;
+  bool batch_folded;
   bool out_hnwc;
 };
 cudaError_t launch_window_gemm(const Plan& p, const GemmArgs& a, cudaStream_t st, int* launches);

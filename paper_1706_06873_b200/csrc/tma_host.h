@@ -16,4 +16,10 @@ cudaError_t encode_tiled(CUtensorMap* map, bool tf32, int rank, const void* base
                          const uint64_t* dims, const uint64_t* strides_bytes,
                          const uint32_t* box);
 
+// Same with an explicit swizzle span in bytes (0 = none, 32, 64, 128), for
+// the epilogue's TMA stores.
+cudaError_t encode_tiled_swz(CUtensorMap* map, bool tf32, int rank, const void* base,
+                             const uint64_t* dims, const uint64_t* strides_bytes,
+                             const uint32_t* box, int swizzle_bytes);
+
 }  // namespace mec

@@ -19,22 +19,33 @@
 // the same (row, h) they perform bit-identical arithmetic.
 //
 // Kernel structure (persistent, one CTA per SM, 6 warps):
-//   warp 0     TMA producer: A window tile (128 rows x 128 B) + B tile
-//              (bn rows of Kt x 128 B) per K-tile into a `stages`-deep ring,
-//              128-byte swizzled, mbarrier complete_tx.
-//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
-//              (M = 128, N = bn, K = 16 bf16 / 8 tf32 per instruction),
-//              fp32 accumulators in TMEM, double-buffered (2 x bn columns)
-//              so the epilogue of tile i overlaps the MMAs of tile i+1.
-//   warps 2-5  epilogue: tcgen05.ld (32 lanes x 16 columns), fp32 -> bf16
-//              (RN-even) or fp32, 128-bit stores to O.  Row (n, w) and output
-//              row h give the n-h-w-c address directly -- for Solution A
-//              this applies Alg.2 l.17-19's permutation O[n,h] = O_hnwc[h,n]
-//              at store time (MEC_SOLA_FIX_EPILOGUE); with out_hnwc the
-//              paper's h-n-w-c intermediate is written instead.
-// Tile order: N-tile fastest, then h, then the row tile, then the group: the
-// CTAs in flight at any time work on neighbouring windows of the same L rows,
-// which overlap k_h/s_h-fold, so the re-reads hit L2.
+//   warp 0     TMA producer: per pipeline stage two K-atoms, each an A window
+//              tile (128 rows x 128 B) [+ a B tile (bn rows of Kt x 128 B)
+//              when the weights are not resident], 128-byte swizzled,
+//              mbarrier complete_tx.
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer: 8 MMAs
+//              (M = 128, N = bn, K = 16 bf16 / 8 tf32) per stage wait, with
+//              precomputed 32-bit descriptor offsets; fp32 accumulators in
+//              TMEM, double-buffered (2 x bn columns) so the epilogue of tile
+//              i overlaps the MMAs of tile i+1.
+//   warps 2-5  epilogue, one TMEM lane quarter (32 rows) each, in passes of
+//              128/64 output bytes per row: tcgen05.ld -> fp32 -> bf16 (RN)
+//              or fp32 -> swizzled (conflict-free) shared staging -> one TMA
+//              store per image the 32 rows touch.  The box's row coordinate
+//              is w = row - n*o_w, so rows outside image n are clipped by the
+//              tensor bounds (negative coordinates included): the store
+//              writes O[n, h, w, :] directly in n-h-w-c -- for Solution A this
+//              applies Alg.2 l.17-19's permutation O[n,h] = O_hnwc[h,n] at
+//              store time (MEC_SOLA_FIX_EPILOGUE); with out_hnwc the paper's
+//              h-n-w-c intermediate is stored instead.
+// Scheduling: the tiles (h, row tile, group, N tile) are split into "combos"
+// of one weight variant v = delta(h)/delta_step and one N tile; every CTA
+// works on a single combo, so when the combo's weight operand is small
+// (bn x kdim_pad, <= 120 KB: C1, C2, C3, ...) it is loaded into shared memory
+// ONCE per CTA and stays resident -- only the L windows stream through the
+// smem ring.  Within a combo, h is fastest: the CTAs in flight work on
+// neighbouring windows of the same L rows (overlapping k_h/s_h-fold), so the
+// re-reads hit L2.
 //
 // TMA alignment: a box must start 16-byte aligned in dim 0, but window h
 // starts at column h*shift (shift = s_h k_w i_c, e.g. 132 bf16 = 264 B for
@@ -51,46 +62,108 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "mec_internal.h"
 #include "ptx.cuh"
 #include "tma_host.h"
 
+#ifdef MEC_TRACE
+// Debug-only stage timestamps (built into a separate libmec_trace.so by
+// tools/trace_gemm.py; never in the product library).
+__device__ unsigned long long* g_mec_trace = nullptr;
+__device__ __forceinline__ unsigned long long mec_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define MEC_TRACE_EV(tl, ev)                                                              \
+  do {                                                                                    \
+    if (g_mec_trace != nullptr && (tl) < 64)                                              \
+      g_mec_trace[(static_cast<size_t>(blockIdx.x) * 64 + (tl)) * 16 + (ev)] = mec_gtime(); \
+  } while (0)
+extern "C" int mec_trace_enable(void** dev_buf_out, size_t* bytes_out) {
+  const size_t bytes = static_cast<size_t>(1024) * 64 * 16 * 8;
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, bytes) != cudaSuccess) return 1;
+  cudaMemset(buf, 0, bytes);
+  if (cudaMemcpyToSymbol(g_mec_trace, &buf, sizeof(buf)) != cudaSuccess) return 2;
+  *dev_buf_out = buf;
+  *bytes_out = bytes;
+  return 0;
+}
+extern "C" int mec_trace_read(void* host, const void* dev, size_t bytes) {
+  return cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+}
+#else
+#define MEC_TRACE_EV(tl, ev) \
+  do {                       \
+  } while (0)
+#endif
+
 namespace mec {
 namespace {
 
-constexpr int kThreads = 192;
-constexpr int kATileBytes = kBM * kTileKBytes;  // 16 KB
+constexpr int kEpiGroups = 2;  // epilogue warp-groups, alternating tiles
+constexpr int kThreads = 64 + kEpiGroups * 128;
+constexpr int kAtomBytes = kBM * kTileKBytes;  // 16 KB: 128 rows x 128 B
+constexpr int kAtomsPerStage = 2;
+constexpr int kStageABytes = kAtomsPerStage * kAtomBytes;
+constexpr int kMaxCombos = 32;  // n_var (<= 8) x N tiles (<= 4 for k_c <= 1024)
+constexpr int kEpiWarps = 4 * kEpiGroups;
 
 struct GemmParams {
   void* O;
   int64_t o_h, o_w, i_n, k_c;
+  // row tiling.  flat: the batch-folded rows n o_w + w in 128-row tiles (one
+  // group).  packed: `ipt` images per tile, image j in TMEM lanes
+  // [j S, j S + S) (S = o_w rounded up to 32), so no 32-row epilogue block
+  // straddles two images; ipt = 1 is one image per tile (Solution B, and
+  // Solution A when o_w > 64).
+  bool flat;
+  int ipt, slot;
   int64_t rows, groups, n_mt;
   int64_t shift;
-  int vec, delta_step;
   int64_t kc_pad;
-  int bk;
-  int nk;           // K-tiles per window
+  int bk;           // K-atom width in elements (64 bf16 / 32 fp32)
+  int n_atoms;      // K-atoms per window
+  int n_kstages;    // ceil(n_atoms / 2)
   int bn, n_tiles_n;
-  int64_t num_tiles;
+  int n_var;
+  int n_combo;      // n_var * n_tiles_n
+  int ctas_per_combo;
+  int h_first[8];   // smallest h with weight variant v
   int stages;
+  bool resident;    // weight operand resident in smem
   uint32_t tmem_cols;
+  int n_acc;        // TMEM accumulator buffers (4 if 4 bn <= 512, else 2)
   uint32_t idesc;
   bool out_hnwc;
-  bool vec_ok;
+  bool tma_store;   // epilogue via TMA stores (k_c elt multiple of 16)
+  int pw;           // epilogue pass width (columns); pw * out_elt = 128 / 64 / 32 bytes
+  int n_pass;       // bn / pw
+  uint32_t stage_out_bytes;  // staging bytes per epilogue warp (32 rows x pw x elt, 1 KB aligned)
+  int dbg;  // trace builds only: 1 = no epilogue stores, 2 = no MMA, 4 = no A loads
 };
 
 struct TileCoord {
-  int64_t nt, h, mt, g;
+  int64_t h, mt, g;
 };
 
-__device__ __forceinline__ TileCoord decode_tile(const GemmParams& p, int64_t t) {
+// Combo c = v * n_tiles_n + nt.  Tile t of the combo: h-index fastest, then
+// row tile, then group.
+__device__ __forceinline__ int64_t combo_tiles(const GemmParams& p, int v) {
+  const int64_t nh = (p.o_h - p.h_first[v] + p.n_var - 1) / p.n_var;
+  return nh * p.n_mt * p.groups;
+}
+
+__device__ __forceinline__ TileCoord decode_tile(const GemmParams& p, int v, int64_t t) {
+  const int64_t nh = (p.o_h - p.h_first[v] + p.n_var - 1) / p.n_var;
   TileCoord c;
-  c.nt = t % p.n_tiles_n;
-  t /= p.n_tiles_n;
-  c.h = t % p.o_h;
-  t /= p.o_h;
+  const int64_t hi = t % nh;
+  t /= nh;
+  c.h = p.h_first[v] + hi * p.n_var;
   c.mt = t % p.n_mt;
   c.g = t / p.n_mt;
   return c;
@@ -104,35 +177,49 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 template <bool kTF32>
 __global__ void __launch_bounds__(kThreads, 1)
     window_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                       const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+                       const __grid_constant__ CUtensorMap tmB,
+                       const __grid_constant__ CUtensorMap tmO, const GemmParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + kSmemAlign - 1) & ~uintptr_t(kSmemAlign - 1));
   const int S = p.stages;
   const uint32_t b_tile_bytes = static_cast<uint32_t>(p.bn) * kTileKBytes;
+  // smem: [S A-stages][B: n_atoms resident tiles or S x 2 streamed][epi staging][barriers]
+  const int nb = p.resident ? p.n_atoms : S * kAtomsPerStage;
   unsigned char* smemA = smem;
-  unsigned char* smemB = smem + static_cast<size_t>(S) * kATileBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smemB + static_cast<size_t>(S) * b_tile_bytes);
+  unsigned char* smemB = smem + static_cast<size_t>(S) * kStageABytes;
+  unsigned char* smemE = smemB + static_cast<size_t>(nb) * b_tile_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smemE + static_cast<size_t>(kEpiWarps) * p.stage_out_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
-  uint64_t* tempty = bars + 2 * S + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+  uint64_t* tempty = bars + 2 * S + 4;
+  uint64_t* bfull = bars + 2 * S + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 9);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // this CTA's combo: weight variant v and N tile nt
+  const int combo = blockIdx.x % p.n_combo;
+  const int v = combo / p.n_tiles_n;
+  const int nt = combo % p.n_tiles_n;
+  const int64_t t_begin = blockIdx.x / p.n_combo;
+  const int64_t t_step = p.ctas_per_combo;
+  const int64_t n_tiles = combo_tiles(p, v);
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
+    ptx::tma_prefetch_desc(&tmO);
     for (int i = 0; i < S; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 4);
+      ptx::mbar_init(&tempty[i], 4);  // the 4 warps of one epilogue group
     }
+    ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc_dyn(tmem_slot, p.tmem_cols);
@@ -140,64 +227,102 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) MEC_TRACE_EV(0, 7);
+  const int32_t b_row0 = static_cast<int32_t>(v * p.kc_pad + nt * p.bn);
 
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
       const uint64_t hintA = ptx::policy_evict_normal();
       const uint64_t hintB = ptx::policy_evict_last();
+      if (p.resident && t_begin < n_tiles) {
+        ptx::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(p.n_atoms) * b_tile_bytes);
+        for (int a = 0; a < p.n_atoms; ++a)
+          ptx::tma_load_2d(smemB + static_cast<size_t>(a) * b_tile_bytes, &tmB, bfull, a * p.bk,
+                           b_row0, hintB);
+      }
+      constexpr int64_t kVec = kTF32 ? 4 : 8;  // elements per 16 bytes
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        const TileCoord c = decode_tile(p, t);
-        // window start h*shift, rounded down to a 16-byte boundary (TMA rule);
-        // the delta-shifted weight copy absorbs the difference
+      for (int64_t t = t_begin; t < n_tiles; t += t_step) {
+        const int tl = static_cast<int>((t - t_begin) / t_step);
+        MEC_TRACE_EV(tl, 0);
+        const TileCoord c = decode_tile(p, v, t);
+        // window start h*shift rounded down to 16 bytes (TMA rule); variant v absorbs delta
         const int64_t xw = c.h * p.shift;
-        const int64_t delta = xw % p.vec;
-        const int32_t x0 = static_cast<int32_t>(xw - delta);
+        const int32_t x0 = static_cast<int32_t>(xw - xw % kVec);
         const int32_t y0 = static_cast<int32_t>(c.mt * kBM);
         const int32_t z0 = static_cast<int32_t>(c.g);
-        const int32_t n0 = static_cast<int32_t>((delta / p.delta_step) * p.kc_pad + c.nt * p.bn);
-        for (int kt = 0; kt < p.nk; ++kt) {
+        for (int ks = 0; ks < p.n_kstages; ++ks) {
+          const int na = min(kAtomsPerStage, p.n_atoms - ks * kAtomsPerStage);
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[stage], kATileBytes + b_tile_bytes);
-          ptx::tma_load_3d(smemA + static_cast<size_t>(stage) * kATileBytes, &tmA, &full[stage],
-                           x0 + kt * p.bk, y0, z0, hintA);
-          ptx::tma_load_2d(smemB + static_cast<size_t>(stage) * b_tile_bytes, &tmB, &full[stage],
-                           kt * p.bk, n0, hintB);
+          if (p.dbg & 4) {
+            ptx::mbar_arrive(&full[stage]);
+          } else {
+            ptx::mbar_arrive_expect_tx(
+                &full[stage], static_cast<uint32_t>(na) * (kAtomBytes + (p.resident ? 0u : b_tile_bytes)));
+            for (int a = 0; a < na; ++a) {
+              const int atom = ks * kAtomsPerStage + a;
+              unsigned char* dstA = smemA + static_cast<size_t>(stage) * kStageABytes + a * kAtomBytes;
+              if (p.ipt <= 1) {
+                ptx::tma_load_3d(dstA, &tmA, &full[stage], x0 + atom * p.bk, y0, z0, hintA);
+              } else {  // one box of `slot` rows per image of the tile (images >= i_n: zero fill)
+                for (int j = 0; j < p.ipt; ++j)
+                  ptx::tma_load_3d(dstA + j * p.slot * kTileKBytes, &tmA, &full[stage],
+                                   x0 + atom * p.bk, 0, z0 * p.ipt + j, hintA);
+              }
+              if (!p.resident)
+                ptx::tma_load_2d(smemB + static_cast<size_t>(stage * kAtomsPerStage + a) * b_tile_bytes,
+                                 &tmB, &full[stage], atom * p.bk, b_row0, hintB);
+            }
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
+        MEC_TRACE_EV(tl, 1);
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     int stage = 0;
     uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    const uint32_t a_base = ptx::smem_u32(smemA);
-    const uint32_t b_base = ptx::smem_u32(smemB);
-    for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    const uint64_t a_desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smemA));
+    const uint64_t b_desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smemB));
+    if (p.resident && t_begin < n_tiles) ptx::mbar_wait(bfull, 0);
+    for (int64_t t = t_begin; t < n_tiles; t += t_step) {
+      const int tl = static_cast<int>((t - t_begin) / t_step);
+      const int acc = tl % p.n_acc;
+      const uint32_t acc_phase = static_cast<uint32_t>(tl / p.n_acc) & 1u;
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
+      if (lane == 0) MEC_TRACE_EV(tl, 2);
       const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * p.bn);
-      for (int kt = 0; kt < p.nk; ++kt) {
+      for (int ks = 0; ks < p.n_kstages; ++ks) {
+        const int na = min(kAtomsPerStage, p.n_atoms - ks * kAtomsPerStage);
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
+        if (ks == 0 && lane == 0) MEC_TRACE_EV(tl, 3);
         if (ptx::elect_one()) {
-          const uint32_t a_addr = a_base + stage * kATileBytes;
-          const uint32_t b_addr = b_base + stage * b_tile_bytes;
+          // descriptor start-address field is in 16-byte units
+          const uint32_t a_off = static_cast<uint32_t>(stage * kStageABytes) >> 4;
+          for (int a = 0; a < na; ++a) {
+            const uint32_t b_atom = p.resident ? static_cast<uint32_t>(ks * kAtomsPerStage + a)
+                                               : static_cast<uint32_t>(stage * kAtomsPerStage + a);
+            const uint64_t ad = a_desc0 + a_off + static_cast<uint32_t>(a * (kAtomBytes >> 4));
+            const uint64_t bd = b_desc0 + ((b_atom * b_tile_bytes) >> 4);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {  // 4 x 32 B = one 128-byte K-tile row
-            ptx::mma_ss<kTF32>(d_tmem, ptx::smem_desc_sw128(a_addr + 32 * k),
-                               ptx::smem_desc_sw128(b_addr + 32 * k), p.idesc,
-                               (kt | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < 4; ++k) {  // 4 x 32 B = one 128-byte atom row
+              if (p.dbg & 2) break;
+              ptx::mma_ss<kTF32>(d_tmem, ad + 2 * k, bd + 2 * k, p.idesc, (ks | a | k) != 0 ? 1u : 0u);
+            }
           }
           ptx::mma_commit(&empty[stage]);
-          if (kt == p.nk - 1) ptx::mma_commit(&tfull[acc]);
+          if (ks == p.n_kstages - 1) {
+            ptx::mma_commit(&tfull[acc]);
+            MEC_TRACE_EV(tl, 4);
+          }
         }
         __syncwarp();
         if (++stage == S) {
@@ -205,79 +330,174 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       }
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
     }
   } else {
-    // ===================== epilogue (warps 2..5) =====================
+    // ===================== epilogue (warps 2..9: two groups) =====================
     const int quarter = warp & 3;  // TMEM lanes [32 quarter, 32 quarter + 32)
-    const int row_in_tile = quarter * 32 + lane;
+    const int group = (warp - 2) >> 2;  // group g takes tiles tl = g, g + 2, ...
     constexpr int kOutElt = kTF32 ? 4 : 2;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      const TileCoord c = decode_tile(p, t);
+    const uint32_t stg = ptx::smem_u32(smemE) + static_cast<uint32_t>(warp - 2) * p.stage_out_bytes;
+    const int row_bytes = p.pw * kOutElt;  // 128, 64 or 32
+    // swizzle of the staging box (matches the O tensor map): chunk c of row r
+    // lives at chunk c ^ f(r) -- conflict-free 16-byte stores
+    const int swz_shift = row_bytes == 128 ? 0 : (row_bytes == 64 ? 1 : 2);
+    const int swz_mask = row_bytes == 128 ? 7 : (row_bytes == 64 ? 3 : 1);
+    const uint32_t my_row = stg + static_cast<uint32_t>(lane * row_bytes);
+    const uint32_t my_x = static_cast<uint32_t>((lane >> swz_shift) & swz_mask);
+    const int64_t cols_left = p.k_c - static_cast<int64_t>(nt) * p.bn;
+    for (int64_t t = t_begin + group * t_step; t < n_tiles; t += kEpiGroups * t_step) {
+      const int tl = static_cast<int>((t - t_begin) / t_step);
+      const int acc = tl % p.n_acc;
+      const uint32_t acc_phase = static_cast<uint32_t>(tl / p.n_acc) & 1u;
+      const TileCoord c = decode_tile(p, v, t);
+      // this warp's 32 rows: image n, columns w0 .. w0 + nvalid - 1 (packed), or
+      // flattened rows gr0 .. gr0 + nvalid - 1 (flat)
+      int64_t gr0, nvalid, n_img = 0, w0 = 0;
+      if (p.flat) {
+        const int64_t r0 = c.mt * kBM + quarter * 32;
+        nvalid = min(static_cast<int64_t>(32), p.rows - r0);
+        gr0 = r0;
+      } else {
+        const int j = (quarter * 32) / p.slot;
+        n_img = c.g * p.ipt + j;
+        w0 = c.mt * kBM + quarter * 32 - j * p.slot;
+        nvalid = n_img < p.i_n ? min(static_cast<int64_t>(32), p.o_w - w0) : 0;
+        gr0 = n_img * p.o_w + w0;
+      }
+      // this lane's output row: O[n, h, w] (or O_hnwc[h, n o_w + w]) at column nt*bn
+      unsigned char* orow_own;
+      {
+        const int64_t gr = gr0 + lane;
+        int64_t out_row;
+        if (p.out_hnwc) {
+          out_row = c.h * (p.i_n * p.o_w) + gr;
+        } else {
+          const int64_t n = gr / p.o_w, w = gr - n * p.o_w;
+          out_row = (n * p.o_h + c.h) * p.o_w + w;
+        }
+        orow_own = static_cast<unsigned char*>(p.O) +
+                   (out_row * p.k_c + static_cast<int64_t>(nt) * p.bn) * kOutElt;
+      }
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      const int64_t r = c.mt * kBM + row_in_tile;
-      const bool valid = r < p.rows;
-      const int64_t gr = c.g * p.rows + r;  // flattened (n, w) row of L
-      int64_t out_row;
-      if (p.out_hnwc) {
-        out_row = c.h * (p.i_n * p.o_w) + gr;  // O_hnwc[h, n o_w + w]
-      } else {
-        const int64_t n = gr / p.o_w, w = gr - n * p.o_w;
-        out_row = (n * p.o_h + c.h) * p.o_w + w;  // O[n, h, w]
-      }
-      unsigned char* orow =
-          static_cast<unsigned char*>(p.O) + (out_row * p.k_c + c.nt * p.bn) * kOutElt;
-      const int64_t cols_left = p.k_c - c.nt * p.bn;  // valid columns in this N tile
-      const uint32_t taddr =
-          tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * p.bn);
-      for (int c0 = 0; c0 < p.bn; c0 += 16) {
-        uint32_t v[16];
-        ptx::tmem_ld_32x32b_x16(taddr + c0, v);
+      if ((warp & 3) == 2 && lane == 0) MEC_TRACE_EV(tl, 5);
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                             static_cast<uint32_t>(acc * p.bn);
+      for (int pass = 0; pass < p.n_pass; ++pass) {
+        const int c0 = pass * p.pw;
+        uint32_t v16[4][16];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j * 16 < p.pw) ptx::tmem_ld_32x32b_x16(taddr + c0 + 16 * j, v16[j]);
         ptx::tmem_ld_wait();
-        if (!valid || c0 >= cols_left) continue;
-        if constexpr (kTF32) {
-          if (p.vec_ok) {
+        if ((warp & 3) == 2 && lane == 0 && pass < 2) MEC_TRACE_EV(tl, 8 + 4 * pass);
+        if (nvalid <= 0 || c0 >= cols_left) continue;  // warp-uniform
+        if (p.tma_store) {
+          // the previous pass's TMA store must have finished reading the staging box
+          if (lane == 0) ptx::bulk_wait_group_read<0>();
+          __syncwarp();
+          if ((warp & 3) == 2 && lane == 0 && pass < 2) MEC_TRACE_EV(tl, 10 + 4 * pass);
+          const int nchunk = row_bytes / 16;
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (c0 + 4 * j + 4 <= cols_left)
-                *reinterpret_cast<uint4*>(orow + (c0 + 4 * j) * 4) =
-                    make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          } else {
-            for (int j = 0; j < 16 && c0 + j < cols_left; ++j)
-              reinterpret_cast<uint32_t*>(orow)[c0 + j] = v[j];
+          for (int ch = 0; ch < 8; ++ch) {
+            if (ch >= nchunk) break;
+            uint32_t q0, q1, q2, q3;
+            if constexpr (kTF32) {
+              const int j = ch >> 2, e = (ch & 3) * 4;
+              q0 = v16[j][e];
+              q1 = v16[j][e + 1];
+              q2 = v16[j][e + 2];
+              q3 = v16[j][e + 3];
+            } else {
+              const int j = ch >> 1, e = (ch & 1) * 8;
+              q0 = pack_bf16x2(__uint_as_float(v16[j][e]), __uint_as_float(v16[j][e + 1]));
+              q1 = pack_bf16x2(__uint_as_float(v16[j][e + 2]), __uint_as_float(v16[j][e + 3]));
+              q2 = pack_bf16x2(__uint_as_float(v16[j][e + 4]), __uint_as_float(v16[j][e + 5]));
+              q3 = pack_bf16x2(__uint_as_float(v16[j][e + 6]), __uint_as_float(v16[j][e + 7]));
+            }
+            ptx::st_shared_v4(my_row + ((static_cast<uint32_t>(ch) ^ my_x) << 4), q0, q1, q2, q3);
           }
-        } else {
-          uint32_t pk[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            pk[j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-          if (p.vec_ok) {
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-              if (c0 + 8 * j + 8 <= cols_left)
-                *reinterpret_cast<uint4*>(orow + (c0 + 8 * j) * 2) =
-                    make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if ((warp & 3) == 2 && lane == 0 && pass < 2) MEC_TRACE_EV(tl, 9 + 4 * pass);
+          const int32_t col = static_cast<int32_t>(nt * p.bn + c0);
+          if (!p.flat) {
+            // packed: the 32 rows lie in image n_img (rows past o_w are clipped)
+            if (lane == 0 && !(p.dbg & 1)) {
+              if (p.out_hnwc)  // O_hnwc as {k_c, o_w, i_n, o_h}
+                ptx::tma_store_4d(&tmO, smemE + (warp - 2) * p.stage_out_bytes, col,
+                                  static_cast<int32_t>(w0), static_cast<int32_t>(n_img),
+                                  static_cast<int32_t>(c.h));
+              else  // O as {k_c, o_w, o_h, i_n}
+                ptx::tma_store_4d(&tmO, smemE + (warp - 2) * p.stage_out_bytes, col,
+                                  static_cast<int32_t>(w0), static_cast<int32_t>(c.h),
+                                  static_cast<int32_t>(n_img));
+              ptx::bulk_commit_group();
+            }
+          } else if (p.out_hnwc) {
+            if (lane == 0 && !(p.dbg & 1)) {
+              ptx::tma_store_3d(&tmO, smemE + (warp - 2) * p.stage_out_bytes, col,
+                                static_cast<int32_t>(gr0), static_cast<int32_t>(c.h));
+              ptx::bulk_commit_group();
+            }
           } else {
-            for (int j = 0; j < 16 && c0 + j < cols_left; ++j)
-              reinterpret_cast<uint16_t*>(orow)[c0 + j] =
-                  static_cast<uint16_t>(pk[j >> 1] >> ((j & 1) * 16));
+            // rows of the first image: one TMA store (rows past o_w are clipped);
+            // TMA stores reject negative coordinates, so the rows of any later
+            // image in this 32-row block are stored from the staging box by the
+            // warp (16 B per lane, coalesced)
+            const int64_t n_first = gr0 / p.o_w;
+            const int k_first = static_cast<int>(min(nvalid, (n_first + 1) * p.o_w - gr0));
+            if (lane == 0 && !(p.dbg & 1)) {
+              ptx::tma_store_4d(&tmO, smemE + (warp - 2) * p.stage_out_bytes, col,
+                                static_cast<int32_t>(gr0 - n_first * p.o_w), static_cast<int32_t>(c.h),
+                                static_cast<int32_t>(n_first));
+              ptx::bulk_commit_group();
+            }
+            if (k_first < nvalid && !(p.dbg & 1)) {
+              const int lg = nchunk == 8 ? 3 : (nchunk == 4 ? 2 : 1);
+              const int nrest = static_cast<int>(nvalid) - k_first;
+              const int total = nrest * nchunk;
+              for (int ci0 = 0; ci0 < total; ci0 += 32) {  // warp-uniform trip count
+                const int ci = min(ci0 + lane, total - 1);
+                const int row = k_first + (ci >> lg), ch = ci & (nchunk - 1);
+                const unsigned long long base =
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(orow_own), row);
+                const uint32_t x = static_cast<uint32_t>((row >> swz_shift) & swz_mask);
+                const uint4 val = ptx::ld_shared_v4(stg + static_cast<uint32_t>(row * row_bytes) +
+                                                    ((static_cast<uint32_t>(ch) ^ x) << 4));
+                if (ci0 + lane < total)
+                  *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(base) + c0 * kOutElt + ch * 16) =
+                      val;
+              }
+            }
+          }
+        } else if (lane < nvalid) {
+          // k_c * elt not a multiple of 16 (or k_c not a multiple of the pass
+          // width): element stores from registers
+          unsigned char* orow = orow_own;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int col = c0 + j * 16 + e;
+              if (j * 16 + e < p.pw && col < cols_left) {
+                if constexpr (kTF32) {
+                  reinterpret_cast<uint32_t*>(orow)[col] = v16[j][e];
+                } else {
+                  const uint32_t pkd = pack_bf16x2(__uint_as_float(v16[j][e]), 0.0f);
+                  reinterpret_cast<uint16_t*>(orow)[col] = static_cast<uint16_t>(pkd & 0xFFFFu);
+                }
+              }
+            }
           }
         }
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
+      if ((warp & 3) == 2 && lane == 0) MEC_TRACE_EV(tl, 6);
     }
+    if (lane == 0) ptx::bulk_wait_group<0>();
   }
 
   ptx::tc_fence_before();
@@ -293,14 +513,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st,
                                int* launches) {
   const bool tf32 = pl.dt == MEC_DTYPE_TF32;
-  CUtensorMap tmA, tmB;
-  // A: the lowered tensor L viewed as {columns, rows, groups} (Alg.2 l.9 / l.21).
+  const int out_elt = pl.elt;
+  CUtensorMap tmA, tmB, tmO;
+  // Row tiling (see GemmParams): Solution A with o_w < 32 folds flat (a
+  // 32-row epilogue block then spans several images); otherwise image slots.
+  const bool flat = a.batch_folded && pl.o_w < 32;
+  int slot = 128, ipt = 1;
+  if (!flat && pl.o_w <= 128) {
+    slot = static_cast<int>((pl.o_w + 31) / 32 * 32);
+    if (a.batch_folded) ipt = std::max(1, 128 / slot);
+    if (ipt == 1) slot = 128;
+  }
+  const int64_t rows = flat ? pl.s.i_n * pl.o_w : pl.o_w;
+  const int64_t groups = flat ? 1 : (pl.s.i_n + ipt - 1) / ipt;
+  const int64_t n_mt = flat ? (rows + kBM - 1) / kBM : (ipt > 1 ? 1 : (pl.o_w + kBM - 1) / kBM);
+  // A: the lowered tensor L (Alg.2 l.9 / l.21) as {columns, rows, groups}:
+  // flat {i_h k_w i_c, i_n o_w, 1}, else per image {i_h k_w i_c, o_w, i_n}.
   {
-    const uint64_t dims[3] = {static_cast<uint64_t>(pl.l_cols), static_cast<uint64_t>(a.rows),
-                              static_cast<uint64_t>(a.groups)};
+    const uint64_t dims[3] = {static_cast<uint64_t>(pl.l_cols), static_cast<uint64_t>(rows),
+                              static_cast<uint64_t>(flat ? 1 : pl.s.i_n)};
     const uint64_t strides[2] = {static_cast<uint64_t>(pl.pitch) * pl.elt,
-                                 static_cast<uint64_t>(pl.pitch) * pl.elt * a.rows};
-    const uint32_t box[3] = {static_cast<uint32_t>(pl.bk), kBM, 1};
+                                 static_cast<uint64_t>(pl.pitch) * pl.elt * rows};
+    const uint32_t box[3] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(ipt > 1 ? slot : kBM), 1};
     cudaError_t e = encode_tiled(&tmA, tf32, 3, a.L, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
@@ -320,39 +554,114 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   p.o_w = pl.o_w;
   p.i_n = pl.s.i_n;
   p.k_c = pl.s.k_c;
-  p.rows = a.rows;
-  p.groups = a.groups;
-  p.n_mt = (a.rows + kBM - 1) / kBM;
+  p.flat = flat;
+  p.ipt = ipt;
+  p.slot = slot;
+  p.rows = rows;
+  p.groups = groups;
+  p.n_mt = n_mt;
   p.shift = pl.shift;
-  p.vec = pl.vec;
-  p.delta_step = pl.delta_step;
   p.kc_pad = pl.kc_pad;
   p.bk = pl.bk;
-  p.nk = static_cast<int>(pl.kdim_pad / pl.bk);
+  p.n_atoms = static_cast<int>(pl.kdim_pad / pl.bk);
+  p.n_kstages = (p.n_atoms + kAtomsPerStage - 1) / kAtomsPerStage;
   p.bn = pl.bn;
   p.n_tiles_n = pl.n_tiles_n;
-  p.num_tiles = a.groups * p.n_mt * pl.o_h * pl.n_tiles_n;
+  p.n_var = pl.n_var;
+  p.n_combo = pl.n_var * pl.n_tiles_n;
+  if (p.n_combo > kMaxCombos) return cudaErrorInvalidConfiguration;
+  // first h of each weight variant: delta(h) = (h shift) mod vec = v delta_step
+  for (int v = 0; v < 8; ++v) p.h_first[v] = static_cast<int>(pl.o_h);  // none
+  for (int64_t h = 0; h < std::min<int64_t>(pl.o_h, pl.n_var); ++h) {
+    const int v = static_cast<int>(((h * pl.shift) % pl.vec) / pl.delta_step);
+    if (p.h_first[v] > h) p.h_first[v] = static_cast<int>(h);
+  }
   p.out_hnwc = a.out_hnwc;
-  p.vec_ok = ((pl.s.k_c * pl.elt) % 16 == 0) && (reinterpret_cast<uintptr_t>(a.O) % 16 == 0);
+#ifdef MEC_TRACE
+  if (const char* e = getenv("MEC_DEBUG_FLAGS")) p.dbg = atoi(e);
+#endif
   p.idesc = ptx::instr_desc(tf32, kBM, pl.bn);
+  p.n_acc = 4 * pl.bn <= 512 ? 4 : 2;
   uint32_t cols = 32;
-  while (cols < 2u * pl.bn) cols <<= 1;
+  while (cols < static_cast<uint32_t>(p.n_acc * pl.bn)) cols <<= 1;
   p.tmem_cols = cols;
 
-  const size_t stage_bytes = kATileBytes + static_cast<size_t>(pl.bn) * kTileKBytes;
-  const size_t budget = 220 * 1024;
-  int stages = static_cast<int>(std::min<size_t>(8, budget / stage_bytes));
-  stages = std::max(2, std::min<int>(stages, std::max(2, p.nk * 2)));
-  p.stages = stages;
-  const size_t smem = kSmemAlign + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+  // epilogue: pass width = 128 / 64 / 32 bytes per row, dividing bn
+  p.tma_store = ((pl.s.k_c * out_elt) % 16 == 0) && (reinterpret_cast<uintptr_t>(a.O) % 16 == 0);
+  int row_bytes = 128;
+  while (row_bytes > 32 && (pl.bn * out_elt) % row_bytes != 0) row_bytes /= 2;
+  p.pw = row_bytes / out_elt;
+  p.n_pass = pl.bn / p.pw;
+  // a store box wider than the tensor's k_c extent traps (seen on B200 for
+  // k_c = 8 with a 16-column box): such shapes use the register-store path
+  if (pl.s.k_c % p.pw != 0) p.tma_store = false;
+  p.stage_out_bytes = static_cast<uint32_t>(32 * row_bytes);  // 1-4 KB, swizzle-atom aligned
+  if (p.tma_store) {
+    if (a.out_hnwc && flat) {  // O_hnwc viewed as {k_c, i_n o_w, o_h}
+      const uint64_t dims[3] = {static_cast<uint64_t>(pl.s.k_c),
+                                static_cast<uint64_t>(pl.s.i_n * pl.o_w),
+                                static_cast<uint64_t>(pl.o_h)};
+      const uint64_t strides[2] = {static_cast<uint64_t>(pl.s.k_c) * out_elt,
+                                   static_cast<uint64_t>(pl.s.i_n * pl.o_w * pl.s.k_c) * out_elt};
+      const uint32_t box[3] = {static_cast<uint32_t>(p.pw), 32, 1};
+      cudaError_t e = encode_tiled_swz(&tmO, tf32, 3, a.O, dims, strides, box, row_bytes);
+      if (e != cudaSuccess) return e;
+    } else if (a.out_hnwc) {  // O_hnwc viewed as {k_c, o_w, i_n, o_h}
+      const uint64_t dims[4] = {static_cast<uint64_t>(pl.s.k_c), static_cast<uint64_t>(pl.o_w),
+                                static_cast<uint64_t>(pl.s.i_n), static_cast<uint64_t>(pl.o_h)};
+      const uint64_t strides[3] = {static_cast<uint64_t>(pl.s.k_c) * out_elt,
+                                   static_cast<uint64_t>(pl.o_w * pl.s.k_c) * out_elt,
+                                   static_cast<uint64_t>(pl.s.i_n * pl.o_w * pl.s.k_c) * out_elt};
+      const uint32_t box[4] = {static_cast<uint32_t>(p.pw), 32, 1, 1};
+      cudaError_t e = encode_tiled_swz(&tmO, tf32, 4, a.O, dims, strides, box, row_bytes);
+      if (e != cudaSuccess) return e;
+    } else {  // O viewed as {k_c, o_w, o_h, i_n}
+      const uint64_t dims[4] = {static_cast<uint64_t>(pl.s.k_c), static_cast<uint64_t>(pl.o_w),
+                                static_cast<uint64_t>(pl.o_h), static_cast<uint64_t>(pl.s.i_n)};
+      const uint64_t strides[3] = {static_cast<uint64_t>(pl.s.k_c) * out_elt,
+                                   static_cast<uint64_t>(pl.o_w * pl.s.k_c) * out_elt,
+                                   static_cast<uint64_t>(pl.o_h * pl.o_w * pl.s.k_c) * out_elt};
+      const uint32_t box[4] = {static_cast<uint32_t>(p.pw), 32, 1, 1};
+      cudaError_t e = encode_tiled_swz(&tmO, tf32, 4, a.O, dims, strides, box, row_bytes);
+      if (e != cudaSuccess) return e;
+    }
+  } else {
+    std::memset(&tmO, 0, sizeof(tmO));
+  }
 
-  const int64_t grid = std::min<int64_t>(p.num_tiles, num_sms());
-  if (grid <= 0) return cudaSuccess;
+  const size_t b_tile = static_cast<size_t>(pl.bn) * kTileKBytes;
+  const size_t b_res = b_tile * p.n_atoms;
+  const size_t epi = static_cast<size_t>(kEpiWarps) * p.stage_out_bytes;
+  const size_t budget = 222 * 1024 - epi;  // after the 1 KB alignment slack
+  p.resident = b_res + 2 * kStageABytes <= budget && b_res <= 120 * 1024;
+  int stages;
+  if (p.resident) {
+    stages = static_cast<int>(std::min<size_t>(8, (budget - b_res) / kStageABytes));
+  } else {
+    stages = static_cast<int>(std::min<size_t>(8, budget / (kStageABytes + kAtomsPerStage * b_tile)));
+  }
+  stages = std::max(1, std::min(stages, std::max(2, 2 * p.n_kstages)));
+  p.stages = stages;
+  const size_t smem = kSmemAlign + stages * static_cast<size_t>(kStageABytes) +
+                      (p.resident ? b_res : stages * kAtomsPerStage * b_tile) + epi +
+                      (2 * stages + 10) * 8 + 16;
+
+  // grid: a multiple of the combo count, at most one CTA per SM
+  int64_t max_tiles = 0;
+  for (int v = 0; v < pl.n_var; ++v) {
+    const int64_t nh = (pl.o_h - p.h_first[v] + pl.n_var - 1) / pl.n_var;
+    max_tiles = std::max<int64_t>(max_tiles, std::max<int64_t>(0, nh) * p.n_mt * groups);
+  }
+  if (max_tiles == 0) return cudaSuccess;
+  int64_t per = std::max<int64_t>(1, num_sms() / p.n_combo);
+  per = std::min<int64_t>(per, max_tiles);
+  p.ctas_per_combo = static_cast<int>(per);
+  const int64_t grid = per * p.n_combo;
   auto kern = tf32 ? window_gemm_kernel<true> : window_gemm_kernel<false>;
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(tmA, tmB, p);
+  kern<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(tmA, tmB, tmO, p);
   if (launches) ++*launches;
   return cudaGetLastError();
 }
