@@ -68,15 +68,15 @@ __device__ __forceinline__ void prep_weight_tile(const LowerParams& p, int64_t t
   tile -= v * tiles_j * tiles_c;
   const int64_t jt = tile % tiles_j, ct = tile / tiles_j;
   const int64_t delta = v * p.delta_step;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const T* K = reinterpret_cast<const T*>(p.K);
   T* Kt = reinterpret_cast<T*>(p.Kt) + v * p.kc_pad * p.kdim_pad;
-  for (int r = ty; r < 32; r += 8) {
+  for (int r = ty; r < 32; r += nw) {
     const int64_t j = jt * 32 + r - delta, c = ct * 32 + tx;
     tbuf[r][tx] = (j >= 0 && j < p.kdim && c < p.k_c) ? K[j * p.k_c + c] : T(0);
   }
   __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
+  for (int r = ty; r < 32; r += nw) {
     const int64_t c = ct * 32 + r, j = jt * 32 + tx;
     if (c < p.kc_pad && j < p.kdim_pad) Kt[c * p.kdim_pad + j] = tbuf[tx][r];
   }
@@ -184,32 +184,62 @@ __global__ void __launch_bounds__(256) lower_kernel(const LowerParams p) {
     __syncthreads();
     const uint32_t* W = reinterpret_cast<const uint32_t*>(smem);
     const bool odd_tail = (seg_bytes & 3u) != 0;  // last word holds one 2-byte element
+    unsigned char* L0 = p.L + (((n * p.o_w) * p.pitch + h0 * p.kwc) * sizeof(T));
+    const uint32_t pitch_bytes = static_cast<uint32_t>(p.pitch * sizeof(T));
+    const uint32_t wstep_bytes = p.wstep * static_cast<uint32_t>(sizeof(T));
+    // one warp per 32-word column block, looping over every output column w:
+    // the lane's table entries are decoded once; the inner loop is 2 LDS +
+    // PRMT + STG with incremental addresses (the launch sizes the block to
+    // the number of column blocks)
+    const uint32_t nblk = (seg_words + 31) / 32;
     const uint32_t full_words = odd_tail ? seg_words - 1 : seg_words;
-    // one warp per w: the segment pointer and table parity are hoisted, the
-    // inner loop is table LDS + 2 LDS + PRMT + STG per word
-    for (uint32_t w = warp; w < p.o_w; w += nwarps) {
-      const uint32_t wbyte = w * p.wstep * static_cast<uint32_t>(sizeof(T));
-      const uint32_t* tab = table + ((wbyte >> 1) & 1u) * seg_words;
-      const uint32_t* Wb = W + (wbyte >> 2);
-      uint32_t* dst = reinterpret_cast<uint32_t*>(
-          p.L + (((n * p.o_w + w) * p.pitch + h0 * p.kwc) * sizeof(T)));
-      for (uint32_t j = lane; j < full_words; j += 32) {
-        const uint32_t entry = tab[j];
-        const uint32_t x = Wb[entry & 0x7FFFu];
-        if constexpr (sizeof(T) == 4) {
-          dst[j] = x;
-        } else {
-          const uint32_t y = Wb[(entry >> 15) & 0x7FFFu];
-          const uint32_t selector = ((entry >> 30) & 1u ? 0x0032u : 0x0010u) |
-                                    ((entry >> 31) ? 0x7600u : 0x5400u);
-          dst[j] = __byte_perm(x, y, selector);
+    for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
+      const uint32_t j = jb * 32 + lane;
+      const bool active = j < full_words;
+      const uint32_t jj = j < seg_words ? j : seg_words - 1;
+      const uint32_t e0 = table[jj], e1 = table[seg_words + jj];
+      const uint32_t a0 = e0 & 0x7FFFu, b0 = (e0 >> 15) & 0x7FFFu;
+      const uint32_t a1 = e1 & 0x7FFFu, b1 = (e1 >> 15) & 0x7FFFu;
+      const uint32_t s0 = ((e0 >> 30) & 1u ? 0x0032u : 0x0010u) | ((e0 >> 31) ? 0x7600u : 0x5400u);
+      const uint32_t s1 = ((e1 >> 30) & 1u ? 0x0032u : 0x0010u) | ((e1 >> 31) ? 0x7600u : 0x5400u);
+      uint32_t wbyte = 0;
+      uint32_t* dst = reinterpret_cast<uint32_t*>(L0 + 4 * jj);
+      if (active && (wstep_bytes & 3u) == 0) {
+        // word-aligned column step (e.g. AlexNet conv1: 24 B): parity 0 always
+        const uint32_t wstep_words = wstep_bytes >> 2;
+        const uint32_t* xa = W + a0;
+        const uint32_t* xb = W + b0;
+        const uint32_t n_w = static_cast<uint32_t>(p.o_w);
+#pragma unroll 4
+        for (uint32_t w = 0; w < n_w; ++w) {
+          const uint32_t x = *xa;
+          uint32_t val = x;
+          if constexpr (sizeof(T) == 2) val = __byte_perm(x, *xb, s0);
+          *dst = val;
+          xa += wstep_words;
+          xb += wstep_words;
+          dst = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst) + pitch_bytes);
         }
-      }
-      if (odd_tail && lane == 0) {
-        const uint32_t entry = tab[seg_words - 1];
-        const uint32_t x = Wb[entry & 0x7FFFu];
-        const uint32_t lo = ((entry >> 30) & 1u) ? (x >> 16) : (x & 0xFFFFu);
-        reinterpret_cast<uint16_t*>(dst)[2 * (seg_words - 1)] = static_cast<uint16_t>(lo);
+      } else if (active) {
+        for (uint32_t w = 0; w < static_cast<uint32_t>(p.o_w); ++w) {
+          const bool par = (wbyte >> 1) & 1u;
+          const uint32_t* Wb = W + (wbyte >> 2);
+          const uint32_t x = Wb[par ? a1 : a0];
+          uint32_t val = x;
+          if constexpr (sizeof(T) == 2) val = __byte_perm(x, Wb[par ? b1 : b0], par ? s1 : s0);
+          *dst = val;
+          wbyte += wstep_bytes;
+          dst = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst) + pitch_bytes);
+        }
+      } else if (odd_tail && j == seg_words - 1) {  // the segment's last 2-byte element
+        for (uint32_t w = 0; w < static_cast<uint32_t>(p.o_w); ++w) {
+          const bool par = (wbyte >> 1) & 1u;
+          const uint32_t x = W[(wbyte >> 2) + (par ? a1 : a0)];
+          const uint32_t lo = ((par ? e1 : e0) >> 30) & 1u ? (x >> 16) : (x & 0xFFFFu);
+          *reinterpret_cast<uint16_t*>(dst) = static_cast<uint16_t>(lo);
+          wbyte += wstep_bytes;
+          dst = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst) + pitch_bytes);
+        }
       }
     }
     return;
@@ -328,6 +358,12 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   p.aligned = base_ok && (p.kwc % vec == 0) && (p.wstep % vec == 0) && (p.iwc % vec == 0) &&
               (pitch % vec == 0);
 
+  // general (word-table) path: one warp per 32-word column block of a segment
+  int threads = 256;
+  if (!p.aligned) {
+    const int64_t words = (hb * static_cast<int64_t>(p.kwc) * pl.elt + 3) / 4;
+    threads = static_cast<int>(32 * std::min<int64_t>(8, std::max<int64_t>(2, (words + 31) / 32)));
+  }
   const size_t staged = static_cast<size_t>(hb * row_bytes) + 96;
   p.table_off = static_cast<uint32_t>((staged + 15) / 16 * 16);
   const size_t seg_words = (static_cast<size_t>(hb) * p.kwc * pl.elt + 3) / 4;
@@ -338,12 +374,12 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(lower_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
-    lower_kernel<uint16_t><<<static_cast<unsigned>(grid), 256, smem, st>>>(p);
+    lower_kernel<uint16_t><<<static_cast<unsigned>(grid), threads, smem, st>>>(p);
   } else {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(lower_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
-    lower_kernel<uint32_t><<<static_cast<unsigned>(grid), 256, smem, st>>>(p);
+    lower_kernel<uint32_t><<<static_cast<unsigned>(grid), threads, smem, st>>>(p);
   }
   if (launches) ++*launches;
   return cudaGetLastError();

@@ -134,10 +134,21 @@ struct GemmParams {
   int n_combo;      // n_var * n_tiles_n
   int ctas_per_combo;
   int h_first[8];   // smallest h with weight variant v
+  // multi-row tiles: a tile computes R consecutive output rows h0 .. h0+R-1;
+  // it streams the union of their windows once (columns [h0 shift,
+  // (h0+R-1) shift + kdim)) and issues every A atom's MMAs into the R TMEM
+  // accumulators it overlaps, B addressed per 32-byte K chunk (needs
+  // shift % kchunk == 0, one weight variant, resident weights).  R = 1 is
+  // the one-window-per-tile schedule.
+  int R;
+  int kchunk;       // elements per 32-byte MMA K step (16 bf16 / 8 tf32)
+  int kchunk_log2;
+  int n_chunks;     // ceil(kdim / kchunk): B chunks holding weights
+  int kdim;
   int stages;
   bool resident;    // weight operand resident in smem
   uint32_t tmem_cols;
-  int n_acc;        // TMEM accumulator buffers (4 if 4 bn <= 512, else 2)
+  int n_acc;        // TMEM accumulator sets (each R x bn columns)
   uint32_t idesc;
   bool out_hnwc;
   bool tma_store;   // epilogue via TMA stores (k_c elt multiple of 16)
@@ -148,24 +159,38 @@ struct GemmParams {
 };
 
 struct TileCoord {
-  int64_t h, mt, g;
+  int64_t h, mt, g;  // h = first output row of the tile
+  int r_eff;         // output rows in the tile (R, fewer at the end)
+  int n_a;           // A atoms streamed for the tile
 };
 
-// Combo c = v * n_tiles_n + nt.  Tile t of the combo: h-index fastest, then
+// h-slots of combo v: R == 1: h = h_first[v] + i n_var; R > 1: h0 = i R.
+__device__ __forceinline__ int64_t combo_hslots(const GemmParams& p, int v) {
+  return p.R == 1 ? (p.o_h - p.h_first[v] + p.n_var - 1) / p.n_var : (p.o_h + p.R - 1) / p.R;
+}
+
+// Combo c = v * n_tiles_n + nt.  Tile t of the combo: h-slot fastest, then
 // row tile, then group.
 __device__ __forceinline__ int64_t combo_tiles(const GemmParams& p, int v) {
-  const int64_t nh = (p.o_h - p.h_first[v] + p.n_var - 1) / p.n_var;
-  return nh * p.n_mt * p.groups;
+  return combo_hslots(p, v) * p.n_mt * p.groups;
 }
 
 __device__ __forceinline__ TileCoord decode_tile(const GemmParams& p, int v, int64_t t) {
-  const int64_t nh = (p.o_h - p.h_first[v] + p.n_var - 1) / p.n_var;
+  const int64_t nh = combo_hslots(p, v);
   TileCoord c;
   const int64_t hi = t % nh;
   t /= nh;
-  c.h = p.h_first[v] + hi * p.n_var;
   c.mt = t % p.n_mt;
   c.g = t / p.n_mt;
+  if (p.R == 1) {
+    c.h = p.h_first[v] + hi * p.n_var;
+    c.r_eff = 1;
+    c.n_a = p.n_atoms;
+  } else {
+    c.h = hi * p.R;
+    c.r_eff = static_cast<int>(min(static_cast<int64_t>(p.R), p.o_h - c.h));
+    c.n_a = static_cast<int>(((c.r_eff - 1) * p.shift + p.kdim + p.bk - 1) / p.bk);
+  }
   return c;
 }
 
@@ -197,7 +222,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bfull = bars + 2 * S + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 9);
 
-  const int warp = threadIdx.x >> 5;
+  // warp index broadcast from lane 0: provably warp-uniform, so role branches
+  // are uniform and the MMA issue loop keeps descriptors in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   // this CTA's combo: weight variant v and N tile nt
   const int combo = blockIdx.x % p.n_combo;
@@ -253,8 +280,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int32_t x0 = static_cast<int32_t>(xw - xw % kVec);
         const int32_t y0 = static_cast<int32_t>(c.mt * kBM);
         const int32_t z0 = static_cast<int32_t>(c.g);
-        for (int ks = 0; ks < p.n_kstages; ++ks) {
-          const int na = min(kAtomsPerStage, p.n_atoms - ks * kAtomsPerStage);
+        const int n_ks = (c.n_a + kAtomsPerStage - 1) / kAtomsPerStage;
+        for (int ks = 0; ks < n_ks; ++ks) {
+          const int na = min(kAtomsPerStage, c.n_a - ks * kAtomsPerStage);
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (p.dbg & 4) {
             ptx::mbar_arrive(&full[stage]);
@@ -290,38 +318,67 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     const uint64_t a_desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smemA));
     const uint64_t b_desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smemB));
+    const uint32_t b_tile16 = b_tile_bytes >> 4;
     if (p.resident && t_begin < n_tiles) ptx::mbar_wait(bfull, 0);
     for (int64_t t = t_begin; t < n_tiles; t += t_step) {
       const int tl = static_cast<int>((t - t_begin) / t_step);
+      const TileCoord c = decode_tile(p, v, t);
       const int acc = tl % p.n_acc;
       const uint32_t acc_phase = static_cast<uint32_t>(tl / p.n_acc) & 1u;
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
       if (lane == 0) MEC_TRACE_EV(tl, 2);
-      const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * p.bn);
-      for (int ks = 0; ks < p.n_kstages; ++ks) {
-        const int na = min(kAtomsPerStage, p.n_atoms - ks * kAtomsPerStage);
+      const uint32_t d_set = tmem_base + static_cast<uint32_t>(acc * p.R * p.bn);
+      const int n_ks = (c.n_a + kAtomsPerStage - 1) / kAtomsPerStage;
+      uint32_t started = 0;  // multi-row: accumulators that received an MMA
+      for (int ks = 0; ks < n_ks; ++ks) {
+        const int na = min(kAtomsPerStage, c.n_a - ks * kAtomsPerStage);
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
         if (ks == 0 && lane == 0) MEC_TRACE_EV(tl, 3);
-        if (ptx::elect_one()) {
-          // descriptor start-address field is in 16-byte units
+        {
+          // the whole warp runs the (warp-uniform) descriptor arithmetic; one
+          // elected lane issues each MMA / commit
           const uint32_t a_off = static_cast<uint32_t>(stage * kStageABytes) >> 4;
           for (int a = 0; a < na; ++a) {
-            const uint32_t b_atom = p.resident ? static_cast<uint32_t>(ks * kAtomsPerStage + a)
-                                               : static_cast<uint32_t>(stage * kAtomsPerStage + a);
             const uint64_t ad = a_desc0 + a_off + static_cast<uint32_t>(a * (kAtomBytes >> 4));
-            const uint64_t bd = b_desc0 + ((b_atom * b_tile_bytes) >> 4);
+            if (p.R == 1) {
+              const uint32_t b_atom = p.resident ? static_cast<uint32_t>(ks * kAtomsPerStage + a)
+                                                 : static_cast<uint32_t>(stage * kAtomsPerStage + a);
+              const uint64_t bd = b_desc0 + b_atom * b_tile16;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {  // 4 x 32 B = one 128-byte atom row
-              if (p.dbg & 2) break;
-              ptx::mma_ss<kTF32>(d_tmem, ad + 2 * k, bd + 2 * k, p.idesc, (ks | a | k) != 0 ? 1u : 0u);
+              for (int k = 0; k < 4; ++k) {  // 4 x 32 B = one 128-byte atom row
+                if (p.dbg & 2) break;
+                ptx::mma_ss_elect<kTF32>(d_set, ad + 2 * k, bd + 2 * k, p.idesc,
+                                         (ks | a | k) != 0 ? 1u : 0u);
+              }
+            } else {
+              // atom covers window positions o .. o + bk of output row h0 + r;
+              // its K chunk k pairs with B chunk (o / kchunk) + k
+              const int col0 = (ks * kAtomsPerStage + a) * p.bk;
+              for (int r = 0; r < c.r_eff; ++r) {
+                const int o = col0 - r * static_cast<int>(p.shift);
+                if (o + p.bk <= 0 || o >= p.kdim || (p.dbg & 2)) continue;
+                const int c0 = o >> p.kchunk_log2;  // exact: o is a multiple of kchunk
+                const uint32_t d_tmem = d_set + static_cast<uint32_t>(r * p.bn);
+                uint32_t accf = (started >> r) & 1u;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const int ch = c0 + k;
+                  if (ch < 0 || ch >= p.n_chunks) continue;
+                  const uint64_t bd =
+                      b_desc0 + static_cast<uint32_t>((ch >> 2) * static_cast<int>(b_tile16) + (ch & 3) * 2);
+                  ptx::mma_ss_elect<kTF32>(d_tmem, ad + 2 * k, bd, p.idesc, accf);
+                  accf = 1u;
+                }
+                started |= accf << r;
+              }
             }
           }
-          ptx::mma_commit(&empty[stage]);
-          if (ks == p.n_kstages - 1) {
-            ptx::mma_commit(&tfull[acc]);
-            MEC_TRACE_EV(tl, 4);
+          ptx::mma_commit_elect(&empty[stage]);
+          if (ks == n_ks - 1) {
+            ptx::mma_commit_elect(&tfull[acc]);
+            if (lane == 0) MEC_TRACE_EV(tl, 4);
           }
         }
         __syncwarp();
@@ -349,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tl = static_cast<int>((t - t_begin) / t_step);
       const int acc = tl % p.n_acc;
       const uint32_t acc_phase = static_cast<uint32_t>(tl / p.n_acc) & 1u;
-      const TileCoord c = decode_tile(p, v, t);
+      TileCoord c = decode_tile(p, v, t);
       // this warp's 32 rows: image n, columns w0 .. w0 + nvalid - 1 (packed), or
       // flattened rows gr0 .. gr0 + nvalid - 1 (flat)
       int64_t gr0, nvalid, n_img = 0, w0 = 0;
@@ -381,8 +438,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       if ((warp & 3) == 2 && lane == 0) MEC_TRACE_EV(tl, 5);
+      const int64_t h_tile = c.h;
+      for (int rr = 0; rr < c.r_eff; ++rr) {
+      c.h = h_tile + rr;  // output row stored by this sub-pass
+      if (rr > 0) orow_own += (p.out_hnwc ? p.i_n * p.o_w : p.o_w) * p.k_c * kOutElt;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                             static_cast<uint32_t>(acc * p.bn);
+                             static_cast<uint32_t>((acc * p.R + rr) * p.bn);
       for (int pass = 0; pass < p.n_pass; ++pass) {
         const int c0 = pass * p.pw;
         uint32_t v16[4][16];
@@ -492,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      }  // rows rr of the tile
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
@@ -581,10 +643,10 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   if (const char* e = getenv("MEC_DEBUG_FLAGS")) p.dbg = atoi(e);
 #endif
   p.idesc = ptx::instr_desc(tf32, kBM, pl.bn);
-  p.n_acc = 4 * pl.bn <= 512 ? 4 : 2;
-  uint32_t cols = 32;
-  while (cols < static_cast<uint32_t>(p.n_acc * pl.bn)) cols <<= 1;
-  p.tmem_cols = cols;
+  p.kchunk = 32 / pl.elt;
+  p.kchunk_log2 = pl.elt == 2 ? 4 : 3;
+  p.kdim = static_cast<int>(pl.kdim);
+  p.n_chunks = static_cast<int>((pl.kdim + p.kchunk - 1) / p.kchunk);
 
   // epilogue: pass width = 128 / 64 / 32 bytes per row, dividing bn
   p.tma_store = ((pl.s.k_c * out_elt) % 16 == 0) && (reinterpret_cast<uintptr_t>(a.O) % 16 == 0);
@@ -640,7 +702,23 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   } else {
     stages = static_cast<int>(std::min<size_t>(8, budget / (kStageABytes + kAtomsPerStage * b_tile)));
   }
+  // multi-row tiles (see GemmParams::R)
+  p.R = 1;
+  if (pl.n_var == 1 && p.resident && pl.shift % p.kchunk == 0 && pl.shift < pl.kdim && pl.o_h > 1) {
+    const int r = static_cast<int>(std::min<int64_t>({8, 512 / (2 * pl.bn), pl.o_h}));
+    if (r >= 2) p.R = r;
+  }
+#ifdef MEC_TRACE
+  if (const char* e = getenv("MEC_DEBUG_R")) p.R = std::max(1, std::min(p.R, atoi(e)));
+#endif
+  p.n_acc = p.R > 1 ? 2 : (4 * pl.bn <= 512 ? 4 : 2);
+  uint32_t cols = 32;
+  while (cols < static_cast<uint32_t>(p.n_acc * p.R * pl.bn)) cols <<= 1;
+  p.tmem_cols = cols;
   stages = std::max(1, std::min(stages, std::max(2, 2 * p.n_kstages)));
+#ifdef MEC_TRACE
+  if (const char* e = getenv("MEC_DEBUG_STAGES")) stages = std::min(stages, atoi(e));
+#endif
   p.stages = stages;
   const size_t smem = kSmemAlign + stages * static_cast<size_t>(kStageABytes) +
                       (p.resident ? b_res : stages * kAtomsPerStage * b_tile) + epi +
@@ -649,7 +727,8 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   // grid: a multiple of the combo count, at most one CTA per SM
   int64_t max_tiles = 0;
   for (int v = 0; v < pl.n_var; ++v) {
-    const int64_t nh = (pl.o_h - p.h_first[v] + pl.n_var - 1) / pl.n_var;
+    const int64_t nh = p.R == 1 ? (pl.o_h - p.h_first[v] + pl.n_var - 1) / pl.n_var
+                                : (pl.o_h + p.R - 1) / p.R;
     max_tiles = std::max<int64_t>(max_tiles, std::max<int64_t>(0, nh) * p.n_mt * groups);
   }
   if (max_tiles == 0) return cudaSuccess;
