@@ -25,7 +25,7 @@
  *    fp32 (4 B) in memory, multiplied as tf32 (tcgen05 kind::tf32), fp32
  *    accumulation, O written as fp32.
  *  - Inputs must be finite: the K-tail of a window reads up to one K-tile of
- *    neighbouring lowered data, multiplied by zero weight rows (DESIGN.md 5.3).
+ *    neighbouring lowered data, multiplied by zero weight rows (DESIGN.md 6.2).
  */
 #ifndef MEC_H
 #define MEC_H
@@ -66,7 +66,10 @@ typedef enum {
   MEC_PATH_AUTO = 0,       /* Alg.2 l.8: A iff o_w <= T and #O <= #L, else B */
   MEC_PATH_SOLUTION_A = 1, /* batch-folded */
   MEC_PATH_SOLUTION_B = 2, /* per-image */
-  MEC_PATH_FUSED = 3       /* lowering fused into the GEMM (L never in HBM); reserved */
+  MEC_PATH_FUSED = 3       /* lowering fused into the GEMM: each K-atom of a window tile is
+                              read as a TMA box of I, L is never written (needs i_c elt a
+                              multiple of 128 B and s_w <= 2; else MEC_ERR_UNSUPPORTED).
+                              Never chosen by MEC_PATH_AUTO (which follows Alg.2 l.8). */
 } mec_path_t;
 
 /* How Solution A reaches n-h-w-c (Alg.2 l.13-19). */
@@ -84,7 +87,8 @@ typedef struct {
   int path;       /* mec_path_t; MEC_PATH_AUTO by default */
   int T;          /* threshold of Alg.2 l.8; <= 0 means MEC_DEFAULT_T */
   int sola_fix;   /* mec_sola_fix_t; used only when Solution A runs */
-  int reserved0;
+  int rows_per_tile; /* output rows h per GEMM tile (multi-row schedule: the union of
+                        their overlapping windows of L is streamed once); 0 = auto (1) */
   void* workspace;        /* device buffer >= mec_workspace_bytes(); NULL = stream-ordered pool */
   size_t workspace_bytes;
   /* Optional cudaEvent_t handles recorded on `stream` at stage boundaries

@@ -54,7 +54,7 @@ class MecOptions(ctypes.Structure):
         ("path", ctypes.c_int),
         ("T", ctypes.c_int),
         ("sola_fix", ctypes.c_int),
-        ("reserved0", ctypes.c_int),
+        ("rows_per_tile", ctypes.c_int),
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_size_t),
         ("stage_events", ctypes.c_void_p * 4),

@@ -305,6 +305,17 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
     const int64_t tiles = pl.n_var * ((pl.kdim_pad + 31) / 32) * ((pl.kc_pad + 31) / 32);
     prep_blocks = std::min<int64_t>(tiles, 2LL * num_sms());
   }
+  if (L == nullptr) {  // weight operand only (fused path)
+    if (prep_blocks == 0) return cudaSuccess;
+    LowerParams q = p;
+    q.n_lower_blocks = 0;
+    if (pl.elt == 2)
+      lower_kernel<uint16_t><<<static_cast<unsigned>(prep_blocks), 256, 64, st>>>(q);
+    else
+      lower_kernel<uint32_t><<<static_cast<unsigned>(prep_blocks), 256, 64, st>>>(q);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
 
   const int64_t row_bytes = static_cast<int64_t>(p.iwc) * pl.elt;
   const int64_t max_smem = 96 * 1024;

@@ -82,7 +82,15 @@ int num_sms() {
 
 static cudaError_t encode_impl(CUtensorMap* map, bool tf32, int rank, const void* base,
                                const uint64_t* dims, const uint64_t* strides_bytes,
-                               const uint32_t* box, CUtensorMapSwizzle swz);
+                               const uint32_t* box, CUtensorMapSwizzle swz,
+                               const uint32_t* elem_strides = nullptr);
+
+cudaError_t encode_tiled_strided(CUtensorMap* map, bool tf32, int rank, const void* base,
+                                 const uint64_t* dims, const uint64_t* strides_bytes,
+                                 const uint32_t* box, const uint32_t* elem_strides) {
+  return encode_impl(map, tf32, rank, base, dims, strides_bytes, box, CU_TENSOR_MAP_SWIZZLE_128B,
+                     elem_strides);
+}
 
 cudaError_t encode_tiled(CUtensorMap* map, bool tf32, int rank, const void* base,
                          const uint64_t* dims, const uint64_t* strides_bytes,
@@ -102,7 +110,8 @@ cudaError_t encode_tiled_swz(CUtensorMap* map, bool tf32, int rank, const void* 
 
 static cudaError_t encode_impl(CUtensorMap* map, bool tf32, int rank, const void* base,
                                const uint64_t* dims, const uint64_t* strides_bytes,
-                               const uint32_t* box, CUtensorMapSwizzle swz) {
+                               const uint32_t* box, CUtensorMapSwizzle swz,
+                               const uint32_t* elem_strides) {
   std::call_once(g_encode_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -119,7 +128,7 @@ static cudaError_t encode_impl(CUtensorMap* map, bool tf32, int rank, const void
   for (int i = 0; i < rank; ++i) {
     d[i] = dims[i];
     b[i] = box[i];
-    es[i] = 1;
+    es[i] = elem_strides ? elem_strides[i] : 1;
     if (i < rank - 1) s[i] = strides_bytes[i];
   }
   CUresult r = g_encode(map, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
@@ -272,10 +281,11 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
   if (opt->path < MEC_PATH_AUTO || opt->path > MEC_PATH_FUSED) return MEC_ERR_INVALID_ARG;
   if (opt->sola_fix < MEC_SOLA_FIX_EPILOGUE || opt->sola_fix > MEC_SOLA_FIX_NONE)
     return MEC_ERR_INVALID_ARG;
+  if (opt->rows_per_tile < 0) return MEC_ERR_INVALID_ARG;
   const int T = opt->T > 0 ? opt->T : MEC_DEFAULT_T;
   int path = opt->path;
   if (path == MEC_PATH_AUTO) path = mec_select_path(s, s_h, s_w, T);
-  if (path == MEC_PATH_FUSED) return MEC_ERR_UNSUPPORTED;
+  if (path == MEC_PATH_FUSED && !mec::fused_eligible(p)) return MEC_ERR_UNSUPPORTED;
   // Solution A's literal format fix repurposes L as auxiliary space,
   // which requires |L| >= |O|.
   if (path == MEC_PATH_SOLUTION_A && opt->sola_fix == MEC_SOLA_FIX_LITERAL && p.n_O > p.n_L)
@@ -312,15 +322,21 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
   cudaError_t e = cudaSuccess;
   rec(0);
   // Alg.2 l.2-7: lowering into the pitch-padded L, and K as a (k_h k_w i_c) x k_c matrix
-  e = mec::launch_lower(p, I, L, p.pitch, K, Kt, stream_, &launches);
+  // (the fused path skips L: only the weight operand is prepared)
+  e = mec::launch_lower(p, I, path == MEC_PATH_FUSED ? nullptr : L, p.pitch, K, Kt, stream_, &launches);
   if (e != cudaSuccess) goto fail;
   rec(1);
   {
     mec::GemmArgs ga{};
-    ga.L = L;
+    ga.L = path == MEC_PATH_FUSED ? I : L;
+    ga.fused = path == MEC_PATH_FUSED;
     ga.Kt = Kt;
     ga.O = O;
-    if (path == MEC_PATH_SOLUTION_A) {  // l.9: L as (i_n o_w) x (i_h k_w i_c)
+    ga.rows_per_tile = opt->rows_per_tile;
+    if (path == MEC_PATH_FUSED) {  // batch-folded tiles of windows of I
+      ga.batch_folded = true;
+      ga.out_hnwc = false;
+    } else if (path == MEC_PATH_SOLUTION_A) {  // l.9: L as (i_n o_w) x (i_h k_w i_c)
       ga.batch_folded = true;
       ga.out_hnwc = opt->sola_fix != MEC_SOLA_FIX_EPILOGUE;
     } else {  // l.21: L as i_n matrices of o_w x (i_h k_w i_c)

@@ -55,7 +55,7 @@ mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, P
 // in the same launch, the weight operand (Alg.2 l.7, K as a (k_h k_w i_c) x
 // k_c matrix), transposed to K-major and shifted:
 //   Kt[v][c][j] = K_mat[j - v*delta_step][c]  (0 outside, v < n_var).
-// Kt may be null (mec_lower).
+// Kt may be null (mec_lower); L may be null (weight prep only, fused path).
 cudaError_t launch_lower(const Plan& p, const void* I, void* L, int64_t pitch, const void* K,
                          void* Kt, cudaStream_t st, int* launches);
 
@@ -69,7 +69,14 @@ struct GemmArgs {
   void* O;
   bool batch_folded;
   bool out_hnwc;
+  int rows_per_tile;  // requested multi-row R (0/1 = one output row per tile)
+  bool fused;         // A atoms read straight from I (L == I pointer), see DESIGN.md 6.4
 };
+
+// The fused path reads each K-atom (a, b, channel block) of a window tile as a
+// TMA box of the NHWC input: needs whole 128-byte channel blocks per pixel and
+// a pixel traversal stride s_w <= 2 (box rows x s_w <= 256).
+bool fused_eligible(const Plan& p);
 cudaError_t launch_window_gemm(const Plan& p, const GemmArgs& a, cudaStream_t st, int* launches);
 
 // Solution A format fix, paper-literal (Alg.2 l.13-19): "Copy L = O" and the

@@ -22,4 +22,10 @@ cudaError_t encode_tiled_swz(CUtensorMap* map, bool tf32, int rank, const void* 
                              const uint64_t* dims, const uint64_t* strides_bytes,
                              const uint32_t* box, int swizzle_bytes);
 
+// Tiled map with per-dimension traversal strides (elementStrides), 128-byte
+// swizzle: the fused path's view of the NHWC input (pixel stride s_w).
+cudaError_t encode_tiled_strided(CUtensorMap* map, bool tf32, int rank, const void* base,
+                                 const uint64_t* dims, const uint64_t* strides_bytes,
+                                 const uint32_t* box, const uint32_t* elem_strides);
+
 }  // namespace mec

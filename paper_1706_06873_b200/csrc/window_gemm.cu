@@ -108,8 +108,7 @@ namespace {
 constexpr int kEpiGroups = 2;  // epilogue warp-groups, alternating tiles
 constexpr int kThreads = 64 + kEpiGroups * 128;
 constexpr int kAtomBytes = kBM * kTileKBytes;  // 16 KB: 128 rows x 128 B
-constexpr int kAtomsPerStage = 2;
-constexpr int kStageABytes = kAtomsPerStage * kAtomBytes;
+constexpr int kMaxAtomsPerStage = 2;
 constexpr int kMaxCombos = 32;  // n_var (<= 8) x N tiles (<= 4 for k_c <= 1024)
 constexpr int kEpiWarps = 4 * kEpiGroups;
 
@@ -122,6 +121,8 @@ struct GemmParams {
   // straddles two images; ipt = 1 is one image per tile (Solution B, and
   // Solution A when o_w > 64).
   bool flat;
+  bool fused;       // A atoms are TMA boxes of I: atom (a, b, cb) of output row h
+  int ncb, k_w, s_h, s_w;
   int ipt, slot;
   int64_t rows, groups, n_mt;
   int64_t shift;
@@ -146,6 +147,7 @@ struct GemmParams {
   int n_chunks;     // ceil(kdim / kchunk): B chunks holding weights
   int kdim;
   int stages;
+  int aps;          // K-atoms per pipeline stage (2 with resident weights, else 1)
   bool resident;    // weight operand resident in smem
   uint32_t tmem_cols;
   int n_acc;        // TMEM accumulator sets (each R x bn columns)
@@ -208,6 +210,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + kSmemAlign - 1) & ~uintptr_t(kSmemAlign - 1));
   const int S = p.stages;
+  const int kAtomsPerStage = p.aps;
+  const int kStageABytes = kAtomsPerStage * kAtomBytes;
   const uint32_t b_tile_bytes = static_cast<uint32_t>(p.bn) * kTileKBytes;
   // smem: [S A-stages][B: n_atoms resident tiles or S x 2 streamed][epi staging][barriers]
   const int nb = p.resident ? p.n_atoms : S * kAtomsPerStage;
@@ -292,7 +296,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int a = 0; a < na; ++a) {
               const int atom = ks * kAtomsPerStage + a;
               unsigned char* dstA = smemA + static_cast<size_t>(stage) * kStageABytes + a * kAtomBytes;
-              if (p.ipt <= 1) {
+              if (p.fused) {
+                // K atom -> (kernel row a, kernel column b, channel block cb); rows = pixels
+                // s_w w + b of input row s_h h + a (pixel traversal stride s_w in the map)
+                const int ab = atom / p.ncb, cb = atom - ab * p.ncb;
+                const int fa = ab / p.k_w, fb = ab - fa * p.k_w;
+                const int32_t zy = static_cast<int32_t>(c.h * p.s_h + fa);
+                if (p.ipt <= 1) {
+                  ptx::tma_load_4d(dstA, &tmA, &full[stage], cb * p.bk,
+                                   static_cast<int32_t>(c.mt * kBM * p.s_w + fb), zy, z0, hintA);
+                } else {
+                  for (int j = 0; j < p.ipt; ++j)
+                    ptx::tma_load_4d(dstA + j * p.slot * kTileKBytes, &tmA, &full[stage], cb * p.bk, fb,
+                                     zy, z0 * p.ipt + j, hintA);
+                }
+              } else if (p.ipt <= 1) {
                 ptx::tma_load_3d(dstA, &tmA, &full[stage], x0 + atom * p.bk, y0, z0, hintA);
               } else {  // one box of `slot` rows per image of the tile (images >= i_n: zero fill)
                 for (int j = 0; j < p.ipt; ++j)
@@ -572,6 +590,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
+bool fused_eligible(const Plan& pl) {
+  return (pl.s.i_c * pl.elt) % kTileKBytes == 0 && pl.s_w <= 2;
+}
+
 cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st,
                                int* launches) {
   const bool tf32 = pl.dt == MEC_DTYPE_TF32;
@@ -579,7 +601,7 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   CUtensorMap tmA, tmB, tmO;
   // Row tiling (see GemmParams): Solution A with o_w < 32 folds flat (a
   // 32-row epilogue block then spans several images); otherwise image slots.
-  const bool flat = a.batch_folded && pl.o_w < 32;
+  const bool flat = !a.fused && a.batch_folded && pl.o_w < 32;
   int slot = 128, ipt = 1;
   if (!flat && pl.o_w <= 128) {
     slot = static_cast<int>((pl.o_w + 31) / 32 * 32);
@@ -589,6 +611,21 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   const int64_t rows = flat ? pl.s.i_n * pl.o_w : pl.o_w;
   const int64_t groups = flat ? 1 : (pl.s.i_n + ipt - 1) / ipt;
   const int64_t n_mt = flat ? (rows + kBM - 1) / kBM : (ipt > 1 ? 1 : (pl.o_w + kBM - 1) / kBM);
+  if (a.fused) {
+    // A: the NHWC input as {i_c, i_w, i_h, i_n}; a box is bk channels x `rows`
+    // pixels taken every s_w pixels (elementStrides) -- one K-atom of `rows`
+    // windows, read in place: L is never materialised.
+    const uint64_t dims[4] = {static_cast<uint64_t>(pl.s.i_c), static_cast<uint64_t>(pl.s.i_w),
+                              static_cast<uint64_t>(pl.s.i_h), static_cast<uint64_t>(pl.s.i_n)};
+    const uint64_t strides[3] = {static_cast<uint64_t>(pl.s.i_c) * pl.elt,
+                                 static_cast<uint64_t>(pl.s.i_w * pl.s.i_c) * pl.elt,
+                                 static_cast<uint64_t>(pl.s.i_h * pl.s.i_w * pl.s.i_c) * pl.elt};
+    const uint32_t rows_box = static_cast<uint32_t>(ipt > 1 ? slot : kBM);
+    const uint32_t box[4] = {static_cast<uint32_t>(pl.bk), rows_box * static_cast<uint32_t>(pl.s_w), 1, 1};
+    const uint32_t es[4] = {1, static_cast<uint32_t>(pl.s_w), 1, 1};
+    cudaError_t e = encode_tiled_strided(&tmA, tf32, 4, a.L, dims, strides, box, es);
+    if (e != cudaSuccess) return e;
+  } else
   // A: the lowered tensor L (Alg.2 l.9 / l.21) as {columns, rows, groups}:
   // flat {i_h k_w i_c, i_n o_w, 1}, else per image {i_h k_w i_c, o_w, i_n}.
   {
@@ -625,18 +662,27 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   p.shift = pl.shift;
   p.kc_pad = pl.kc_pad;
   p.bk = pl.bk;
-  p.n_atoms = static_cast<int>(pl.kdim_pad / pl.bk);
-  p.n_kstages = (p.n_atoms + kAtomsPerStage - 1) / kAtomsPerStage;
+  p.n_atoms = static_cast<int>((a.fused ? pl.kdim : pl.kdim_pad) / pl.bk);
+  p.fused = a.fused;
+  p.ncb = static_cast<int>(pl.s.i_c / pl.bk);
+  p.k_w = static_cast<int>(pl.s.k_w);
+  p.s_h = pl.s_h;
+  p.s_w = pl.s_w;
+
   p.bn = pl.bn;
   p.n_tiles_n = pl.n_tiles_n;
-  p.n_var = pl.n_var;
-  p.n_combo = pl.n_var * pl.n_tiles_n;
+  p.n_var = a.fused ? 1 : pl.n_var;  // the fused path uses weight variant 0 only
+  p.n_combo = p.n_var * pl.n_tiles_n;
   if (p.n_combo > kMaxCombos) return cudaErrorInvalidConfiguration;
   // first h of each weight variant: delta(h) = (h shift) mod vec = v delta_step
   for (int v = 0; v < 8; ++v) p.h_first[v] = static_cast<int>(pl.o_h);  // none
-  for (int64_t h = 0; h < std::min<int64_t>(pl.o_h, pl.n_var); ++h) {
-    const int v = static_cast<int>(((h * pl.shift) % pl.vec) / pl.delta_step);
-    if (p.h_first[v] > h) p.h_first[v] = static_cast<int>(h);
+  if (a.fused) {
+    p.h_first[0] = 0;
+  } else {
+    for (int64_t h = 0; h < std::min<int64_t>(pl.o_h, pl.n_var); ++h) {
+      const int v = static_cast<int>(((h * pl.shift) % pl.vec) / pl.delta_step);
+      if (p.h_first[v] > h) p.h_first[v] = static_cast<int>(h);
+    }
   }
   p.out_hnwc = a.out_hnwc;
 #ifdef MEC_TRACE
@@ -695,21 +741,31 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   const size_t b_res = b_tile * p.n_atoms;
   const size_t epi = static_cast<size_t>(kEpiWarps) * p.stage_out_bytes;
   const size_t budget = 222 * 1024 - epi;  // after the 1 KB alignment slack
-  p.resident = b_res + 2 * kStageABytes <= budget && b_res <= 120 * 1024;
+  p.resident = b_res + 2 * kMaxAtomsPerStage * kAtomBytes <= budget && b_res <= 120 * 1024;
+  p.aps = p.resident ? 2 : 1;
+  const size_t stage_a = static_cast<size_t>(p.aps) * kAtomBytes;
+  p.n_kstages = (p.n_atoms + p.aps - 1) / p.aps;
   int stages;
   if (p.resident) {
-    stages = static_cast<int>(std::min<size_t>(8, (budget - b_res) / kStageABytes));
+    stages = static_cast<int>(std::min<size_t>(8, (budget - b_res) / stage_a));
   } else {
-    stages = static_cast<int>(std::min<size_t>(8, budget / (kStageABytes + kAtomsPerStage * b_tile)));
+    stages = static_cast<int>(std::min<size_t>(8, budget / (stage_a + p.aps * b_tile)));
   }
   // multi-row tiles (see GemmParams::R)
+  // Multi-row tiles (requested via mec_options_t::rows_per_tile) are parity-
+  // tested, but with SS operands the extra B reads make them shared-memory-
+  // bound on B200 (slower than R = 1), so auto = 1.
   p.R = 1;
-  if (pl.n_var == 1 && p.resident && pl.shift % p.kchunk == 0 && pl.shift < pl.kdim && pl.o_h > 1) {
+  if (a.rows_per_tile > 1 && !a.fused && pl.n_var == 1 && p.resident && pl.shift % p.kchunk == 0 &&
+      pl.shift < pl.kdim && pl.o_h > 1) {
     const int r = static_cast<int>(std::min<int64_t>({8, 512 / (2 * pl.bn), pl.o_h}));
-    if (r >= 2) p.R = r;
+    p.R = std::max(1, std::min(r, a.rows_per_tile));
   }
 #ifdef MEC_TRACE
-  if (const char* e = getenv("MEC_DEBUG_R")) p.R = std::max(1, std::min(p.R, atoi(e)));
+  if (const char* e = getenv("MEC_DEBUG_R")) {
+    if (!a.fused && pl.n_var == 1 && p.resident && pl.shift % p.kchunk == 0 && pl.shift < pl.kdim && pl.o_h > 1)
+      p.R = std::max(1, std::min<int>(std::min<int64_t>({8, 512 / (2 * pl.bn), pl.o_h}), atoi(e)));
+  }
 #endif
   p.n_acc = p.R > 1 ? 2 : (4 * pl.bn <= 512 ? 4 : 2);
   uint32_t cols = 32;
@@ -720,14 +776,14 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   if (const char* e = getenv("MEC_DEBUG_STAGES")) stages = std::min(stages, atoi(e));
 #endif
   p.stages = stages;
-  const size_t smem = kSmemAlign + stages * static_cast<size_t>(kStageABytes) +
-                      (p.resident ? b_res : stages * kAtomsPerStage * b_tile) + epi +
+  const size_t smem = kSmemAlign + stages * stage_a +
+                      (p.resident ? b_res : stages * p.aps * b_tile) + epi +
                       (2 * stages + 10) * 8 + 16;
 
   // grid: a multiple of the combo count, at most one CTA per SM
   int64_t max_tiles = 0;
-  for (int v = 0; v < pl.n_var; ++v) {
-    const int64_t nh = p.R == 1 ? (pl.o_h - p.h_first[v] + pl.n_var - 1) / pl.n_var
+  for (int v = 0; v < p.n_var; ++v) {
+    const int64_t nh = p.R == 1 ? (pl.o_h - p.h_first[v] + p.n_var - 1) / p.n_var
                                 : (pl.o_h + p.R - 1) / p.R;
     max_tiles = std::max<int64_t>(max_tiles, std::max<int64_t>(0, nh) * p.n_mt * groups);
   }

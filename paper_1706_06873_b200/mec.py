@@ -92,7 +92,8 @@ def lower(I: torch.Tensor, k_h: int, k_w: int, s_h: int, s_w: int, out: torch.Te
 
 def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torch.Tensor | None = None,
                  path: int = MEC_PATH_AUTO, T: int = MEC_DEFAULT_T, sola_fix: int = MEC_SOLA_FIX_EPILOGUE,
-                 workspace: torch.Tensor | None = None, stage_events=None, return_path: bool = False):
+                 workspace: torch.Tensor | None = None, stage_events=None, return_path: bool = False,
+                 rows_per_tile: int = 0):
     """mec_conv_forward_ex: O = MEC(I, K, s) (Algorithm 2), O in n-h-w-c
     (or h-n-w-c with sola_fix=MEC_SOLA_FIX_NONE when Solution A runs)."""
     _cuda(I, "I")
@@ -111,6 +112,7 @@ def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torc
     opt = _lib.MecOptions()
     _lib.lib().mec_options_init(ctypes.byref(opt))
     opt.path, opt.T, opt.sola_fix = int(path), int(T), int(sola_fix)
+    opt.rows_per_tile = int(rows_per_tile)
     if workspace is not None:
         _cuda(workspace, "workspace")
         opt.workspace = workspace.data_ptr()

@@ -156,6 +156,70 @@ def test_full24_values_within_north_star_tolerance(cuda_ok, dtype):
     check_O(O, ref, dtype, 576, tight=False)
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("rpt", [2, 3, 4, 8])
+@pytest.mark.parametrize("name,batch", [("cv9", 3), ("cv10", 2), ("cv11", 2), ("cv8", 1)])
+def test_multi_row_tiles(cuda_ok, name, batch, rpt, dtype):
+    """Multi-row schedule (rows_per_tile): each streamed window atom feeds the
+    MMAs of up to R output rows; must equal the one-row schedule bit for bit
+    (same per-accumulator MMA order) and the oracle within tolerance."""
+    i_h, i_w, i_c, k_h, k_w, k_c, s = synth.TABLE2[name]
+    shape = (batch, i_h, i_w, i_c, k_h, k_w, k_c)
+    I, K = make_inputs(shape, dtype, seed=3000 + rpt)
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    for path in (MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B):
+        O1 = mec.conv_forward(Id, Kd, s, s, path=path)
+        OR = mec.conv_forward(Id, Kd, s, s, path=path, rows_per_tile=rpt)
+        torch.cuda.synchronize()
+        check_O(OR, ref, dtype, k_h * k_w * i_c)
+        assert torch.equal(O1, OR)
+
+
+FUSED_CASES = [("cv4", 1), ("cv6", 3), ("cv8", 1), ("cv9", 3), ("cv10", 2), ("cv11", 3), ("cv12", 5)]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("name,batch", FUSED_CASES)
+def test_fused_path(cuda_ok, name, batch, dtype):
+    """MEC_PATH_FUSED (section 8 row a6): K-atoms of each window read as TMA boxes of
+    I, L never written.  Same MMA sequence as the two-kernel path -> bit-identical."""
+    from paper_1706_06873_b200._lib import MEC_PATH_FUSED
+    i_h, i_w, i_c, k_h, k_w, k_c, s = synth.TABLE2[name]
+    shape = (batch, i_h, i_w, i_c, k_h, k_w, k_c)
+    I, K = make_inputs(shape, dtype, seed=4000 + int(name[2:]))
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    OF, chosen = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_FUSED, return_path=True)
+    O2 = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_SOLUTION_B)
+    torch.cuda.synchronize()
+    assert chosen == MEC_PATH_FUSED
+    check_O(OF, ref, dtype, k_h * k_w * i_c)
+    assert torch.equal(OF, O2)
+
+
+@pytest.mark.parametrize("shape,s", [((4, 56, 56, 256, 1, 1, 64), 1), ((3, 28, 28, 192, 1, 1, 64), 1),
+                                     ((2, 30, 33, 64, 3, 3, 96), 2), ((2, 17, 140, 128, 2, 3, 48), 1)])
+def test_fused_path_misc(cuda_ok, shape, s):
+    from paper_1706_06873_b200._lib import MEC_PATH_FUSED
+    I, K = make_inputs(shape, "bf16", seed=77)
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    OF = mec.conv_forward(to_dev(I, "bf16"), to_dev(K, "bf16"), s, s, path=MEC_PATH_FUSED)
+    check_O(OF, ref, "bf16", shape[3] * shape[4] * shape[5])
+
+
+def test_fused_path_unsupported_shapes(cuda_ok):
+    from paper_1706_06873_b200._lib import MEC_PATH_FUSED
+    I = torch.zeros(1, 20, 20, 3, device="cuda", dtype=torch.bfloat16)  # i_c = 3: 6-byte pixels
+    K = torch.zeros(3, 3, 3, 8, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(MecError):
+        mec.conv_forward(I, K, 1, 1, path=MEC_PATH_FUSED)
+    I = torch.zeros(1, 30, 30, 64, device="cuda", dtype=torch.bfloat16)  # s_w = 3 > 2
+    K = torch.zeros(3, 3, 64, 8, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(MecError):
+        mec.conv_forward(I, K, 3, 3, path=MEC_PATH_FUSED)
+
+
 # ------------------------------------------------------------------ lowering
 
 LOWER_CASES = [

@@ -1,10 +1,11 @@
 #!/bin/bash
-# quick iteration: parity tests, C1/C3 bench lines, ncu capture of C1 kernels
+# quick iteration: parity tests, bench lines (two-kernel and fused), ncu capture of C1 kernels
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-timeout 300 python bench.py --no-cpu-baseline --steps 30 > gpurun_out/q_c1.json 2> gpurun_out/q.err
-timeout 300 python bench.py --config C3 --no-cpu-baseline --steps 20 --no-e2e >> gpurun_out/q_c1.json 2>> gpurun_out/q.err
-timeout 300 python bench.py --config C4_cv7 --batch 128 --no-cpu-baseline --steps 10 --no-e2e >> gpurun_out/q_c1.json 2>> gpurun_out/q.err
-timeout 300 python bench.py --config C4_cv12 --batch 128 --no-cpu-baseline --steps 10 --no-e2e >> gpurun_out/q_c1.json 2>> gpurun_out/q.err
+B="timeout 300 python bench.py --no-cpu-baseline --no-e2e"
+$B --steps 30 > gpurun_out/q_c1.json 2> gpurun_out/q.err
+for c in "C3" "C3 --path fused" "C2" "C2 --path fused" "C2_tf32 --path fused"; do $B --config $c --steps 10 >> gpurun_out/q_c1.json 2>> gpurun_out/q.err; done
+for c in C4_cv5 C4_cv6 C4_cv12 C4_cv7; do $B --config $c --batch 128 --steps 10 >> gpurun_out/q_c1.json 2>> gpurun_out/q.err; done
+for c in C4_cv4 C4_cv8 C4_cv9 C4_cv11 C4_r50_1x1_256to64; do $B --config $c --batch 128 --steps 10 --path fused >> gpurun_out/q_c1.json 2>> gpurun_out/q.err; done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"window_gemm|lower_kernel" -s 4 -c 2 -o gpurun_out/prof_q python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_q.log 2>&1
 tail -2 gpurun_out/q.err
