@@ -54,6 +54,7 @@ struct LowerParams {
   unsigned char* Kt;
   int64_t kdim, k_c, kdim_pad, kc_pad;
   int n_var, delta_step;
+  int64_t kwc_src, kwc_pad;  // gather layout: Kt column a kwc_pad + j <- K_mat row a kwc_src + j (0: identity)
   bool aligned;   // fast path: every strip and segment 16-byte aligned
 };
 
@@ -72,8 +73,15 @@ __device__ __forceinline__ void prep_weight_tile(const LowerParams& p, int64_t t
   const T* K = reinterpret_cast<const T*>(p.K);
   T* Kt = reinterpret_cast<T*>(p.Kt) + v * p.kc_pad * p.kdim_pad;
   for (int r = ty; r < 32; r += nw) {
-    const int64_t j = jt * 32 + r - delta, c = ct * 32 + tx;
-    tbuf[r][tx] = (j >= 0 && j < p.kdim && c < p.k_c) ? K[j * p.k_c + c] : T(0);
+    int64_t j = jt * 32 + r - delta;
+    const int64_t c = ct * 32 + tx;
+    bool ok = j >= 0;
+    if (p.kwc_pad > 0 && ok) {  // gather layout: per-kernel-row padding
+      const int64_t a = j / p.kwc_pad, rr = j - a * p.kwc_pad;
+      ok = rr < p.kwc_src;
+      j = a * p.kwc_src + rr;
+    }
+    tbuf[r][tx] = (ok && j < p.kdim && c < p.k_c) ? K[j * p.k_c + c] : T(0);
   }
   __syncthreads();
   for (int r = ty; r < 32; r += nw) {
@@ -278,7 +286,7 @@ __global__ void __launch_bounds__(256) lower_direct_kernel(const T* __restrict__
 }  // namespace
 
 cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, const void* K,
-                         void* Kt, cudaStream_t st, int* launches) {
+                         void* Kt, cudaStream_t st, int* launches, bool gather_kt) {
   const mec_shape_t& s = pl.s;
   LowerParams p{};
   p.I = static_cast<const unsigned char*>(I);
@@ -299,10 +307,16 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   p.kc_pad = pl.kc_pad;
   p.n_var = pl.n_var;
   p.delta_step = pl.delta_step;
+  if (gather_kt) {
+    p.n_var = 1;
+    p.kdim_pad = pl.kdim_g;
+    p.kwc_src = s.k_w * s.i_c;
+    p.kwc_pad = pl.kwc_p;
+  }
 
   int64_t prep_blocks = 0;
   if (Kt != nullptr) {
-    const int64_t tiles = pl.n_var * ((pl.kdim_pad + 31) / 32) * ((pl.kc_pad + 31) / 32);
+    const int64_t tiles = p.n_var * ((p.kdim_pad + 31) / 32) * ((pl.kc_pad + 31) / 32);
     prep_blocks = std::min<int64_t>(tiles, 2LL * num_sms());
   }
   if (L == nullptr) {  // weight operand only (fused path)

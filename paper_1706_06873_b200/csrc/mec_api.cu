@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -173,7 +174,9 @@ mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, P
   p->n_O = s->i_n * p->o_h * p->o_w * s->k_c;
   p->bytes_L_pitched = static_cast<size_t>(s->i_n * p->o_w * p->pitch) * p->elt;
   p->off_kt = static_cast<size_t>(round_up(static_cast<int64_t>(p->bytes_L_pitched), 1024));
-  p->bytes_kt = static_cast<size_t>(p->n_var * p->kc_pad * p->kdim_pad) * p->elt;
+  p->kwc_p = round_up(s->k_w * s->i_c, p->vec);
+  p->kdim_g = round_up(s->k_h * p->kwc_p, p->bk);
+  p->bytes_kt = static_cast<size_t>(std::max(p->n_var * p->kdim_pad, p->kdim_g) * p->kc_pad) * p->elt;
   p->ws_bytes = p->off_kt + p->bytes_kt + 1024;
   // TMA coordinate / extent limits (int32 coordinates, dims <= 2^32)
   if (p->l_cols + p->kdim_pad >= (1LL << 31) || s->i_n * p->o_w >= (1LL << 31) ||
@@ -285,7 +288,8 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
   const int T = opt->T > 0 ? opt->T : MEC_DEFAULT_T;
   int path = opt->path;
   if (path == MEC_PATH_AUTO) path = mec_select_path(s, s_h, s_w, T);
-  if (path == MEC_PATH_FUSED && !mec::fused_eligible(p)) return MEC_ERR_UNSUPPORTED;
+  if (path == MEC_PATH_FUSED && !mec::fused_eligible(p) && !mec::gather_eligible(p))
+    return MEC_ERR_UNSUPPORTED;
   // Solution A's literal format fix repurposes L as auxiliary space,
   // which requires |L| >= |O|.
   if (path == MEC_PATH_SOLUTION_A && opt->sola_fix == MEC_SOLA_FIX_LITERAL && p.n_O > p.n_L)
@@ -323,7 +327,8 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
   rec(0);
   // Alg.2 l.2-7: lowering into the pitch-padded L, and K as a (k_h k_w i_c) x k_c matrix
   // (the fused path skips L: only the weight operand is prepared)
-  e = mec::launch_lower(p, I, path == MEC_PATH_FUSED ? nullptr : L, p.pitch, K, Kt, stream_, &launches);
+  e = mec::launch_lower(p, I, path == MEC_PATH_FUSED ? nullptr : L, p.pitch, K, Kt, stream_, &launches,
+                        path == MEC_PATH_FUSED && !mec::fused_eligible(p));
   if (e != cudaSuccess) goto fail;
   rec(1);
   {

@@ -36,13 +36,18 @@ struct Plan {
   int delta_step;        // gcd(shift, vec)
   int n_var;             // number of shifted weight copies
   int64_t kdim_pad;      // (kdim + max delta) rounded up to bk
+  // gather path: the reduction index is re-laid out as
+  // a kwc_p + j (kernel row a, j < k_w i_c), each kernel row padded to 16 bytes
+  // (kwc_p elements) so every 16-byte chunk of an A row is one contiguous run of I
+  int64_t kwc_p;
+  int64_t kdim_g;        // k_h kwc_p rounded up to bk
   int n_tiles_n;         // ceil(k_c / 256)
   int bn;                // N tile (multiple of 16, <= 256)
   int64_t kc_pad;        // n_tiles_n * bn
   int64_t n_L, n_O;      // #L (dense) and #O, elements
   size_t bytes_L_pitched;  // i_n o_w pitch elt
   size_t off_kt;           // workspace offset of the prepared weight operand
-  size_t bytes_kt;         // n_var kc_pad kdim_pad elt
+  size_t bytes_kt;         // max(n_var kc_pad kdim_pad, kc_pad kdim_g) elt
   size_t ws_bytes;         // total workspace (incl. alignment slack)
 };
 
@@ -56,8 +61,10 @@ mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, P
 // k_c matrix), transposed to K-major and shifted:
 //   Kt[v][c][j] = K_mat[j - v*delta_step][c]  (0 outside, v < n_var).
 // Kt may be null (mec_lower); L may be null (weight prep only, fused path).
+// gather_kt: build the gather path's operand instead (one copy, n_var = 1):
+//   Kt[c][a kwc_p + j] = K_mat[a k_w i_c + j][c] for j < k_w i_c, 0 otherwise.
 cudaError_t launch_lower(const Plan& p, const void* I, void* L, int64_t pitch, const void* K,
-                         void* Kt, cudaStream_t st, int* launches);
+                         void* Kt, cudaStream_t st, int* launches, bool gather_kt = false);
 
 // Window GEMMs (Alg.2 l.10-12 or l.23-25) on tcgen05.  batch_folded:
 // Solution A (rows of several images share one 128-row tile); otherwise
@@ -77,6 +84,9 @@ struct GemmArgs {
 // TMA box of the NHWC input: needs whole 128-byte channel blocks per pixel and
 // a pixel traversal stride s_w <= 2 (box rows x s_w <= 256).
 bool fused_eligible(const Plan& p);
+// Fused path for the other layers (e.g. i_c = 3): input rows staged by bulk
+// copies, A atoms assembled in smem by builder warps.
+bool gather_eligible(const Plan& p);
 cudaError_t launch_window_gemm(const Plan& p, const GemmArgs& a, cudaStream_t st, int* launches);
 
 // Solution A format fix, paper-literal (Alg.2 l.13-19): "Copy L = O" and the

@@ -78,10 +78,19 @@ __device__ __forceinline__ unsigned long long mec_gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define MEC_TRACE_EV(tl, ev)                                                              \
-  do {                                                                                    \
-    if (g_mec_trace != nullptr && (tl) < 64)                                              \
-      g_mec_trace[(static_cast<size_t>(blockIdx.x) * 64 + (tl)) * 16 + (ev)] = mec_gtime(); \
+// the buffer pointer is read once per kernel (mec_trace_ptr, a local of the
+// kernel): re-reading the __device__ variable per event put a global-load
+// latency on every traced step
+#define MEC_TRACE_EV(tl, ev)                                                                \
+  do {                                                                                      \
+    if (mec_trace_ptr != nullptr && (tl) < 64)                                              \
+      mec_trace_ptr[(static_cast<size_t>(blockIdx.x) * 64 + (tl)) * 16 + (ev)] = mec_gtime(); \
+  } while (0)
+// second bank (rows 512 + cta): per-atom builder events
+#define MEC_TRACE_EV2(tl, ev)                                                                     \
+  do {                                                                                            \
+    if (mec_trace_ptr != nullptr && (tl) < 64 && (ev) < 16)                                         \
+      mec_trace_ptr[(static_cast<size_t>(blockIdx.x + 512) * 64 + (tl)) * 16 + (ev)] = mec_gtime(); \
   } while (0)
 extern "C" int mec_trace_enable(void** dev_buf_out, size_t* bytes_out) {
   const size_t bytes = static_cast<size_t>(1024) * 64 * 16 * 8;
@@ -100,17 +109,26 @@ extern "C" int mec_trace_read(void* host, const void* dev, size_t bytes) {
 #define MEC_TRACE_EV(tl, ev) \
   do {                       \
   } while (0)
+#define MEC_TRACE_EV2(tl, ev) \
+  do {                        \
+  } while (0)
 #endif
 
 namespace mec {
 namespace {
 
-constexpr int kEpiGroups = 2;  // epilogue warp-groups, alternating tiles
-constexpr int kThreads = 64 + kEpiGroups * 128;
+// epilogue warp-groups (alternating tiles): 2 on the TMA paths; 1 on the
+// gather path, whose builder warps are the bottleneck (keeps registers unspilled)
+template <bool kGather>
+constexpr int epi_groups() { return kGather ? 1 : 2; }
+constexpr int kBuildGroups = 2;  // gather path: builder warp-groups, atoms dealt round-robin
+constexpr int kBuildWarps = 4 * kBuildGroups;  // warps that assemble A atoms in smem
+template <bool kGather>
+constexpr int kernel_threads() { return 64 + epi_groups<kGather>() * 128 + (kGather ? 32 * kBuildWarps : 0); }
 constexpr int kAtomBytes = kBM * kTileKBytes;  // 16 KB: 128 rows x 128 B
 constexpr int kMaxAtomsPerStage = 2;
 constexpr int kMaxCombos = 32;  // n_var (<= 8) x N tiles (<= 4 for k_c <= 1024)
-constexpr int kEpiWarps = 4 * kEpiGroups;
+constexpr int kMaxEpiWarps = 8;
 
 struct GemmParams {
   void* O;
@@ -123,8 +141,24 @@ struct GemmParams {
   bool flat;
   bool fused;       // A atoms are TMA boxes of I: atom (a, b, cb) of output row h
   int ncb, k_w, s_h, s_w;
+  // gather path (fused, small i_c): the producer bulk-copies the tile's k_h
+  // input rows per image into a 2-slot ring; builder warps assemble each A
+  // atom (window elements j = a kwc + r) from them with a per-atom word table
+  const unsigned char* gI;   // I base
+  const unsigned char* gI_end;
+  int k_h;
+  int64_t i_h, i_w;
+  int row_bytes;    // i_w i_c elt
+  int row_pitch;    // staged row pitch (bytes)
+  int kwc;          // k_w i_c
+  int cpr;          // 16-byte chunks per padded kernel row (kwc_p elt / 16)
+  int wstep_b;      // s_w i_c elt
+  uint32_t a_col0;  // gather: TMEM column of A stage 0 (after the accumulators)
+  uint32_t slot_bytes;
+  int n_slots;      // staged-row slots (2..4)
   int ipt, slot;
   int64_t rows, groups, n_mt;
+  bool tiles32;     // every tile index fits 32 bits
   int64_t shift;
   int64_t kc_pad;
   int bk;           // K-atom width in elements (64 bf16 / 32 fp32)
@@ -156,8 +190,12 @@ struct GemmParams {
   bool tma_store;   // epilogue via TMA stores (k_c elt multiple of 16)
   int pw;           // epilogue pass width (columns); pw * out_elt = 128 / 64 / 32 bytes
   int n_pass;       // bn / pw
-  uint32_t stage_out_bytes;  // staging bytes per epilogue warp (32 rows x pw x elt, 1 KB aligned)
-  int dbg;  // trace builds only: 1 = no epilogue stores, 2 = no MMA, 4 = no A loads
+  uint32_t stage_out_bytes;  // staging box bytes (32 rows x pw x elt, 1 KB aligned)
+  int epi_bufs;              // staging boxes per epilogue warp (1 or 2)
+  bool spin;        // gather: builder/MMA handshakes spin on test_wait
+  int dbg;  // trace builds only: 1 = no epilogue stores, 2 = no MMA, 4 = no A loads,
+            // 8 = gather builders skip row loads, 16 = gather builders skip TMEM stores,
+            // 64 = epilogue skips TMEM loads
 };
 
 struct TileCoord {
@@ -177,13 +215,22 @@ __device__ __forceinline__ int64_t combo_tiles(const GemmParams& p, int v) {
   return combo_hslots(p, v) * p.n_mt * p.groups;
 }
 
-__device__ __forceinline__ TileCoord decode_tile(const GemmParams& p, int v, int64_t t) {
-  const int64_t nh = combo_hslots(p, v);
+// nh = combo_hslots(p, v), computed once per CTA
+__device__ __forceinline__ TileCoord decode_tile(const GemmParams& p, int v, int64_t nh, int64_t t) {
   TileCoord c;
-  const int64_t hi = t % nh;
-  t /= nh;
-  c.mt = t % p.n_mt;
-  c.g = t / p.n_mt;
+  int64_t hi;
+  if (p.tiles32) {  // 32-bit divisions (tile counts < 2^31): far cheaper than 64-bit ones
+    const uint32_t t32 = static_cast<uint32_t>(t), nh32 = static_cast<uint32_t>(nh);
+    const uint32_t q = t32 / nh32, nmt = static_cast<uint32_t>(p.n_mt);
+    hi = t32 - q * nh32;
+    c.mt = q % nmt;
+    c.g = q / nmt;
+  } else {
+    hi = t % nh;
+    t /= nh;
+    c.mt = t % p.n_mt;
+    c.g = t / p.n_mt;
+  }
   if (p.R == 1) {
     c.h = p.h_first[v] + hi * p.n_var;
     c.r_eff = 1;
@@ -196,17 +243,25 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmParams& p, int v, int
   return c;
 }
 
+__device__ __noinline__ void p_sink_dummy(uint32_t x) { asm volatile("" ::"r"(x)); }
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <bool kTF32>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool kTF32, bool kGather>
+__global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
     window_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmO, const GemmParams p) {
+  constexpr int kEpiGroups = epi_groups<kGather>();
+  constexpr int kEpiWarps = 4 * kEpiGroups;
+  constexpr int kFirstBuildWarp = 2 + kEpiWarps;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+#ifdef MEC_TRACE
+  unsigned long long* const mec_trace_ptr = g_mec_trace;
+#endif
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + kSmemAlign - 1) & ~uintptr_t(kSmemAlign - 1));
   const int S = p.stages;
@@ -215,16 +270,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t b_tile_bytes = static_cast<uint32_t>(p.bn) * kTileKBytes;
   // smem: [S A-stages][B: n_atoms resident tiles or S x 2 streamed][epi staging][barriers]
   const int nb = p.resident ? p.n_atoms : S * kAtomsPerStage;
-  unsigned char* smemA = smem;
-  unsigned char* smemB = smem + static_cast<size_t>(S) * kStageABytes;
+  unsigned char* smemA = smem;  // (gather path: A lives in TMEM, no smem ring)
+  unsigned char* smemB = smem + (kGather ? 0 : static_cast<size_t>(S) * kStageABytes);
   unsigned char* smemE = smemB + static_cast<size_t>(nb) * b_tile_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smemE + static_cast<size_t>(kEpiWarps) * p.stage_out_bytes);
+  unsigned char* smemR = smemE + static_cast<size_t>(kEpiWarps) * p.epi_bufs * p.stage_out_bytes;  // gather rows
+  uint32_t* ctable = reinterpret_cast<uint32_t*>(smemR + (kGather ? p.n_slots * p.slot_bytes : 0));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(ctable + (kGather ? p.n_atoms * 8 : 0)) + 15) & ~uintptr_t(15));
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
   uint64_t* tempty = bars + 2 * S + 4;
   uint64_t* bfull = bars + 2 * S + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 9);
+  uint64_t* rfull = bars + 2 * S + 9;   // gather row slots (<= 4)
+  uint64_t* rempty = bars + 2 * S + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 17);
 
   // warp index broadcast from lane 0: provably warp-uniform, so role branches
   // are uniform and the MMA issue loop keeps descriptors in uniform registers
@@ -236,15 +296,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nt = combo % p.n_tiles_n;
   const int64_t t_begin = blockIdx.x / p.n_combo;
   const int64_t t_step = p.ctas_per_combo;
-  const int64_t n_tiles = combo_tiles(p, v);
+  const int64_t nh_c = combo_hslots(p, v);
+  const int64_t n_tiles = nh_c * p.n_mt * p.groups;
 
   if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch_desc(&tmA);
+    if (!kGather) ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
     ptx::tma_prefetch_desc(&tmO);
     for (int i = 0; i < S; ++i) {
-      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&full[i], kGather ? 4 : 1);  // gather: the 4 warps of one builder group
       ptx::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      ptx::mbar_init(&rfull[i], 1);
+      ptx::mbar_init(&rempty[i], kBuildWarps);
     }
     for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(&tfull[i], 1);
@@ -254,6 +319,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc_dyn(tmem_slot, p.tmem_cols);
+  if constexpr (kGather) {
+    // staged-row slots start zeroed, so the builders' reads past a staged span
+    // (met by zero weight columns) only ever see finite values; chunk table:
+    // chunk g of the padded window -> byte offset a row_bytes + 16 (g mod cpr)
+    const uint32_t r_s = ptx::smem_u32(smemR);
+    for (uint32_t i = threadIdx.x; i < p.n_slots * p.slot_bytes / 16; i += blockDim.x)
+      ptx::st_shared_v4(r_s + 16 * i, 0u, 0u, 0u, 0u);
+    for (int g = threadIdx.x; g < p.n_atoms * 8; g += blockDim.x) {
+      const int a = g / p.cpr, off = g - a * p.cpr;
+      ctable[g] = a < p.k_h ? static_cast<uint32_t>(a * p.row_bytes + 16 * off) : 0u;
+    }
+    ptx::fence_proxy_async_smem();  // zeros before the async-proxy row copies
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -275,10 +353,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr int64_t kVec = kTF32 ? 4 : 8;  // elements per 16 bytes
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = t_begin; t < n_tiles; t += t_step) {
+      for (int64_t t = t_begin; !kGather && t < n_tiles; t += t_step) {
         const int tl = static_cast<int>((t - t_begin) / t_step);
         MEC_TRACE_EV(tl, 0);
-        const TileCoord c = decode_tile(p, v, t);
+        const TileCoord c = decode_tile(p, v, nh_c, t);
         // window start h*shift rounded down to 16 bytes (TMA rule); variant v absorbs delta
         const int64_t xw = c.h * p.shift;
         const int32_t x0 = static_cast<int32_t>(xw - xw % kVec);
@@ -330,6 +408,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         MEC_TRACE_EV(tl, 1);
       }
     }
+    if constexpr (kGather) {
+      // Stage the k_h input rows s_h h + a of each image of the tile.  They are
+      // contiguous in I: one bulk copy per image (lane j copies image j) of the
+      // span's 16-byte-aligned superset; the builders recompute its offset.  A
+      // tile's coordinates and copy sizes are computed before waiting for its
+      // slot, so that arithmetic overlaps the wait.
+      const uintptr_t iend = reinterpret_cast<uintptr_t>(p.gI_end);
+      const uint32_t span = static_cast<uint32_t>(p.k_h * p.row_bytes);
+      for (int64_t t = t_begin; t < n_tiles; t += t_step) {
+        const int tl = static_cast<int>((t - t_begin) / t_step);
+        const int slotid = tl % p.n_slots;
+        const TileCoord c = decode_tile(p, v, nh_c, t);
+        const int64_t n = c.g * p.ipt + lane;
+        const bool mine = lane < p.ipt && n < p.i_n;
+        uintptr_t s0 = 0, s1 = 0, tail0 = 0;
+        if (mine) {
+          const uintptr_t src = reinterpret_cast<uintptr_t>(p.gI) +
+                                static_cast<uintptr_t>((n * p.i_h + c.h * p.s_h) * p.row_bytes);
+          s0 = src & ~uintptr_t(15);
+          s1 = (src + span + 15) & ~uintptr_t(15);
+          // the very end of I may fall inside a 16-byte granule: bulk-copy up to the
+          // last full granule, the final bytes with plain loads
+          tail0 = s1 > iend ? (iend & ~uintptr_t(15)) : s1;
+        }
+        const uint32_t bytes = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(tail0 - s0));
+        unsigned char* dimg = smemR + static_cast<size_t>(slotid) * p.slot_bytes +
+                              static_cast<size_t>(lane) * p.k_h * p.row_pitch;
+        ptx::mbar_wait(&rempty[slotid], ((tl / p.n_slots) & 1) ^ 1);
+        if (lane == 0) MEC_TRACE_EV(tl, 7);
+        if (mine && tail0 < s1) {
+          for (uintptr_t b = tail0; b < iend && b < s1; ++b)
+            dimg[b - s0] = *reinterpret_cast<const unsigned char*>(b);
+          __threadfence_block();
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_expect_tx(&rfull[slotid], bytes);  // release: tails above
+        __syncwarp();
+        if (mine && tail0 > s0)
+          ptx::bulk_load(dimg, reinterpret_cast<const void*>(s0), static_cast<uint32_t>(tail0 - s0),
+                         &rfull[slotid]);
+        if (lane == 0) MEC_TRACE_EV(tl, 15);
+      }
+    }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     int stage = 0;
@@ -340,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.resident && t_begin < n_tiles) ptx::mbar_wait(bfull, 0);
     for (int64_t t = t_begin; t < n_tiles; t += t_step) {
       const int tl = static_cast<int>((t - t_begin) / t_step);
-      const TileCoord c = decode_tile(p, v, t);
+      const TileCoord c = decode_tile(p, v, nh_c, t);
       const int acc = tl % p.n_acc;
       const uint32_t acc_phase = static_cast<uint32_t>(tl / p.n_acc) & 1u;
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -351,14 +472,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t started = 0;  // multi-row: accumulators that received an MMA
       for (int ks = 0; ks < n_ks; ++ks) {
         const int na = min(kAtomsPerStage, c.n_a - ks * kAtomsPerStage);
-        ptx::mbar_wait(&full[stage], phase);
+        if (kGather && p.spin) ptx::mbar_spin(&full[stage], phase);
+        else ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
         if (ks == 0 && lane == 0) MEC_TRACE_EV(tl, 3);
+        if (kGather && ks < 7 && lane == 0) MEC_TRACE_EV(tl, 8 + ks);
         {
           // the whole warp runs the (warp-uniform) descriptor arithmetic; one
           // elected lane issues each MMA / commit
           const uint32_t a_off = static_cast<uint32_t>(stage * kStageABytes) >> 4;
-          for (int a = 0; a < na; ++a) {
+          if constexpr (kGather) {
+            // A atom in TMEM columns a_col0 + 32 stage .. + 31: 4 MMAs of K = 32 bytes
+            const uint32_t a_tm = tmem_base + p.a_col0 + static_cast<uint32_t>(stage * 32);
+            const uint64_t bd = b_desc0 + static_cast<uint32_t>(ks) * b_tile16;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (p.dbg & 2) break;
+              ptx::mma_ts_elect<kTF32>(d_set, a_tm + 8 * k, bd + 2 * k, p.idesc, (ks | k) != 0 ? 1u : 0u);
+            }
+          }
+          for (int a = 0; !kGather && a < na; ++a) {
             const uint64_t ad = a_desc0 + a_off + static_cast<uint32_t>(a * (kAtomBytes >> 4));
             if (p.R == 1) {
               const uint32_t b_atom = p.resident ? static_cast<uint32_t>(ks * kAtomsPerStage + a)
@@ -406,25 +539,134 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+  } else if (kGather && warp >= kFirstBuildWarp) {
+    // ===================== A-atom builders (gather path) =====================
+    // Thread (quarter q = warp % 4, lane) owns tile row m = 32 q + lane: output
+    // pixel w of image slot j.  An A atom is 128 bytes of that row's padded
+    // window = 8 chunks of 16 bytes; chunk g is the contiguous run of I at
+    // staged byte  base(j) + w wstep_b + ctable[g]  (ctable: a row_bytes +
+    // 16 (g mod cpr)).  The atom goes to TMEM (tcgen05.st, row m -> lane m),
+    // where the MMA reads it as its A operand.  Builder group bgroup builds
+    // atoms bgroup, bgroup + kBuildGroups, ... of every tile.
+    const int wbg = warp - kFirstBuildWarp;
+    const int quarter = warp & 3;             // TMEM lanes [32 quarter, 32 quarter + 32)
+    const int bgroup = wbg >> 2;
+    const uint32_t table_s = ptx::smem_u32(ctable);
+    const uint32_t r_smem = ptx::smem_u32(smemR);
+    const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quarter) << 16) + p.a_col0;
+    const int m = 32 * quarter + lane;
+    const int j = m / p.slot;                 // image slot of this row
+    const int w_last = static_cast<int>(p.o_w) - 1;
+    // global atom sequence number: stage = seq mod S (S a power of two on this
+    // path); group g builds the atoms with seq = g mod kBuildGroups (balanced
+    // even when n_atoms is odd)
+    uint32_t seq = 0, seq_mod = 0;  // seq_mod = seq mod kBuildGroups
+    const uint32_t s_mask = static_cast<uint32_t>(S - 1);
+    const int s_log2 = __ffs(S) - 1;
+    for (int64_t t = t_begin; t < n_tiles; t += t_step) {
+      const int tl = static_cast<int>((t - t_begin) / t_step);
+      const int slotid = tl % p.n_slots;
+      const TileCoord c = decode_tile(p, v, nh_c, t);
+      const int w = min(static_cast<int>(c.mt * kBM) + m - j * p.slot, w_last);
+      const int64_t n = c.g * p.ipt + j;
+      // offset of the image's span inside its 16-byte-aligned bulk copy
+      const uint32_t sh = n < p.i_n ? static_cast<uint32_t>((reinterpret_cast<uintptr_t>(p.gI) +
+                                                              static_cast<uintptr_t>((n * p.i_h + c.h * p.s_h) * p.row_bytes)) & 15)
+                                    : 0u;
+      const uint32_t base = r_smem + static_cast<uint32_t>(slotid) * p.slot_bytes +
+                            static_cast<uint32_t>(j * p.k_h * p.row_pitch) + sh +
+                            static_cast<uint32_t>(w * p.wstep_b);
+      ptx::mbar_wait(&rfull[slotid], (tl / p.n_slots) & 1);
+      if (wbg == 0 && lane == 0) MEC_TRACE_EV(tl, 0);
+      const int atom0 = static_cast<int>((static_cast<uint32_t>(bgroup) + kBuildGroups - seq_mod) % kBuildGroups);
+      for (int atom = atom0; atom < p.n_atoms; atom += kBuildGroups) {
+        const uint32_t aseq = seq + static_cast<uint32_t>(atom);
+        const int stage = static_cast<int>(aseq & s_mask);
+        const uint32_t phase = (aseq >> s_log2) & 1u;
+        // two halves of 4 chunks (64 bytes of the row): all of a half's loads
+        // first (the asm loads keep program order, so interleaving them with the
+        // shifts would serialise their latencies), then its shifts and a
+        // 16-column TMEM store
+        const uint32_t t_atom = t_row + static_cast<uint32_t>(stage * 32);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const uint4 tt = ptx::ld_shared_v4(table_s + static_cast<uint32_t>(atom * 32 + half * 16));
+          const uint32_t addr[4] = {base + tt.x, base + tt.y, base + tt.z, base + tt.w};
+          uint2 xs[4][3];
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            const uint32_t al = addr[ch] & ~7u;
+            if (p.dbg & 8) {  // trace builds: no row loads
+              xs[ch][0] = xs[ch][1] = xs[ch][2] = make_uint2(al, al);
+              continue;
+            }
+            xs[ch][0] = ptx::ld_shared_v2(al);
+            xs[ch][1] = ptx::ld_shared_v2(al + 8);
+            xs[ch][2] = ptx::ld_shared_v2(al + 16);
+          }
+          uint32_t val[16];
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            const uint32_t A = addr[ch];
+            const uint2 x0 = xs[ch][0], x1 = xs[ch][1], x2 = xs[ch][2];
+            const bool hi = (A & 4u) != 0;
+            const uint32_t w0 = hi ? x0.y : x0.x, w1 = hi ? x1.x : x0.y, w2 = hi ? x1.y : x1.x;
+            const uint32_t w3 = hi ? x2.x : x1.y, w4 = hi ? x2.y : x2.x;
+            const uint32_t bs = (A & 3u) * 8u;
+            val[4 * ch + 0] = __funnelshift_r(w0, w1, bs);
+            val[4 * ch + 1] = __funnelshift_r(w1, w2, bs);
+            val[4 * ch + 2] = __funnelshift_r(w2, w3, bs);
+            val[4 * ch + 3] = __funnelshift_r(w3, w4, bs);
+          }
+          if (half == 0) {
+            if (p.spin) ptx::mbar_spin(&empty[stage], phase ^ 1);  // the MMAs that read this stage are done
+            else ptx::mbar_wait(&empty[stage], phase ^ 1);
+            ptx::tc_fence_after();
+            if (quarter == 0 && lane == 0) MEC_TRACE_EV2(tl, atom);
+          }
+          if (!(p.dbg & 16)) {  // trace builds: 16 = no TMEM stores
+            ptx::tmem_st_32x32b_x16(t_atom + static_cast<uint32_t>(16 * half), val);
+          } else {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc ^= val[i];
+            if (acc == 0x12345678u) p_sink_dummy(acc);
+          }
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&full[stage]);
+        if (quarter == 0 && lane == 0) MEC_TRACE_EV2(tl, 8 + atom);
+      }
+      seq += static_cast<uint32_t>(p.n_atoms);
+      seq_mod = (seq_mod + static_cast<uint32_t>(p.n_atoms)) % kBuildGroups;
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&rempty[slotid]);
+      if (wbg == 0 && lane == 0) MEC_TRACE_EV(tl, 1);
+    }
   } else {
     // ===================== epilogue (warps 2..9: two groups) =====================
     const int quarter = warp & 3;  // TMEM lanes [32 quarter, 32 quarter + 32)
     const int group = (warp - 2) >> 2;  // group g takes tiles tl = g, g + 2, ...
     constexpr int kOutElt = kTF32 ? 4 : 2;
-    const uint32_t stg = ptx::smem_u32(smemE) + static_cast<uint32_t>(warp - 2) * p.stage_out_bytes;
+    // per-warp staging: epi_bufs boxes used in turn, so a pass does not wait for
+    // the previous pass's TMA store to finish reading its box
+    unsigned char* const stg_gen0 = smemE + static_cast<size_t>(warp - 2) * p.epi_bufs * p.stage_out_bytes;
+    const uint32_t stg0 = ptx::smem_u32(stg_gen0);
+    int ebuf = 0;
     const int row_bytes = p.pw * kOutElt;  // 128, 64 or 32
     // swizzle of the staging box (matches the O tensor map): chunk c of row r
     // lives at chunk c ^ f(r) -- conflict-free 16-byte stores
     const int swz_shift = row_bytes == 128 ? 0 : (row_bytes == 64 ? 1 : 2);
     const int swz_mask = row_bytes == 128 ? 7 : (row_bytes == 64 ? 3 : 1);
-    const uint32_t my_row = stg + static_cast<uint32_t>(lane * row_bytes);
     const uint32_t my_x = static_cast<uint32_t>((lane >> swz_shift) & swz_mask);
     const int64_t cols_left = p.k_c - static_cast<int64_t>(nt) * p.bn;
     for (int64_t t = t_begin + group * t_step; t < n_tiles; t += kEpiGroups * t_step) {
       const int tl = static_cast<int>((t - t_begin) / t_step);
       const int acc = tl % p.n_acc;
       const uint32_t acc_phase = static_cast<uint32_t>(tl / p.n_acc) & 1u;
-      TileCoord c = decode_tile(p, v, t);
+      TileCoord c = decode_tile(p, v, nh_c, t);
       // this warp's 32 rows: image n, columns w0 .. w0 + nvalid - 1 (packed), or
       // flattened rows gr0 .. gr0 + nvalid - 1 (flat)
       int64_t gr0, nvalid, n_img = 0, w0 = 0;
@@ -466,16 +708,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int c0 = pass * p.pw;
         uint32_t v16[4][16];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j * 16 < p.pw) ptx::tmem_ld_32x32b_x16(taddr + c0 + 16 * j, v16[j]);
-        ptx::tmem_ld_wait();
-        if ((warp & 3) == 2 && lane == 0 && pass < 2) MEC_TRACE_EV(tl, 8 + 4 * pass);
+        if (p.dbg & 64) {  // trace builds: no TMEM loads in the epilogue
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v16[j][e] = static_cast<uint32_t>(c0 + e);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j * 16 < p.pw) ptx::tmem_ld_32x32b_x16(taddr + c0 + 16 * j, v16[j]);
+          ptx::tmem_ld_wait();
+        }
+        if (!kGather && (warp & 3) == 2 && lane == 0 && pass < 2) MEC_TRACE_EV(tl, 8 + 4 * pass);
         if (nvalid <= 0 || c0 >= cols_left) continue;  // warp-uniform
         if (p.tma_store) {
-          // the previous pass's TMA store must have finished reading the staging box
-          if (lane == 0) ptx::bulk_wait_group_read<0>();
+          // the TMA store that last used this staging box must have finished reading it
+          const uint32_t stg = stg0 + static_cast<uint32_t>(ebuf) * p.stage_out_bytes;
+          unsigned char* const stg_gen = stg_gen0 + static_cast<size_t>(ebuf) * p.stage_out_bytes;
+          const uint32_t my_row = stg + static_cast<uint32_t>(lane * row_bytes);
+          if (++ebuf == p.epi_bufs) ebuf = 0;
+          if (lane == 0) {
+            if (p.epi_bufs > 1)
+              ptx::bulk_wait_group_read<1>();
+            else
+              ptx::bulk_wait_group_read<0>();
+          }
           __syncwarp();
-          if ((warp & 3) == 2 && lane == 0 && pass < 2) MEC_TRACE_EV(tl, 10 + 4 * pass);
+          if (!kGather && (warp & 3) == 2 && lane == 0 && pass < 2) MEC_TRACE_EV(tl, 10 + 4 * pass);
           const int nchunk = row_bytes / 16;
 #pragma unroll
           for (int ch = 0; ch < 8; ++ch) {
@@ -498,24 +757,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           ptx::fence_proxy_async_smem();
           __syncwarp();
-          if ((warp & 3) == 2 && lane == 0 && pass < 2) MEC_TRACE_EV(tl, 9 + 4 * pass);
+          if (!kGather && (warp & 3) == 2 && lane == 0 && pass < 2) MEC_TRACE_EV(tl, 9 + 4 * pass);
           const int32_t col = static_cast<int32_t>(nt * p.bn + c0);
           if (!p.flat) {
             // packed: the 32 rows lie in image n_img (rows past o_w are clipped)
             if (lane == 0 && !(p.dbg & 1)) {
               if (p.out_hnwc)  // O_hnwc as {k_c, o_w, i_n, o_h}
-                ptx::tma_store_4d(&tmO, smemE + (warp - 2) * p.stage_out_bytes, col,
+                ptx::tma_store_4d(&tmO, stg_gen, col,
                                   static_cast<int32_t>(w0), static_cast<int32_t>(n_img),
                                   static_cast<int32_t>(c.h));
               else  // O as {k_c, o_w, o_h, i_n}
-                ptx::tma_store_4d(&tmO, smemE + (warp - 2) * p.stage_out_bytes, col,
+                ptx::tma_store_4d(&tmO, stg_gen, col,
                                   static_cast<int32_t>(w0), static_cast<int32_t>(c.h),
                                   static_cast<int32_t>(n_img));
               ptx::bulk_commit_group();
             }
           } else if (p.out_hnwc) {
             if (lane == 0 && !(p.dbg & 1)) {
-              ptx::tma_store_3d(&tmO, smemE + (warp - 2) * p.stage_out_bytes, col,
+              ptx::tma_store_3d(&tmO, stg_gen, col,
                                 static_cast<int32_t>(gr0), static_cast<int32_t>(c.h));
               ptx::bulk_commit_group();
             }
@@ -527,7 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t n_first = gr0 / p.o_w;
             const int k_first = static_cast<int>(min(nvalid, (n_first + 1) * p.o_w - gr0));
             if (lane == 0 && !(p.dbg & 1)) {
-              ptx::tma_store_4d(&tmO, smemE + (warp - 2) * p.stage_out_bytes, col,
+              ptx::tma_store_4d(&tmO, stg_gen, col,
                                 static_cast<int32_t>(gr0 - n_first * p.o_w), static_cast<int32_t>(c.h),
                                 static_cast<int32_t>(n_first));
               ptx::bulk_commit_group();
@@ -594,6 +853,43 @@ bool fused_eligible(const Plan& pl) {
   return (pl.s.i_c * pl.elt) % kTileKBytes == 0 && pl.s_w <= 2;
 }
 
+namespace {
+// staged row pitch: row bytes + slack for the 16-byte alignment shift of a
+// span and the builders' 24-byte chunk reads past its end
+int gather_row_pitch(const Plan& pl) {
+  return static_cast<int>((pl.s.i_w * pl.s.i_c * pl.elt + 48 + 15) / 16 * 16);
+}
+int tile_ipt(const Plan& pl) {
+  if (pl.o_w > 128) return 1;
+  const int slot = static_cast<int>((pl.o_w + 31) / 32 * 32);
+  return std::max(1, 128 / slot);
+}
+int64_t gather_slot_bytes(const Plan& pl) {
+  return (static_cast<int64_t>(tile_ipt(pl)) * pl.s.k_h * gather_row_pitch(pl) + 127) / 128 * 128;
+}
+constexpr size_t kSmemBudget = 222 * 1024;  // usable dynamic smem after the 1 KB alignment slack
+// epilogue staging boxes (32 rows x 128/64/32 bytes) per epilogue warp: 2 on
+// the gather path (4 epilogue warps), 1 on the TMA paths (8 warps; their smem
+// goes to A stages)
+int epi_bufs(bool gather) { return gather ? 2 : 1; }
+size_t epi_bytes(const Plan& pl, bool gather) {
+  int row_bytes = 128;
+  while (row_bytes > 32 && (pl.bn * pl.elt) % row_bytes != 0) row_bytes /= 2;
+  return static_cast<size_t>(4 * (gather ? 1 : 2)) * epi_bufs(gather) * 32 * row_bytes;
+}
+}  // namespace
+
+bool gather_eligible(const Plan& pl) {
+  if (fused_eligible(pl)) return false;
+  const int64_t n_atoms = pl.kdim_g / pl.bk;
+  const int64_t b_res = static_cast<int64_t>(pl.bn) * kTileKBytes * n_atoms;
+  const int64_t need = b_res + 2 * gather_slot_bytes(pl) + n_atoms * 32 + 64 +
+                       static_cast<int64_t>(epi_bytes(pl, true));
+  // one N tile (k_c <= 256); weights resident; two staged-row slots; A in TMEM
+  return pl.n_tiles_n == 1 && need <= static_cast<int64_t>(kSmemBudget) &&
+         pl.s.i_w * pl.s.i_c * pl.elt < (1LL << 24) && pl.s.k_h < 256;
+}
+
 cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st,
                                int* launches) {
   const bool tf32 = pl.dt == MEC_DTYPE_TF32;
@@ -611,7 +907,10 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   const int64_t rows = flat ? pl.s.i_n * pl.o_w : pl.o_w;
   const int64_t groups = flat ? 1 : (pl.s.i_n + ipt - 1) / ipt;
   const int64_t n_mt = flat ? (rows + kBM - 1) / kBM : (ipt > 1 ? 1 : (pl.o_w + kBM - 1) / kBM);
-  if (a.fused) {
+  const bool gather = a.fused && !fused_eligible(pl);
+  if (gather) {
+    std::memset(&tmA, 0, sizeof(tmA));  // A atoms are assembled in smem by builder warps
+  } else if (a.fused) {
     // A: the NHWC input as {i_c, i_w, i_h, i_n}; a box is bk channels x `rows`
     // pixels taken every s_w pixels (elementStrides) -- one K-atom of `rows`
     // windows, read in place: L is never materialised.
@@ -639,9 +938,10 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   }
   // B: the prepared weight operand Kt, n_var x kc_pad rows of kdim_pad, K-major.
   {
-    const uint64_t dims[2] = {static_cast<uint64_t>(pl.kdim_pad),
-                              static_cast<uint64_t>(pl.n_var * pl.kc_pad)};
-    const uint64_t strides[1] = {static_cast<uint64_t>(pl.kdim_pad) * pl.elt};
+    const int64_t kcols = gather ? pl.kdim_g : pl.kdim_pad;
+    const uint64_t dims[2] = {static_cast<uint64_t>(kcols),
+                              static_cast<uint64_t>((gather ? 1 : pl.n_var) * pl.kc_pad)};
+    const uint64_t strides[1] = {static_cast<uint64_t>(kcols) * pl.elt};
     const uint32_t box[2] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(pl.bn)};
     cudaError_t e = encode_tiled(&tmB, tf32, 2, a.Kt, dims, strides, box);
     if (e != cudaSuccess) return e;
@@ -662,7 +962,18 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   p.shift = pl.shift;
   p.kc_pad = pl.kc_pad;
   p.bk = pl.bk;
-  p.n_atoms = static_cast<int>((a.fused ? pl.kdim : pl.kdim_pad) / pl.bk);
+  p.n_atoms = static_cast<int>(gather ? pl.kdim_g / pl.bk
+                                      : (a.fused ? (pl.kdim + pl.bk - 1) / pl.bk : pl.kdim_pad / pl.bk));
+  p.cpr = static_cast<int>(pl.kwc_p * pl.elt / 16);
+  p.gI = static_cast<const unsigned char*>(a.L);
+  p.gI_end = p.gI + static_cast<size_t>(pl.s.i_n * pl.s.i_h * pl.s.i_w * pl.s.i_c) * pl.elt;
+  p.k_h = static_cast<int>(pl.s.k_h);
+  p.i_h = pl.s.i_h;
+  p.i_w = pl.s.i_w;
+  p.row_bytes = static_cast<int>(pl.s.i_w * pl.s.i_c * pl.elt);
+  p.row_pitch = gather_row_pitch(pl);
+  p.kwc = static_cast<int>(pl.s.k_w * pl.s.i_c);
+  p.wstep_b = static_cast<int>(pl.s_w * pl.s.i_c * pl.elt);
   p.fused = a.fused;
   p.ncb = static_cast<int>(pl.s.i_c / pl.bk);
   p.k_w = static_cast<int>(pl.s.k_w);
@@ -688,6 +999,8 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
 #ifdef MEC_TRACE
   if (const char* e = getenv("MEC_DEBUG_FLAGS")) p.dbg = atoi(e);
 #endif
+  p.spin = gather;
+  if (const char* e = getenv("MEC_GATHER_SPIN")) p.spin = gather && atoi(e) != 0;
   p.idesc = ptx::instr_desc(tf32, kBM, pl.bn);
   p.kchunk = 32 / pl.elt;
   p.kchunk_log2 = pl.elt == 2 ? 4 : 3;
@@ -704,6 +1017,7 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   // k_c = 8 with a 16-column box): such shapes use the register-store path
   if (pl.s.k_c % p.pw != 0) p.tma_store = false;
   p.stage_out_bytes = static_cast<uint32_t>(32 * row_bytes);  // 1-4 KB, swizzle-atom aligned
+  p.epi_bufs = epi_bufs(gather);
   if (p.tma_store) {
     if (a.out_hnwc && flat) {  // O_hnwc viewed as {k_c, i_n o_w, o_h}
       const uint64_t dims[3] = {static_cast<uint64_t>(pl.s.k_c),
@@ -739,17 +1053,34 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
 
   const size_t b_tile = static_cast<size_t>(pl.bn) * kTileKBytes;
   const size_t b_res = b_tile * p.n_atoms;
-  const size_t epi = static_cast<size_t>(kEpiWarps) * p.stage_out_bytes;
-  const size_t budget = 222 * 1024 - epi;  // after the 1 KB alignment slack
-  p.resident = b_res + 2 * kMaxAtomsPerStage * kAtomBytes <= budget && b_res <= 120 * 1024;
-  p.aps = p.resident ? 2 : 1;
-  const size_t stage_a = static_cast<size_t>(p.aps) * kAtomBytes;
+  const size_t epi = epi_bytes(pl, gather);
+  const size_t budget = kSmemBudget - epi;
+  if (gather) p.slot_bytes = static_cast<uint32_t>(gather_slot_bytes(pl));
+  if (gather) {
+    // as many staged-row slots (2..4) as fit next to the resident weights: the
+    // rows of tile t are requested when tile t - n_slots has been built
+    const size_t fixed = b_res + p.n_atoms * 32 + 64;
+    p.n_slots = 2;
+    while (p.n_slots < 4 && fixed + (p.n_slots + 1) * static_cast<size_t>(p.slot_bytes) <= budget) ++p.n_slots;
+  }
+  const size_t gather_bytes =
+      gather ? p.n_slots * static_cast<size_t>(p.slot_bytes) + p.n_atoms * 32 + 64 : 0;
+  if (gather_bytes > budget) return cudaErrorInvalidConfiguration;
+  const size_t budget_g = budget - gather_bytes;
+  // gather: A atoms live in TMEM, so only the weights need shared memory
+  p.resident = gather ? b_res <= budget_g
+                      : (b_res + 2 * kMaxAtomsPerStage * kAtomBytes <= budget_g && b_res <= 120 * 1024);
+  if (gather && !p.resident) return cudaErrorInvalidConfiguration;
+  p.aps = (p.resident && !gather) ? 2 : 1;
+  const size_t stage_a = gather ? 0 : static_cast<size_t>(p.aps) * kAtomBytes;
   p.n_kstages = (p.n_atoms + p.aps - 1) / p.aps;
   int stages;
-  if (p.resident) {
-    stages = static_cast<int>(std::min<size_t>(8, (budget - b_res) / stage_a));
+  if (gather) {
+    stages = 8;  // set from the TMEM budget below
+  } else if (p.resident) {
+    stages = static_cast<int>(std::min<size_t>(8, (budget_g - b_res) / stage_a));
   } else {
-    stages = static_cast<int>(std::min<size_t>(8, budget / (stage_a + p.aps * b_tile)));
+    stages = static_cast<int>(std::min<size_t>(8, budget_g / (stage_a + p.aps * b_tile)));
   }
   // multi-row tiles (see GemmParams::R)
   // Multi-row tiles (requested via mec_options_t::rows_per_tile) are parity-
@@ -771,14 +1102,27 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(p.n_acc * p.R * pl.bn)) cols <<= 1;
   p.tmem_cols = cols;
+  if (gather) {
+    // TMEM: n_acc accumulators, then A stages of 32 columns (128 bytes per row)
+    // as many accumulators as leave >= 4 A stages (>= 2 for the widest N tiles)
+    p.n_acc = 1;
+    for (int k = 4; k >= 2; --k)
+      if ((k * pl.bn + 31) / 32 * 32 + 4 * 32 <= 512) { p.n_acc = k; break; }
+    p.a_col0 = static_cast<uint32_t>((p.n_acc * pl.bn + 31) / 32 * 32);
+    p.tmem_cols = 512;
+    stages = static_cast<int>(std::min<uint32_t>(8, (512 - p.a_col0) / 32));
+    while (stages & (stages - 1)) --stages;  // a power of two (builders' stage arithmetic)
+  }
   stages = std::max(1, std::min(stages, std::max(2, 2 * p.n_kstages)));
 #ifdef MEC_TRACE
   if (const char* e = getenv("MEC_DEBUG_STAGES")) stages = std::min(stages, atoi(e));
 #endif
+  if (gather)
+    while (stages & (stages - 1)) --stages;
   p.stages = stages;
   const size_t smem = kSmemAlign + stages * stage_a +
-                      (p.resident ? b_res : stages * p.aps * b_tile) + epi +
-                      (2 * stages + 10) * 8 + 16;
+                      (p.resident ? b_res : stages * p.aps * b_tile) + epi + gather_bytes +
+                      (2 * stages + 18) * 8 + 32;
 
   // grid: a multiple of the combo count, at most one CTA per SM
   int64_t max_tiles = 0;
@@ -791,12 +1135,15 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   int64_t per = std::max<int64_t>(1, num_sms() / p.n_combo);
   per = std::min<int64_t>(per, max_tiles);
   p.ctas_per_combo = static_cast<int>(per);
+  p.tiles32 = max_tiles + per < (1LL << 31) && pl.o_h < (1LL << 31);
   const int64_t grid = per * p.n_combo;
-  auto kern = tf32 ? window_gemm_kernel<true> : window_gemm_kernel<false>;
+  auto kern = tf32 ? (gather ? window_gemm_kernel<true, true> : window_gemm_kernel<true, false>)
+                   : (gather ? window_gemm_kernel<false, true> : window_gemm_kernel<false, false>);
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(tmA, tmB, tmO, p);
+  const int threads = gather ? kernel_threads<true>() : kernel_threads<false>();
+  kern<<<static_cast<unsigned>(grid), threads, smem, st>>>(tmA, tmB, tmO, p);
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -120,10 +120,12 @@ def test_argument_validation_without_device_work():
     opt.path = 9
     assert L.mec_conv_forward_ex(16, 32, 48, ctypes.byref(s), 1, 1, 0, None, ctypes.byref(opt)) == \
         _lib.MEC_ERR_INVALID_ARG
-    # forced fused path is reserved
+    # forced fused path on a shape neither fused variant takes (k_c > 256: two N tiles,
+    # i_c elt not a multiple of 128 B) -- rejected host-side
+    s3 = _lib.MecShape(1, 7, 7, 1, 3, 3, 300)
     L.mec_options_init(ctypes.byref(opt))
     opt.path = _lib.MEC_PATH_FUSED
-    assert L.mec_conv_forward_ex(16, 32, 48, ctypes.byref(s), 1, 1, 0, None, ctypes.byref(opt)) == \
+    assert L.mec_conv_forward_ex(16, 32, 48, ctypes.byref(s3), 1, 1, 0, None, ctypes.byref(opt)) == \
         _lib.MEC_ERR_UNSUPPORTED
     # Solution A's literal format fix needs #L >= #O: 1x6x6x1, 3x3x8 -> #O 128 > #L 72
     s2 = _lib.MecShape(1, 6, 6, 1, 3, 3, 8)

@@ -208,16 +208,54 @@ def test_fused_path_misc(cuda_ok, shape, s):
     check_O(OF, ref, "bf16", shape[3] * shape[4] * shape[5])
 
 
+GATHER_CASES = [("cv1", 3), ("cv2", 2), ("cv3", 2), ("cv7", 1)]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("name,batch", GATHER_CASES)
+def test_fused_gather_path(cuda_ok, name, batch, dtype):
+    """MEC_PATH_FUSED for small i_c (AlexNet conv1 and co.): input rows staged by
+    bulk copies, A atoms assembled in smem by builder warps, L never written."""
+    from paper_1706_06873_b200._lib import MEC_PATH_FUSED
+    i_h, i_w, i_c, k_h, k_w, k_c, s = synth.TABLE2[name]
+    shape = (batch, i_h, i_w, i_c, k_h, k_w, k_c)
+    I, K = make_inputs(shape, dtype, seed=5000 + int(name[2:]))
+    if dtype == "tf32" and name in ("cv1", "cv2"):
+        # fp32 weights of an 11x11x3x96 kernel (147 KB) cannot stay resident next to
+        # the staged rows: the fused gather path refuses, the two-kernel path runs it
+        with pytest.raises(MecError):
+            mec.conv_forward(to_dev(I, dtype), to_dev(K, dtype), s, s, path=MEC_PATH_FUSED)
+        return
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    OF, chosen = mec.conv_forward(to_dev(I, dtype), to_dev(K, dtype), s, s, path=MEC_PATH_FUSED,
+                                  return_path=True)
+    torch.cuda.synchronize()
+    assert chosen == MEC_PATH_FUSED
+    check_O(OF, ref, dtype, k_h * k_w * i_c)
+
+
+@pytest.mark.parametrize("shape,s", [((3, 9, 11, 3, 3, 5, 8), 1), ((2, 30, 16, 64, 3, 3, 32), 3),
+                                     ((5, 23, 21, 6, 3, 3, 24), 2), ((2, 40, 38, 5, 4, 3, 40), 1)])
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_fused_gather_misc(cuda_ok, shape, s, dtype):
+    from paper_1706_06873_b200._lib import MEC_PATH_FUSED
+    I, K = make_inputs(shape, dtype, seed=91)
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    OF = mec.conv_forward(to_dev(I, dtype), to_dev(K, dtype), s, s, path=MEC_PATH_FUSED)
+    check_O(OF, ref, dtype, shape[3] * shape[4] * shape[5])
+
+
+def test_fused_gather_C1_full_batch_sampled(cuda_ok):
+    from paper_1706_06873_b200._lib import MEC_PATH_FUSED
+    sampled_parity("C1", "bf16", [0, 13, 31], path=MEC_PATH_FUSED)
+
+
 def test_fused_path_unsupported_shapes(cuda_ok):
     from paper_1706_06873_b200._lib import MEC_PATH_FUSED
-    I = torch.zeros(1, 20, 20, 3, device="cuda", dtype=torch.bfloat16)  # i_c = 3: 6-byte pixels
-    K = torch.zeros(3, 3, 3, 8, device="cuda", dtype=torch.bfloat16)
+    I = torch.zeros(1, 20, 20, 3, device="cuda", dtype=torch.bfloat16)
+    K = torch.zeros(3, 3, 3, 300, device="cuda", dtype=torch.bfloat16)  # two N tiles: not fused
     with pytest.raises(MecError):
         mec.conv_forward(I, K, 1, 1, path=MEC_PATH_FUSED)
-    I = torch.zeros(1, 30, 30, 64, device="cuda", dtype=torch.bfloat16)  # s_w = 3 > 2
-    K = torch.zeros(3, 3, 64, 8, device="cuda", dtype=torch.bfloat16)
-    with pytest.raises(MecError):
-        mec.conv_forward(I, K, 3, 3, path=MEC_PATH_FUSED)
 
 
 # ------------------------------------------------------------------ lowering

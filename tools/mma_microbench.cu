@@ -12,20 +12,23 @@
 
 using namespace mec;
 
-template <bool kElectInAsm>
+// kMode: 0 = SS, elect in asm; 1 = SS, elect block; 2 = TS (A in TMEM cols 256..); 3 = TS + commit per 4
+template <int kMode>
 __global__ void __launch_bounds__(128, 1) mma_bench(int n, int iters, unsigned long long* cycles) {
+  constexpr bool kElectInAsm = kMode != 1;
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2;
   __shared__ uint32_t tslot;
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar, 1);
+    ptx::mbar_init(&bar2, 1);
     ptx::fence_mbar_init();
   }
   // zero operands
-  for (int i = threadIdx.x; i < (32768 + 32768) / 16; i += blockDim.x)
+  for (int i = threadIdx.x; i < (32768 + 7 * 16384) / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
-  if (warp == 0) ptx::tmem_alloc_dyn(&tslot, 256);
+  if (warp == 0) ptx::tmem_alloc_dyn(&tslot, 512);
   ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
   __syncthreads();
@@ -37,7 +40,25 @@ __global__ void __launch_bounds__(128, 1) mma_bench(int n, int iters, unsigned l
     const uint64_t bd0 = ptx::smem_desc_sw128(ptx::smem_u32(smem + 32768));
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
-      if constexpr (kElectInAsm) {
+      if constexpr (kMode >= 4) {
+        // 7 B atoms (N x 128 B each), 4 MMAs per atom, commit per atom (kernel-like)
+#pragma unroll 1
+        for (int a = 0; a < 7; ++a) {
+          const uint64_t bd = bd0 + static_cast<uint32_t>(a * n * 128 / 16);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            ptx::mma_ts_elect<false>(tmem, tmem + 256 + 32 * (a & 3) + 8 * k, bd + 2 * k, idesc, (it | a | k) != 0);
+          ptx::mma_commit_elect(&bar2);
+        }
+      } else if constexpr (kMode >= 2) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          ptx::mma_ts_elect<false>(tmem, tmem + 256 + 8 * (k & 3) + 32 * (k >> 2), bd0 + (k & 3) * 2, idesc,
+                                   (it | k) != 0);
+          if (kMode == 3 && (k & 3) == 3) ptx::mma_commit_elect(&bar2);
+        }
+      } else if constexpr (kElectInAsm) {
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           ptx::mma_ss_elect<false>(tmem, ad0 + (k & 3) * 2 + (k >> 2) * 1024, bd0 + (k & 3) * 2, idesc,
@@ -57,32 +78,49 @@ __global__ void __launch_bounds__(128, 1) mma_bench(int n, int iters, unsigned l
     const long long t1 = clock64();
     if (threadIdx.x == 32) cycles[blockIdx.x] = t1 - t0;
   }
+  if (kMode == 5 && warp >= 2) {
+    uint32_t acc = 0;
+    const uint32_t base = ptx::smem_u32(smem) + (threadIdx.x & 31) * 24;
+    for (int i = 0; i < iters * 40; ++i) {
+      const uint2 v = ptx::ld_shared_v2(base + (i & 63) * 8);
+      acc += v.x ^ v.y;
+    }
+    if (acc == 0x12345) cycles[1023] = acc;
+  }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 0) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, 256);
+    ptx::tmem_dealloc(tmem, 512);
   }
 }
 
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 1024 * sizeof(unsigned long long));
-  const int smem = 65536 + 1024;
-  cudaFuncSetAttribute(mma_bench<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(mma_bench<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = 32768 + 7 * 16384 + 1024;
+  cudaFuncSetAttribute(mma_bench<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_bench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_bench<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_bench<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_bench<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  for (int variant = 0; variant < 2; ++variant) {
-    for (int n : {32, 64, 96, 128, 192, 256}) {
+  const char* names[6] = {"SS elect-in-asm", "SS elect-block ", "TS             ", "TS commit/4    ",
+                          "TS 7 B atoms   ", "TS 7B + LDS    "};
+  for (int variant = 0; variant < 6; ++variant) {
+    for (int n : {32, 64, 96, 128}) {
       cudaEvent_t a, b;
       cudaEventCreate(&a);
       cudaEventCreate(&b);
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(a);
-        if (variant == 0)
-          mma_bench<true><<<148, 128, smem>>>(n, iters, d);
-        else
-          mma_bench<false><<<148, 128, smem>>>(n, iters, d);
+        if (variant == 0) mma_bench<0><<<148, 128, smem>>>(n, iters, d);
+        if (variant == 1) mma_bench<1><<<148, 128, smem>>>(n, iters, d);
+        if (variant == 2) mma_bench<2><<<148, 128, smem>>>(n, iters, d);
+        if (variant == 3) mma_bench<3><<<148, 128, smem>>>(n, iters, d);
+        if (variant == 4) mma_bench<4><<<148, 128, smem>>>(n, iters, d);
+        if (variant == 5) mma_bench<5><<<148, 128, smem>>>(n, iters, d);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
       }
@@ -90,10 +128,10 @@ int main() {
       cudaEventElapsedTime(&ms, a, b);
       unsigned long long h[148];
       cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-      const double mmas = 8.0 * iters;
+      const double mmas = (variant >= 4 ? 28.0 : 8.0) * iters;
       const double flops = 148.0 * mmas * 2.0 * 128 * n * 16;
       printf("%s N=%3d: %.1f cycles/MMA (cta0), %.3f ms, %.0f TFLOP/s  [%s]\n",
-             variant == 0 ? "elect-in-asm" : "elect-block ", n, h[0] / mmas, ms, flops / (ms * 1e-3) / 1e12,
+             names[variant], n, h[0] / mmas, ms, flops / (ms * 1e-3) / 1e12,
              cudaGetErrorString(cudaGetLastError()));
     }
   }

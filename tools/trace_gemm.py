@@ -18,7 +18,7 @@ tdt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
 I = torch.empty((cfg["i_n"], cfg["i_h"], cfg["i_w"], cfg["i_c"]), dtype=tdt, device="cuda")
 K = torch.empty((cfg["k_h"], cfg["k_w"], cfg["i_c"], cfg["k_c"]), dtype=tdt, device="cuda")
 mec.synth_fill(I, 1, 0, 0); mec.synth_fill(K, 1, 1, 0)
-path = {"auto": 0, "A": 1, "B": 2}[args.path]
+path = {"auto": 0, "A": 1, "B": 2, "fused": 3}[args.path]
 for _ in range(3): mec.conv_forward(I, K, cfg["s_h"], cfg["s_w"], path=path)
 torch.cuda.synchronize()
 buf = ctypes.c_void_p(); nbytes = ctypes.c_size_t()
@@ -38,7 +38,10 @@ for c in ([] if args.quiet else list(ctas[:2]) + [ctas[-1]]):
     for tl in range(64):
         row = tr[c, tl, :7]
         if row[0] == 0 and row[2] == 0: break
-        print("  tile", tl, " ".join(f"{n}={(x - t0)/1e3:7.2f}" if x else f"{n}=   -   " for n, x in zip(names, row)))
+        extra = "".join(f" {n}={(tr[c, tl, e] - t0)/1e3:7.2f}" for n, e in
+                        (("R_wait", 7), ("R_dec", 8), ("R_arm", 9), ("R_cp0", 10), ("R_cp1", 11), ("R_req", 15))
+                        if tr[c, tl, e])
+        print("  tile", tl, " ".join(f"{n}={(x - t0)/1e3:7.2f}" if x else f"{n}=   -   " for n, x in zip(names, row)) + extra)
 # aggregates
 ends = tr[ctas][:, :, 6]; ends = ends[ends > 0]
 print("kernel span us", (ends.max() - t0) / 1e3)
@@ -52,5 +55,21 @@ sub = tr[ctas][:, 1:, :]
 def med(a, b):
     m = (sub[:, :, a] > 0) & (sub[:, :, b] > 0)
     return np.median((sub[:, :, b] - sub[:, :, a])[m]) / 1e3 if m.any() else float('nan')
+if (sub[:, :, 15] > 0).any():
+    print("gather: rempty->copies issued %.3f | copies issued->rows ready %.3f | rows ready->built %.3f" % (
+        med(7, 15), med(15, 0), med(0, 1)))
+    print("gather: built(t-2) -> rempty(t) passed %.3f" % np.median(((sub[:, 2:, 7] - sub[:, :-2, 1]))[(sub[:, 2:, 7] > 0) & (sub[:, :-2, 1] > 0)] / 1e3))
+b2 = tr[512 + ctas][:, 1:, :]
+if (b2[:, :, 8] > 0).any():
+    def med2(bank_a, ia, bank_b, ib):
+        A = bank_a[:, :, ia]; B = bank_b[:, :, ib]; m = (A > 0) & (B > 0)
+        return np.median((B - A)[m]) / 1e3 if m.any() else float('nan')
+    print("builder per atom (us after M_tempty): empty passed:", " ".join("%.2f" % med2(sub, 2, b2, k) for k in range(7)))
+    print("builder per atom (us after M_tempty): full arrived:", " ".join("%.2f" % med2(sub, 2, b2, 8 + k) for k in range(7)))
+    print("builder build time per atom (empty passed -> arrived):", " ".join("%.2f" % med2(b2, k, b2, 8 + k) for k in range(7)))
+if (sub[:, :, 14] > 0).any():
+    print("gather MMA full-wait passes (us after tempty), median per atom:",
+          " ".join("%.2f" % med(2, 8 + k) for k in range(7)))
+    print("stages", os.environ.get("MEC_DEBUG_STAGES"))
 print("epilogue breakdown (median us, tiles >= 1): tfull->p0 ldwait %.3f | ldwait->bulkwait %.3f | bulkwait->staged %.3f | p0 staged->p1 ldwait %.3f | p1 ldwait->bulkwait %.3f | p1 bulkwait->staged %.3f | p1 staged -> done %.3f" % (
     med(5, 8), med(8, 10), med(10, 9), med(9, 12), med(12, 14), med(14, 13), med(13, 6)))
