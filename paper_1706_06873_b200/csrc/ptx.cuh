@@ -65,6 +65,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// try_wait with a nanosleep backoff between failed probes: for waits that are
+// usually long (epilogue waiting for an accumulator, producer waiting for a
+// slot), so idle warps do not keep the mbarrier unit busy.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  while (!ok) {
+    __nanosleep(ns);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+
 // Pure spin on the non-blocking test_wait (no hardware suspend between probes).
 __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);

@@ -193,6 +193,7 @@ struct GemmParams {
   uint32_t stage_out_bytes;  // staging box bytes (32 rows x pw x elt, 1 KB aligned)
   int epi_bufs;              // staging boxes per epilogue warp (1 or 2)
   bool spin;        // gather: builder/MMA handshakes spin on test_wait
+  uint32_t backoff_ns;  // gather: nanosleep between probes of the long waits (0 = none)
   int dbg;  // trace builds only: 1 = no epilogue stores, 2 = no MMA, 4 = no A loads,
             // 8 = gather builders skip row loads, 16 = gather builders skip TMEM stores,
             // 64 = epilogue skips TMEM loads
@@ -435,7 +436,8 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
         const uint32_t bytes = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(tail0 - s0));
         unsigned char* dimg = smemR + static_cast<size_t>(slotid) * p.slot_bytes +
                               static_cast<size_t>(lane) * p.k_h * p.row_pitch;
-        ptx::mbar_wait(&rempty[slotid], ((tl / p.n_slots) & 1) ^ 1);
+        if (p.backoff_ns > 0) ptx::mbar_wait_backoff(&rempty[slotid], ((tl / p.n_slots) & 1) ^ 1, p.backoff_ns);
+        else ptx::mbar_wait(&rempty[slotid], ((tl / p.n_slots) & 1) ^ 1);
         if (lane == 0) MEC_TRACE_EV(tl, 7);
         if (mine && tail0 < s1) {
           for (uintptr_t b = tail0; b < iend && b < s1; ++b)
@@ -596,10 +598,12 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             const uint32_t al = addr[ch] & ~7u;
+#ifdef MEC_TRACE
             if (p.dbg & 8) {  // trace builds: no row loads
               xs[ch][0] = xs[ch][1] = xs[ch][2] = make_uint2(al, al);
               continue;
             }
+#endif
             xs[ch][0] = ptx::ld_shared_v2(al);
             xs[ch][1] = ptx::ld_shared_v2(al + 8);
             xs[ch][2] = ptx::ld_shared_v2(al + 16);
@@ -612,7 +616,7 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
             const bool hi = (A & 4u) != 0;
             const uint32_t w0 = hi ? x0.y : x0.x, w1 = hi ? x1.x : x0.y, w2 = hi ? x1.y : x1.x;
             const uint32_t w3 = hi ? x2.x : x1.y, w4 = hi ? x2.y : x2.x;
-            const uint32_t bs = (A & 3u) * 8u;
+            const uint32_t bs = A << 3;  // shf.r uses the low 5 bits: (A mod 4) bytes
             val[4 * ch + 0] = __funnelshift_r(w0, w1, bs);
             val[4 * ch + 1] = __funnelshift_r(w1, w2, bs);
             val[4 * ch + 2] = __funnelshift_r(w2, w3, bs);
@@ -624,14 +628,16 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
             ptx::tc_fence_after();
             if (quarter == 0 && lane == 0) MEC_TRACE_EV2(tl, atom);
           }
-          if (!(p.dbg & 16)) {  // trace builds: 16 = no TMEM stores
-            ptx::tmem_st_32x32b_x16(t_atom + static_cast<uint32_t>(16 * half), val);
-          } else {
+#ifdef MEC_TRACE
+          if (p.dbg & 16) {  // trace builds: 16 = no TMEM stores
             uint32_t acc = 0;
 #pragma unroll
             for (int i = 0; i < 16; ++i) acc ^= val[i];
             if (acc == 0x12345678u) p_sink_dummy(acc);
+            continue;
           }
+#endif
+          ptx::tmem_st_32x32b_x16(t_atom + static_cast<uint32_t>(16 * half), val);
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
@@ -695,7 +701,8 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
         orow_own = static_cast<unsigned char*>(p.O) +
                    (out_row * p.k_c + static_cast<int64_t>(nt) * p.bn) * kOutElt;
       }
-      ptx::mbar_wait(&tfull[acc], acc_phase);
+      if (kGather && p.backoff_ns > 0) ptx::mbar_wait_backoff(&tfull[acc], acc_phase, p.backoff_ns);
+      else ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       if ((warp & 3) == 2 && lane == 0) MEC_TRACE_EV(tl, 5);
       const int64_t h_tile = c.h;
@@ -999,8 +1006,10 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
 #ifdef MEC_TRACE
   if (const char* e = getenv("MEC_DEBUG_FLAGS")) p.dbg = atoi(e);
 #endif
-  p.spin = gather;
+  p.spin = false;
   if (const char* e = getenv("MEC_GATHER_SPIN")) p.spin = gather && atoi(e) != 0;
+  p.backoff_ns = 0;
+  if (const char* e = getenv("MEC_GATHER_BACKOFF")) p.backoff_ns = gather ? static_cast<uint32_t>(atoi(e)) : 0u;
   p.idesc = ptx::instr_desc(tf32, kBM, pl.bn);
   p.kchunk = 32 / pl.elt;
   p.kchunk_log2 = pl.elt == 2 ? 4 : 3;
@@ -1108,6 +1117,10 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
     p.n_acc = 1;
     for (int k = 4; k >= 2; --k)
       if ((k * pl.bn + 31) / 32 * 32 + 4 * 32 <= 512) { p.n_acc = k; break; }
+    if (const char* e = getenv("MEC_GATHER_NACC")) {
+      const int k = atoi(e);
+      if (k >= 1 && (k * pl.bn + 31) / 32 * 32 + 2 * 32 <= 512) p.n_acc = k;
+    }
     p.a_col0 = static_cast<uint32_t>((p.n_acc * pl.bn + 31) / 32 * 32);
     p.tmem_cols = 512;
     stages = static_cast<int>(std::min<uint32_t>(8, (512 - p.a_col0) / 32));
