@@ -215,7 +215,7 @@ GATHER_CASES = [("cv1", 3), ("cv2", 2), ("cv3", 2), ("cv7", 1)]
 @pytest.mark.parametrize("name,batch", GATHER_CASES)
 def test_fused_gather_path(cuda_ok, name, batch, dtype):
     """MEC_PATH_FUSED for small i_c (AlexNet conv1 and co.): input rows staged by
-    bulk copies, A atoms assembled in smem by builder warps, L never written."""
+    bulk copies, A rows assembled in tensor memory by builder warps, L never written."""
     from paper_1706_06873_b200._lib import MEC_PATH_FUSED
     i_h, i_w, i_c, k_h, k_w, k_c, s = synth.TABLE2[name]
     shape = (batch, i_h, i_w, i_c, k_h, k_w, k_c)

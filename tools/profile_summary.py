@@ -46,9 +46,19 @@ def main():
     ap.add_argument("--full")
     ap.add_argument("--config", required=True)
     ap.add_argument("--tag", default="r1")
+    ap.add_argument("--fused", action="store_true",
+                    help="the capture ran MEC_PATH_FUSED: name kernels as bench.py does (weight_prep, "
+                         "fused_window_gemm) and suffix the output files with _fused")
     args = ap.parse_args()
+    if args.fused:
+        global short
+        plain = short
+
+        def short(name):  # noqa: F811
+            k = plain(name)
+            return {"mec_lower": "weight_prep", "window_gemm": "fused_window_gemm"}.get(k, k)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    base = os.path.join(ROOT, "profiles", f"{args.tag}_{args.config}")
+    base = os.path.join(ROOT, "profiles", f"{args.tag}_{args.config}" + ("_fused" if args.fused else ""))
     if args.launches:
         rows = [r for r in csv.reader(open(args.launches)) if r]
         hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
@@ -69,12 +79,13 @@ def main():
         with open(base + "_launches.csv", "w") as f:
             csv.writer(f).writerows(out)
         with open(base + "_launches_summary.txt", "w") as f:
-            tot = sum(sum(v) for k, v in per.items() if k in ("mec_lower", "window_gemm", "sola_copy",
-                                                                 "sola_transpose"))
+            step_kernels = ("mec_lower", "window_gemm", "sola_copy", "sola_transpose", "weight_prep",
+                            "fused_window_gemm")
+            tot = sum(sum(v) for k, v in per.items() if k in step_kernels)
             f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none, {args.config}\n")
             f.write("# cold-cache serialised launches: compare shares, not absolutes\n")
             for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
-                share = (sum(v) / tot) if k in ("mec_lower", "window_gemm", "sola_copy", "sola_transpose") and tot else 0
+                share = (sum(v) / tot) if k in step_kernels and tot else 0
                 f.write(f"{k:16s} launches={len(v):3d} mean_us={sum(v) / len(v) / 1e3:8.2f} share_of_step={share:.2f}\n")
     if args.full:
         raw = subprocess.run(["ncu", "-i", args.full, "--page", "raw", "--csv"], capture_output=True,
