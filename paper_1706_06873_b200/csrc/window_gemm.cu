@@ -557,7 +557,9 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
     const uint32_t r_smem = ptx::smem_u32(smemR);
     const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quarter) << 16) + p.a_col0;
     const int m = 32 * quarter + lane;
-    const int j = m / p.slot;                 // image slot of this row
+    // image slot of this row (rows past ipt slots -- fewer images than the tile
+    // holds -- read slot 0's data and are never stored)
+    const int j = m / p.slot < p.ipt ? m / p.slot : 0;
     const int w_last = static_cast<int>(p.o_w) - 1;
     // global atom sequence number: stage = seq mod S (S a power of two on this
     // path); group g builds the atoms with seq = g mod kBuildGroups (balanced
@@ -684,7 +686,7 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
         const int j = (quarter * 32) / p.slot;
         n_img = c.g * p.ipt + j;
         w0 = c.mt * kBM + quarter * 32 - j * p.slot;
-        nvalid = n_img < p.i_n ? min(static_cast<int64_t>(32), p.o_w - w0) : 0;
+        nvalid = (j < p.ipt && n_img < p.i_n) ? min(static_cast<int64_t>(32), p.o_w - w0) : 0;
         gr0 = n_img * p.o_w + w0;
       }
       // this lane's output row: O[n, h, w] (or O_hnwc[h, n o_w + w]) at column nt*bn
@@ -871,8 +873,8 @@ int tile_ipt(const Plan& pl) {
   const int slot = static_cast<int>((pl.o_w + 31) / 32 * 32);
   return std::max(1, 128 / slot);
 }
-int64_t gather_slot_bytes(const Plan& pl) {
-  return (static_cast<int64_t>(tile_ipt(pl)) * pl.s.k_h * gather_row_pitch(pl) + 127) / 128 * 128;
+int64_t gather_slot_bytes(const Plan& pl, int ipt) {
+  return (static_cast<int64_t>(ipt) * pl.s.k_h * gather_row_pitch(pl) + 127) / 128 * 128;
 }
 constexpr size_t kSmemBudget = 222 * 1024;  // usable dynamic smem after the 1 KB alignment slack
 // epilogue staging boxes (32 rows x 128/64/32 bytes) per epilogue warp: 2 on
@@ -884,17 +886,24 @@ size_t epi_bytes(const Plan& pl, bool gather) {
   while (row_bytes > 32 && (pl.bn * pl.elt) % row_bytes != 0) row_bytes /= 2;
   return static_cast<size_t>(4 * (gather ? 1 : 2)) * epi_bufs(gather) * 32 * row_bytes;
 }
+// gather path: images per tile -- as many as the 128 rows hold, fewer when two
+// staged-row slots would not fit next to the resident weights (large strides:
+// many images of few output pixels, each needing k_h input rows); 0 = none fits
+int gather_ipt(const Plan& pl) {
+  const int64_t n_atoms = pl.kdim_g / pl.bk;
+  const int64_t fixed = static_cast<int64_t>(pl.bn) * kTileKBytes * n_atoms + n_atoms * 32 + 64 +
+                        static_cast<int64_t>(epi_bytes(pl, true));
+  for (int ipt = tile_ipt(pl); ipt >= 1; --ipt)
+    if (fixed + 2 * gather_slot_bytes(pl, ipt) <= static_cast<int64_t>(kSmemBudget)) return ipt;
+  return 0;
+}
 }  // namespace
 
 bool gather_eligible(const Plan& pl) {
   if (fused_eligible(pl)) return false;
-  const int64_t n_atoms = pl.kdim_g / pl.bk;
-  const int64_t b_res = static_cast<int64_t>(pl.bn) * kTileKBytes * n_atoms;
-  const int64_t need = b_res + 2 * gather_slot_bytes(pl) + n_atoms * 32 + 64 +
-                       static_cast<int64_t>(epi_bytes(pl, true));
-  // one N tile (k_c <= 256); weights resident; two staged-row slots; A in TMEM
-  return pl.n_tiles_n == 1 && need <= static_cast<int64_t>(kSmemBudget) &&
-         pl.s.i_w * pl.s.i_c * pl.elt < (1LL << 24) && pl.s.k_h < 256;
+  // one N tile (k_c <= 256); weights resident next to two staged-row slots; A in TMEM
+  return pl.n_tiles_n == 1 && gather_ipt(pl) > 0 && pl.s.i_w * pl.s.i_c * pl.elt < (1LL << 24) &&
+         pl.s.k_h < 256;
 }
 
 cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st,
@@ -906,15 +915,17 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   // 32-row epilogue block then spans several images); otherwise image slots.
   const bool flat = !a.fused && a.batch_folded && pl.o_w < 32;
   int slot = 128, ipt = 1;
+  const bool gather = a.fused && !fused_eligible(pl);
   if (!flat && pl.o_w <= 128) {
     slot = static_cast<int>((pl.o_w + 31) / 32 * 32);
     if (a.batch_folded) ipt = std::max(1, 128 / slot);
+    if (gather) ipt = gather_ipt(pl);  // fewer when the staged rows would not fit
+    if (ipt < 1) return cudaErrorInvalidConfiguration;
     if (ipt == 1) slot = 128;
   }
   const int64_t rows = flat ? pl.s.i_n * pl.o_w : pl.o_w;
   const int64_t groups = flat ? 1 : (pl.s.i_n + ipt - 1) / ipt;
   const int64_t n_mt = flat ? (rows + kBM - 1) / kBM : (ipt > 1 ? 1 : (pl.o_w + kBM - 1) / kBM);
-  const bool gather = a.fused && !fused_eligible(pl);
   if (gather) {
     std::memset(&tmA, 0, sizeof(tmA));  // A atoms are assembled in smem by builder warps
   } else if (a.fused) {
@@ -1064,7 +1075,7 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   const size_t b_res = b_tile * p.n_atoms;
   const size_t epi = epi_bytes(pl, gather);
   const size_t budget = kSmemBudget - epi;
-  if (gather) p.slot_bytes = static_cast<uint32_t>(gather_slot_bytes(pl));
+  if (gather) p.slot_bytes = static_cast<uint32_t>(gather_slot_bytes(pl, ipt));
   if (gather) {
     // as many staged-row slots (2..4) as fit next to the resident weights: the
     // rows of tile t are requested when tile t - n_slots has been built

@@ -365,3 +365,33 @@ def test_error_paths_on_device(cuda_ok):
     assert float(O.abs().max()) == 0.0
     with pytest.raises(MecError):
         mec.conv_forward(I, K, 1, 1, workspace=ws[: ws.numel() // 2])
+
+
+# ------------------------------------------------ NEXT-2: stride sweep on cv1
+
+_STRIDE_REF = {}
+
+
+def _stride_case(s):
+    """cv1 geometry (Table 2: 227x227x3, 11x11, k_c 96) at stride s (Fig. 4(a))."""
+    i_h, i_w, i_c, k_h, k_w, k_c, _ = synth.TABLE2["cv1"]
+    shape = (1, i_h, i_w, i_c, k_h, k_w, k_c)
+    if s not in _STRIDE_REF:
+        I, K = make_inputs(shape, "bf16", seed=7000 + s)
+        _STRIDE_REF[s] = (I, K, oracle.direct_conv(I, K, s, s, n_threads=8))
+    return shape, _STRIDE_REF[s]
+
+
+@pytest.mark.parametrize("path", ["auto", "fused"])
+@pytest.mark.parametrize("s", range(1, 11))
+def test_cv1_stride_sweep(cuda_ok, s, path):
+    """s = 1..10 exercises s >= k/2, strides that do not divide i - k, and input rows
+    no GEMM reads (reading Q5); the AUTO path follows Alg.2 l.8 at every s."""
+    from paper_1706_06873_b200._lib import MEC_PATH_AUTO, MEC_PATH_FUSED
+    shape, (I, K, ref) = _stride_case(s)
+    p = MEC_PATH_FUSED if path == "fused" else MEC_PATH_AUTO
+    O, chosen = mec.conv_forward(to_dev(I, "bf16"), to_dev(K, "bf16"), s, s, path=p, return_path=True)
+    torch.cuda.synchronize()
+    if path == "auto":
+        assert chosen == oracle.select_path(shape, s, s, 100)
+    check_O(O, ref, "bf16", shape[3] * shape[4] * shape[5])
