@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define MEC_ABI_VERSION 1
+#define MEC_ABI_VERSION 2
 
 typedef enum {
   MEC_OK = 0,
@@ -97,7 +97,15 @@ typedef struct {
    * when there is none).  For per-stage timing only. */
   void* stage_events[4];
   int selected_path; /* OUT: the path that ran (1 = A, 2 = B, 3 = fused) */
-  int reserved1[3];
+  /* Zero padding: the convolution runs on I padded with
+   * pad_h zero rows above and below and pad_w zero columns left and right
+   * (P:41 assumes this padding already applied to I).  The padded input is
+   * never materialised: the lowering (or the fused path's TMA zero fill)
+   * produces the lowered rows of the padded image directly.  o from Eq. 1 on
+   * the padded extents; O is i_n x o_h x o_w x k_c of the padded problem.
+   * Not supported by the fused gather variant (MEC_ERR_UNSUPPORTED). */
+  int pad_h, pad_w;
+  int reserved1;
 } mec_options_t;
 
 /* Fills *opt with defaults (AUTO path, T = 100, epilogue fix, pool workspace). */
@@ -134,6 +142,19 @@ size_t mec_workspace_bytes(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t d
 mec_status_t mec_lower(const void* I, void* L, const mec_shape_t* s, int s_h,
                        int s_w, mec_dtype_t dt, void* stream);
 
+/* mec_workspace_bytes for the padded problem of opt->pad_h / opt->pad_w
+ * (opt may be NULL = no padding). */
+size_t mec_workspace_bytes_ex(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt,
+                              const mec_options_t* opt);
+
+/* Compact lowering of the zero-padded input (NEXT-4): s holds the UNPADDED
+ * extents of I; L is the dense lowering of the (i_h + 2 pad_h) x
+ * (i_w + 2 pad_w) padded image, i_n x o_w x (i_h + 2 pad_h) x k_w x i_c,
+ * with zeros wherever the padded image is zero.  pad_h = pad_w = 0 is
+ * mec_lower.  Errors as mec_lower (negative pads: MEC_ERR_INVALID_ARG). */
+mec_status_t mec_lower_padded(const void* I, void* L, const mec_shape_t* s, int s_h, int s_w,
+                              int pad_h, int pad_w, mec_dtype_t dt, void* stream);
+
 /* O = MEC(I, K, s) (Algorithm 2): lowering, then the window GEMMs
  * of the path picked by Alg.2 l.8 with T = 100, then (Solution A) the format
  * fix, all on `stream`.  O receives i_n x o_h x o_w x k_c in n-h-w-c.  L is
@@ -148,6 +169,24 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O,
                                  const mec_shape_t* s, int s_h, int s_w,
                                  mec_dtype_t dt, void* stream,
                                  mec_options_t* opt);
+
+/* Layout of a convolution output consumed by mec_maxpool. */
+typedef enum {
+  MEC_LAYOUT_NHWC = 0, /* i_n x h x w x c (Alg.2 l.27's O) */
+  MEC_LAYOUT_HNWC = 1  /* h x i_n x w x c (Solution A's O before l.13-19, MEC_SOLA_FIX_NONE) */
+} mec_layout_t;
+
+/* Max pooling as the consumer of a convolution output (
+ * a following pooling layer can consume Solution A's h-n-w-c output,
+ * so its transpose is skipped):
+ *   Y[n, y, x, :] = max_{dy < p_h, dx < p_w} X[n, y s_h + dy, x s_w + dx, :]
+ * X has extents (i_n, h, w, c) in x_layout; Y is n-h-w-c, i_n x
+ * ((h - p_h)/s_h + 1) x ((w - p_w)/s_w + 1) x c (floor).  Device pointers,
+ * 16-byte aligned; c elt must be a multiple of 16 bytes (else
+ * MEC_ERR_UNSUPPORTED).  bf16 maxima are exact; fp32 uses fmaxf. */
+mec_status_t mec_maxpool(const void* X, void* Y, int64_t i_n, int64_t h, int64_t w, int64_t c,
+                         int p_h, int p_w, int s_h, int s_w, mec_layout_t x_layout, mec_dtype_t dt,
+                         void* stream);
 
 /* Number of kernel launches the last successful conv / lower call on this
  * thread enqueued (for the bench's gpu_launches count). */

@@ -42,7 +42,11 @@ EXPORTED = (
     "mec_im2col_elems", "mec_workspace_bytes", "mec_lower", "mec_conv_forward",
     "mec_conv_forward_ex", "mec_last_launch_count", "mec_status_string",
     "mec_last_error_message", "mec_abi_version", "mec_synth_fill", "mec_l2_flush",
+    "mec_workspace_bytes_ex", "mec_lower_padded", "mec_maxpool",
 )
+# mec_layout_t
+MEC_LAYOUT_NHWC = 0
+MEC_LAYOUT_HNWC = 1
 
 
 class MecShape(ctypes.Structure):
@@ -59,7 +63,9 @@ class MecOptions(ctypes.Structure):
         ("workspace_bytes", ctypes.c_size_t),
         ("stage_events", ctypes.c_void_p * 4),
         ("selected_path", ctypes.c_int),
-        ("reserved1", ctypes.c_int * 3),
+        ("pad_h", ctypes.c_int),
+        ("pad_w", ctypes.c_int),
+        ("reserved1", ctypes.c_int),
     ]
 
 
@@ -100,6 +106,12 @@ def lib():
         L.mec_workspace_bytes.restype = ctypes.c_size_t
         L.mec_lower.argtypes = [vp, vp, sp, ci, ci, ci, vp]
         L.mec_lower.restype = ci
+        L.mec_lower_padded.argtypes = [vp, vp, sp, ci, ci, ci, ci, ci, vp]
+        L.mec_lower_padded.restype = ci
+        L.mec_workspace_bytes_ex.argtypes = [sp, ci, ci, ci, P(MecOptions)]
+        L.mec_workspace_bytes_ex.restype = ctypes.c_size_t
+        L.mec_maxpool.argtypes = [vp, vp, i64, i64, i64, i64, ci, ci, ci, ci, ci, ci, vp]
+        L.mec_maxpool.restype = ci
         L.mec_conv_forward.argtypes = [vp, vp, vp, sp, ci, ci, ci, vp]
         L.mec_conv_forward.restype = ci
         L.mec_conv_forward_ex.argtypes = [vp, vp, vp, sp, ci, ci, ci, vp, P(MecOptions)]

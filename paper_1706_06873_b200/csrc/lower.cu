@@ -55,6 +55,11 @@ struct LowerParams {
   int64_t kdim, k_c, kdim_pad, kc_pad;
   int n_var, delta_step;
   int64_t kwc_src, kwc_pad;  // gather layout: Kt column a kwc_pad + j <- K_mat row a kwc_src + j (0: identity)
+  // zero padding (NEXT-4): i_h / iwc above are the padded extents; the caller's
+  // I has src_h rows of src_iwc elements; staged rows are padded in smem
+  bool padded;
+  int64_t src_h, pad_h;
+  uint32_t src_iwc, pad_wc;  // pad_wc = pad_w i_c elements
   bool aligned;   // fast path: every strip and segment 16-byte aligned
 };
 
@@ -108,11 +113,55 @@ __global__ void __launch_bounds__(256) lower_kernel(const LowerParams p) {
   const int64_t h0 = (blockIdx.x % p.bands) * static_cast<int64_t>(p.hb);
   const uint32_t rows = static_cast<uint32_t>(min(static_cast<int64_t>(p.hb), p.i_h - h0));
 
+  uint32_t shift_elems = 0;
+  if (p.padded) {
+    // ---- stage rows h0..h0+rows of the zero-padded image: zero the band,
+    // then copy the source rows it covers at column offset pad_w i_c ----
+    const uint32_t nz = (rows * p.iwc * static_cast<uint32_t>(sizeof(T)) + 15) / 16 + 3;
+    for (uint32_t i = threadIdx.x; i < nz; i += blockDim.x)
+      reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    for (uint32_t hh = 0; hh < rows; ++hh) {
+      const int64_t y = h0 + hh - p.pad_h;
+      if (y < 0 || y >= p.src_h) continue;
+      const T* src = reinterpret_cast<const T*>(p.I) + (n * p.src_h + y) * p.src_iwc;
+      T* dst = reinterpret_cast<T*>(smem) + hh * p.iwc + p.pad_wc;
+      const uint32_t row_b = p.src_iwc * static_cast<uint32_t>(sizeof(T));
+      if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (row_b & 15) == 0) {
+        // 128-bit loads; stores at the padded (possibly 2-byte aligned) offset
+        const uint4* s16 = reinterpret_cast<const uint4*>(src);
+        unsigned char* db = reinterpret_cast<unsigned char*>(dst);
+        const bool w4 = (reinterpret_cast<uintptr_t>(db) & 3) == 0;
+        for (uint32_t i = threadIdx.x; i < row_b / 16; i += blockDim.x) {
+          const uint4 v = __ldg(s16 + i);
+          unsigned char* d = db + 16 * i;
+          if (w4) {
+            uint32_t* d4 = reinterpret_cast<uint32_t*>(d);
+            d4[0] = v.x;
+            d4[1] = v.y;
+            d4[2] = v.z;
+            d4[3] = v.w;
+          } else {
+            uint16_t* d2 = reinterpret_cast<uint16_t*>(d);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              d2[2 * k] = static_cast<uint16_t>(w[k] & 0xFFFFu);
+              d2[2 * k + 1] = static_cast<uint16_t>(w[k] >> 16);
+            }
+          }
+        }
+      } else {
+        for (uint32_t e = threadIdx.x; e < p.src_iwc; e += blockDim.x) dst[e] = src[e];
+      }
+    }
+    __syncthreads();
+  } else {
   // ---- stage I[n, h0:h0+rows, :, :] in shared memory (128-bit loads) ----
   const unsigned char* a0 = p.I + ((n * p.i_h + h0) * p.iwc) * sizeof(T);
   const unsigned char* ab = reinterpret_cast<const unsigned char*>(
       reinterpret_cast<uintptr_t>(a0) & ~static_cast<uintptr_t>(15));
-  const uint32_t shift_elems = static_cast<uint32_t>((a0 - ab) / sizeof(T));
+  shift_elems = static_cast<uint32_t>((a0 - ab) / sizeof(T));
   const uint32_t nbytes = static_cast<uint32_t>(a0 - ab) + rows * p.iwc * sizeof(T);
   const uint32_t n16 = (nbytes + 15) / 16;
   for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
@@ -130,6 +179,7 @@ __global__ void __launch_bounds__(256) lower_kernel(const LowerParams p) {
   // zero the slack past the staged bytes so table reads past a row end are defined
   if (threadIdx.x < 3) reinterpret_cast<uint4*>(smem + 16 * n16)[threadIdx.x] = make_uint4(0, 0, 0, 0);
   __syncthreads();
+  }
 
   const T* srow = reinterpret_cast<const T*>(smem) + shift_elems;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -271,7 +321,9 @@ template <typename T>
 __global__ void __launch_bounds__(256) lower_direct_kernel(const T* __restrict__ I, T* __restrict__ L,
                                                            int64_t i_n, int64_t i_h, int64_t i_w,
                                                            int64_t i_c, int64_t k_w, int64_t s_w,
-                                                           int64_t o_w, int64_t pitch) {
+                                                           int64_t o_w, int64_t pitch, int64_t src_h,
+                                                           int64_t src_w, int64_t pad_h, int64_t pad_w) {
+  // i_h / i_w: padded extents; I has src_h x src_w pixels (zero outside)
   const int64_t kwc = k_w * i_c, row = i_h * kwc;
   const int64_t total = i_n * o_w * row;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
@@ -279,7 +331,10 @@ __global__ void __launch_bounds__(256) lower_direct_kernel(const T* __restrict__
     const int64_t nw = e / row, rem = e - nw * row;
     const int64_t n = nw / o_w, w = nw - n * o_w;
     const int64_t h = rem / kwc, r = rem - h * kwc;
-    L[nw * pitch + rem] = I[((n * i_h + h) * i_w + s_w * w) * i_c + r];
+    const int64_t y = h - pad_h, x = s_w * w + r / i_c - pad_w;
+    L[nw * pitch + rem] = (y >= 0 && y < src_h && x >= 0 && x < src_w)
+                              ? I[((n * src_h + y) * src_w + x) * i_c + r % i_c]
+                              : T(0);
   }
 }
 
@@ -290,7 +345,12 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   const mec_shape_t& s = pl.s;
   LowerParams p{};
   p.I = static_cast<const unsigned char*>(I);
-  p.I_end = p.I + static_cast<size_t>(s.i_n * s.i_h * s.i_w * s.i_c) * pl.elt;
+  p.I_end = p.I + static_cast<size_t>(s.i_n * pl.src_h * pl.src_w * s.i_c) * pl.elt;
+  p.padded = pl.pad_h > 0 || pl.pad_w > 0;
+  p.src_h = pl.src_h;
+  p.pad_h = pl.pad_h;
+  p.src_iwc = static_cast<uint32_t>(pl.src_w * s.i_c);
+  p.pad_wc = static_cast<uint32_t>(pl.pad_w * s.i_c);
   p.L = static_cast<unsigned char*>(L);
   p.i_h = s.i_h;
   p.o_w = pl.o_w;
@@ -350,11 +410,11 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
     if (pl.elt == 2)
       lower_direct_kernel<uint16_t><<<static_cast<unsigned>(grid), 256, 0, st>>>(
           static_cast<const uint16_t*>(I), static_cast<uint16_t*>(L), s.i_n, s.i_h, s.i_w, s.i_c,
-          s.k_w, pl.s_w, pl.o_w, pitch);
+          s.k_w, pl.s_w, pl.o_w, pitch, pl.src_h, pl.src_w, pl.pad_h, pl.pad_w);
     else
       lower_direct_kernel<uint32_t><<<static_cast<unsigned>(grid), 256, 0, st>>>(
           static_cast<const uint32_t*>(I), static_cast<uint32_t*>(L), s.i_n, s.i_h, s.i_w, s.i_c,
-          s.k_w, pl.s_w, pl.o_w, pitch);
+          s.k_w, pl.s_w, pl.o_w, pitch, pl.src_h, pl.src_w, pl.pad_h, pl.pad_w);
     if (launches) ++*launches;
     return cudaGetLastError();
   }

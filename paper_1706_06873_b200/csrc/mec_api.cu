@@ -139,14 +139,25 @@ static cudaError_t encode_impl(CUtensorMap* map, bool tf32, int rank, const void
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, Plan* p) {
-  if (!s || !p) return MEC_ERR_INVALID_ARG;
-  if (s->i_n < 1 || s->i_h < 1 || s->i_w < 1 || s->i_c < 1 || s->k_h < 1 || s->k_w < 1 ||
-      s->k_c < 1 || s_h < 1 || s_w < 1 || s->i_h < s->k_h || s->i_w < s->k_w)
+mec_status_t make_plan(const mec_shape_t* s_in, int s_h, int s_w, mec_dtype_t dt, Plan* p, int pad_h,
+                       int pad_w) {
+  if (!s_in || !p) return MEC_ERR_INVALID_ARG;
+  if (pad_h < 0 || pad_w < 0 || pad_h > (1 << 20) || pad_w > (1 << 20)) return MEC_ERR_INVALID_ARG;
+  if (s_in->i_n < 1 || s_in->i_h < 1 || s_in->i_w < 1 || s_in->i_c < 1 || s_in->k_h < 1 ||
+      s_in->k_w < 1 || s_in->k_c < 1 || s_h < 1 || s_w < 1)
     return MEC_ERR_INVALID_ARG;
+  mec_shape_t padded = *s_in;
+  padded.i_h += 2 * static_cast<int64_t>(pad_h);
+  padded.i_w += 2 * static_cast<int64_t>(pad_w);
+  const mec_shape_t* s = &padded;
+  if (s->i_h < s->k_h || s->i_w < s->k_w) return MEC_ERR_INVALID_ARG;
   if (dt != MEC_DTYPE_BF16 && dt != MEC_DTYPE_TF32) return MEC_ERR_INVALID_ARG;
   std::memset(p, 0, sizeof(*p));
   p->s = *s;
+  p->pad_h = pad_h;
+  p->pad_w = pad_w;
+  p->src_h = s_in->i_h;
+  p->src_w = s_in->i_w;
   p->s_h = s_h;
   p->s_w = s_w;
   p->dt = dt;
@@ -183,6 +194,12 @@ mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, P
       p->kdim_pad >= (1LL << 31))
     return MEC_ERR_INVALID_ARG;
   return MEC_OK;
+}
+
+int select_path_plan(const Plan& p, int T) {
+  if (T <= 0) T = MEC_DEFAULT_T;
+  // Alg.2 l.8 (P:161): "if o_w <= T and |O| <= |L|"
+  return (p.o_w <= T && p.n_O <= p.n_L) ? MEC_PATH_SOLUTION_A : MEC_PATH_SOLUTION_B;
 }
 
 }  // namespace mec
@@ -230,9 +247,7 @@ mec_status_t mec_out_dims(const mec_shape_t* s, int s_h, int s_w, int64_t* o_h, 
 mec_path_t mec_select_path(const mec_shape_t* s, int s_h, int s_w, int T) {
   Plan p;
   if (mec::make_plan(s, s_h, s_w, MEC_DTYPE_BF16, &p) != MEC_OK) return MEC_PATH_AUTO;
-  if (T <= 0) T = MEC_DEFAULT_T;
-  // Alg.2 l.8 (P:161): "if o_w <= T and |O| <= |L|"
-  return (p.o_w <= T && p.n_O <= p.n_L) ? MEC_PATH_SOLUTION_A : MEC_PATH_SOLUTION_B;
+  return static_cast<mec_path_t>(mec::select_path_plan(p, T));
 }
 
 int64_t mec_lowered_elems(const mec_shape_t* s, int s_h, int s_w) {
@@ -253,10 +268,23 @@ size_t mec_workspace_bytes(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t d
   return p.ws_bytes;
 }
 
+size_t mec_workspace_bytes_ex(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt,
+                              const mec_options_t* opt) {
+  Plan p;
+  if (mec::make_plan(s, s_h, s_w, dt, &p, opt ? opt->pad_h : 0, opt ? opt->pad_w : 0) != MEC_OK)
+    return 0;
+  return p.ws_bytes;
+}
+
 mec_status_t mec_lower(const void* I, void* L, const mec_shape_t* s, int s_h, int s_w,
                        mec_dtype_t dt, void* stream) {
+  return mec_lower_padded(I, L, s, s_h, s_w, 0, 0, dt, stream);
+}
+
+mec_status_t mec_lower_padded(const void* I, void* L, const mec_shape_t* s, int s_h, int s_w,
+                              int pad_h, int pad_w, mec_dtype_t dt, void* stream) {
   Plan p;
-  mec_status_t st = mec::make_plan(s, s_h, s_w, dt, &p);
+  mec_status_t st = mec::make_plan(s, s_h, s_w, dt, &p, pad_h, pad_w);
   if (st != MEC_OK) return st;
   if (!I || !L) return MEC_ERR_INVALID_ARG;
   if (!mec::aligned16(I) || !mec::aligned16(L)) return MEC_ERR_MISALIGNED;
@@ -277,7 +305,7 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
     opt = &def;
   }
   Plan p;
-  mec_status_t st = mec::make_plan(s, s_h, s_w, dt, &p);
+  mec_status_t st = mec::make_plan(s, s_h, s_w, dt, &p, opt->pad_h, opt->pad_w);
   if (st != MEC_OK) return st;
   if (!I || !K || !O) return MEC_ERR_INVALID_ARG;
   if (!mec::aligned16(I) || !mec::aligned16(K) || !mec::aligned16(O)) return MEC_ERR_MISALIGNED;
@@ -287,7 +315,7 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
   if (opt->rows_per_tile < 0) return MEC_ERR_INVALID_ARG;
   const int T = opt->T > 0 ? opt->T : MEC_DEFAULT_T;
   int path = opt->path;
-  if (path == MEC_PATH_AUTO) path = mec_select_path(s, s_h, s_w, T);
+  if (path == MEC_PATH_AUTO) path = mec::select_path_plan(p, T);
   if (path == MEC_PATH_FUSED && !mec::fused_eligible(p) && !mec::gather_eligible(p))
     return MEC_ERR_UNSUPPORTED;
   // Solution A's literal format fix repurposes L as auxiliary space,
@@ -371,6 +399,25 @@ fail:
 mec_status_t mec_conv_forward(const void* I, const void* K, void* O, const mec_shape_t* s,
                               int s_h, int s_w, mec_dtype_t dt, void* stream) {
   return mec_conv_forward_ex(I, K, O, s, s_h, s_w, dt, stream, nullptr);
+}
+
+mec_status_t mec_maxpool(const void* X, void* Y, int64_t i_n, int64_t h, int64_t w, int64_t c, int p_h,
+                         int p_w, int s_h, int s_w, mec_layout_t x_layout, mec_dtype_t dt, void* stream) {
+  if (!X || !Y) return MEC_ERR_INVALID_ARG;
+  if (i_n < 1 || h < 1 || w < 1 || c < 1 || p_h < 1 || p_w < 1 || s_h < 1 || s_w < 1 || h < p_h ||
+      w < p_w)
+    return MEC_ERR_INVALID_ARG;
+  if (dt != MEC_DTYPE_BF16 && dt != MEC_DTYPE_TF32) return MEC_ERR_INVALID_ARG;
+  if (x_layout != MEC_LAYOUT_NHWC && x_layout != MEC_LAYOUT_HNWC) return MEC_ERR_INVALID_ARG;
+  const int elt = dt == MEC_DTYPE_BF16 ? 2 : 4;
+  if ((c * elt) % 16 != 0) return MEC_ERR_UNSUPPORTED;
+  if (!mec::aligned16(X) || !mec::aligned16(Y)) return MEC_ERR_MISALIGNED;
+  int launches = 0;
+  cudaError_t e = mec::launch_maxpool(X, Y, i_n, h, w, c, p_h, p_w, s_h, s_w, x_layout == MEC_LAYOUT_HNWC,
+                                      elt, static_cast<cudaStream_t>(stream), &launches);
+  if (e != cudaSuccess) return mec::cuda_fail(e, "mec_maxpool");
+  mec::g_launches = launches;
+  return MEC_OK;
 }
 
 }  // extern "C"

@@ -16,7 +16,13 @@ constexpr int kSmemAlign = 1024;   // SWIZZLE_128B atoms need 1024-byte alignmen
 // of Alg.2 l.8, the window geometry of Alg.2 l.9-12 / l.21-25 and the device
 // buffer layout.  Plain host arithmetic.
 struct Plan {
+  // s is the shape of the (virtually) zero-padded input the convolution runs
+  // on: i_h + 2 pad_h, i_w + 2 pad_w (P:41 assumes padding already applied;
+  // NEXT-4 applies it inside the lowering instead).  src_h / src_w are the
+  // extents of the caller's unpadded I.
   mec_shape_t s;
+  int pad_h, pad_w;
+  int64_t src_h, src_w;
   int s_h, s_w;
   mec_dtype_t dt;
   int elt;               // bytes per element (2 bf16, 4 tf32/fp32)
@@ -52,7 +58,11 @@ struct Plan {
 };
 
 // Returns MEC_OK and fills *p, or MEC_ERR_INVALID_ARG.
-mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, Plan* p);
+// pad_h / pad_w >= 0: zero padding applied virtually (never materialised).
+mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, Plan* p, int pad_h = 0,
+                       int pad_w = 0);
+// Alg.2 l.8 on a plan (the padded shape): 1 = Solution A, 2 = Solution B.
+int select_path_plan(const Plan& p, int T);
 
 // ---- kernels (each returns cudaGetLastError() of its launch) ----
 
@@ -84,6 +94,11 @@ struct GemmArgs {
 // TMA box of the NHWC input: needs whole 128-byte channel blocks per pixel and
 // a pixel traversal stride s_w <= 2 (box rows x s_w <= 256).
 bool fused_eligible(const Plan& p);
+// Max pooling of a convolution output X (n-h-w-c, or h-n-w-c when hnwc) into
+// Y (n-h-w-c), window p_h x p_w, strides s_h, s_w; c elt must be a multiple of 16.
+cudaError_t launch_maxpool(const void* X, void* Y, int64_t i_n, int64_t h, int64_t w, int64_t c, int p_h,
+                           int p_w, int s_h, int s_w, bool hnwc, int elt, cudaStream_t st, int* launches);
+
 // Fused path for the other layers (e.g. i_c = 3): input rows staged by bulk
 // copies, A atoms assembled in smem by builder warps.
 bool gather_eligible(const Plan& p);

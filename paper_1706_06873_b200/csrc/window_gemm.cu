@@ -141,6 +141,7 @@ struct GemmParams {
   bool flat;
   bool fused;       // A atoms are TMA boxes of I: atom (a, b, cb) of output row h
   int ncb, k_w, s_h, s_w;
+  int pad_h, pad_w;  // fused TMA variant: zero padding through TMA out-of-bounds fill
   // gather path (fused, small i_c): the producer bulk-copies the tile's k_h
   // input rows per image into a 2-slot ring; builder warps assemble each A
   // atom (window elements j = a kwc + r) from them with a per-atom word table
@@ -380,14 +381,16 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
                 // s_w w + b of input row s_h h + a (pixel traversal stride s_w in the map)
                 const int ab = atom / p.ncb, cb = atom - ab * p.ncb;
                 const int fa = ab / p.k_w, fb = ab - fa * p.k_w;
-                const int32_t zy = static_cast<int32_t>(c.h * p.s_h + fa);
+                // zero padding (NEXT-4): coordinates of the unpadded I, shifted by the
+                // pads; TMA zero-fills the out-of-bounds pixels and rows of a box
+                const int32_t zy = static_cast<int32_t>(c.h * p.s_h + fa - p.pad_h);
                 if (p.ipt <= 1) {
                   ptx::tma_load_4d(dstA, &tmA, &full[stage], cb * p.bk,
-                                   static_cast<int32_t>(c.mt * kBM * p.s_w + fb), zy, z0, hintA);
+                                   static_cast<int32_t>(c.mt * kBM * p.s_w + fb - p.pad_w), zy, z0, hintA);
                 } else {
                   for (int j = 0; j < p.ipt; ++j)
-                    ptx::tma_load_4d(dstA + j * p.slot * kTileKBytes, &tmA, &full[stage], cb * p.bk, fb,
-                                     zy, z0 * p.ipt + j, hintA);
+                    ptx::tma_load_4d(dstA + j * p.slot * kTileKBytes, &tmA, &full[stage], cb * p.bk,
+                                     fb - p.pad_w, zy, z0 * p.ipt + j, hintA);
                 }
               } else if (p.ipt <= 1) {
                 ptx::tma_load_3d(dstA, &tmA, &full[stage], x0 + atom * p.bk, y0, z0, hintA);
@@ -901,8 +904,9 @@ int gather_ipt(const Plan& pl) {
 
 bool gather_eligible(const Plan& pl) {
   if (fused_eligible(pl)) return false;
-  // one N tile (k_c <= 256); weights resident next to two staged-row slots; A in TMEM
-  return pl.n_tiles_n == 1 && gather_ipt(pl) > 0 && pl.s.i_w * pl.s.i_c * pl.elt < (1LL << 24) &&
+  // one N tile (k_c <= 256); weights resident next to two staged-row slots; A in TMEM;
+  // unpadded input (the staged rows are copied verbatim)
+  return pl.n_tiles_n == 1 && gather_ipt(pl) > 0 && pl.pad_h == 0 && pl.pad_w == 0 && pl.s.i_w * pl.s.i_c * pl.elt < (1LL << 24) &&
          pl.s.k_h < 256;
 }
 
@@ -932,11 +936,12 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
     // A: the NHWC input as {i_c, i_w, i_h, i_n}; a box is bk channels x `rows`
     // pixels taken every s_w pixels (elementStrides) -- one K-atom of `rows`
     // windows, read in place: L is never materialised.
-    const uint64_t dims[4] = {static_cast<uint64_t>(pl.s.i_c), static_cast<uint64_t>(pl.s.i_w),
-                              static_cast<uint64_t>(pl.s.i_h), static_cast<uint64_t>(pl.s.i_n)};
+    // (the caller's unpadded I: src_w x src_h pixels)
+    const uint64_t dims[4] = {static_cast<uint64_t>(pl.s.i_c), static_cast<uint64_t>(pl.src_w),
+                              static_cast<uint64_t>(pl.src_h), static_cast<uint64_t>(pl.s.i_n)};
     const uint64_t strides[3] = {static_cast<uint64_t>(pl.s.i_c) * pl.elt,
-                                 static_cast<uint64_t>(pl.s.i_w * pl.s.i_c) * pl.elt,
-                                 static_cast<uint64_t>(pl.s.i_h * pl.s.i_w * pl.s.i_c) * pl.elt};
+                                 static_cast<uint64_t>(pl.src_w * pl.s.i_c) * pl.elt,
+                                 static_cast<uint64_t>(pl.src_h * pl.src_w * pl.s.i_c) * pl.elt};
     const uint32_t rows_box = static_cast<uint32_t>(ipt > 1 ? slot : kBM);
     const uint32_t box[4] = {static_cast<uint32_t>(pl.bk), rows_box * static_cast<uint32_t>(pl.s_w), 1, 1};
     const uint32_t es[4] = {1, static_cast<uint32_t>(pl.s_w), 1, 1};
@@ -997,6 +1002,8 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   p.k_w = static_cast<int>(pl.s.k_w);
   p.s_h = pl.s_h;
   p.s_w = pl.s_w;
+  p.pad_h = pl.pad_h;
+  p.pad_w = pl.pad_w;
 
   p.bn = pl.bn;
   p.n_tiles_n = pl.n_tiles_n;

@@ -71,31 +71,42 @@ def im2col_elems(shape, s_h, s_w) -> int:
     return _lib.lib().mec_im2col_elems(ctypes.byref(_shape(*shape)), s_h, s_w)
 
 
-def workspace_bytes(shape, s_h, s_w, dtype: torch.dtype) -> int:
-    return _lib.lib().mec_workspace_bytes(ctypes.byref(_shape(*shape)), s_h, s_w, dtype_code(dtype))
+def workspace_bytes(shape, s_h, s_w, dtype: torch.dtype, pad_h: int = 0, pad_w: int = 0) -> int:
+    if pad_h == 0 and pad_w == 0:
+        return _lib.lib().mec_workspace_bytes(ctypes.byref(_shape(*shape)), s_h, s_w, dtype_code(dtype))
+    opt = _lib.MecOptions()
+    _lib.lib().mec_options_init(ctypes.byref(opt))
+    opt.pad_h, opt.pad_w = int(pad_h), int(pad_w)
+    return _lib.lib().mec_workspace_bytes_ex(ctypes.byref(_shape(*shape)), s_h, s_w, dtype_code(dtype),
+                                             ctypes.byref(opt))
 
 
-def lower(I: torch.Tensor, k_h: int, k_w: int, s_h: int, s_w: int, out: torch.Tensor | None = None):
-    """mec_lower: L = compact lowering of I (Alg.2 l.3-6), dense (i_n, o_w, i_h, k_w, i_c)."""
+def lower(I: torch.Tensor, k_h: int, k_w: int, s_h: int, s_w: int, out: torch.Tensor | None = None,
+          pad_h: int = 0, pad_w: int = 0):
+    """mec_lower / mec_lower_padded: L = compact lowering of I (Alg.2 l.3-6), dense
+    (i_n, o_w, i_h', k_w, i_c) of the input zero-padded by pad_h / pad_w (i_h' = i_h + 2 pad_h)."""
     _cuda(I, "I")
     i_n, i_h, i_w, i_c = I.shape
-    o_h, o_w = out_dims(i_h, i_w, k_h, k_w, s_h, s_w)
+    hp, wp = i_h + 2 * pad_h, i_w + 2 * pad_w
+    o_h, o_w = out_dims(hp, wp, k_h, k_w, s_h, s_w)
     if out is None:
-        out = torch.empty((i_n, o_w, i_h, k_w, i_c), dtype=I.dtype, device=I.device)
+        out = torch.empty((i_n, o_w, hp, k_w, i_c), dtype=I.dtype, device=I.device)
     _cuda(out, "L")
-    assert out.dtype == I.dtype and out.numel() == i_n * o_w * i_h * k_w * i_c
-    _lib.check(_lib.lib().mec_lower(I.data_ptr(), out.data_ptr(),
-                                    ctypes.byref(_shape(i_n, i_h, i_w, i_c, k_h, k_w, 1)),
-                                    s_h, s_w, dtype_code(I.dtype), _stream(I)), "mec_lower")
+    assert out.dtype == I.dtype and out.numel() == i_n * o_w * hp * k_w * i_c
+    _lib.check(_lib.lib().mec_lower_padded(I.data_ptr(), out.data_ptr(),
+                                           ctypes.byref(_shape(i_n, i_h, i_w, i_c, k_h, k_w, 1)),
+                                           s_h, s_w, int(pad_h), int(pad_w), dtype_code(I.dtype), _stream(I)),
+               "mec_lower_padded")
     return out
 
 
 def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torch.Tensor | None = None,
                  path: int = MEC_PATH_AUTO, T: int = MEC_DEFAULT_T, sola_fix: int = MEC_SOLA_FIX_EPILOGUE,
                  workspace: torch.Tensor | None = None, stage_events=None, return_path: bool = False,
-                 rows_per_tile: int = 0):
+                 rows_per_tile: int = 0, pad_h: int = 0, pad_w: int = 0):
     """mec_conv_forward_ex: O = MEC(I, K, s) (Algorithm 2), O in n-h-w-c
-    (or h-n-w-c with sola_fix=MEC_SOLA_FIX_NONE when Solution A runs)."""
+    (or h-n-w-c with sola_fix=MEC_SOLA_FIX_NONE when Solution A runs).  pad_h / pad_w:
+    zero padding applied virtually inside the lowering (never materialised)."""
     _cuda(I, "I")
     _cuda(K, "K")
     if K.dtype != I.dtype:
@@ -104,7 +115,7 @@ def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torc
     k_h, k_w, k_ci, k_c = K.shape
     if k_ci != i_c:
         raise ValueError("K's third extent must equal i_c (Table 1)")
-    o_h, o_w = out_dims(i_h, i_w, k_h, k_w, s_h, s_w)
+    o_h, o_w = out_dims(i_h + 2 * pad_h, i_w + 2 * pad_w, k_h, k_w, s_h, s_w)
     if out is None:
         out = torch.empty((i_n, o_h, o_w, k_c), dtype=I.dtype, device=I.device)
     _cuda(out, "O")
@@ -113,6 +124,7 @@ def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torc
     _lib.lib().mec_options_init(ctypes.byref(opt))
     opt.path, opt.T, opt.sola_fix = int(path), int(T), int(sola_fix)
     opt.rows_per_tile = int(rows_per_tile)
+    opt.pad_h, opt.pad_w = int(pad_h), int(pad_w)
     if workspace is not None:
         _cuda(workspace, "workspace")
         opt.workspace = workspace.data_ptr()
@@ -125,6 +137,25 @@ def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torc
                                         s_h, s_w, dtype_code(I.dtype), _stream(I), ctypes.byref(opt))
     _lib.check(st, "mec_conv_forward")
     return (out, opt.selected_path) if return_path else out
+
+
+def maxpool(X: torch.Tensor, p_h: int, p_w: int, s_h: int, s_w: int, hnwc: bool = False,
+            out: torch.Tensor | None = None) -> torch.Tensor:
+    """mec_maxpool: max pooling of a conv output X, given as (i_n, h, w, c) n-h-w-c or, with
+    hnwc=True, as Solution A's (h, i_n, w, c) h-n-w-c; returns (i_n, o_h, o_w, c) n-h-w-c."""
+    _cuda(X, "X")
+    if hnwc:
+        h, i_n, w, c = X.shape
+    else:
+        i_n, h, w, c = X.shape
+    o_h, o_w = (h - p_h) // s_h + 1, (w - p_w) // s_w + 1
+    if out is None:
+        out = torch.empty((i_n, o_h, o_w, c), dtype=X.dtype, device=X.device)
+    _cuda(out, "Y")
+    _lib.check(_lib.lib().mec_maxpool(X.data_ptr(), out.data_ptr(), i_n, h, w, c, p_h, p_w, s_h, s_w,
+                                      _lib.MEC_LAYOUT_HNWC if hnwc else _lib.MEC_LAYOUT_NHWC,
+                                      dtype_code(X.dtype), _stream(X)), "mec_maxpool")
+    return out
 
 
 def last_launch_count() -> int:

@@ -395,3 +395,108 @@ def test_cv1_stride_sweep(cuda_ok, s, path):
     if path == "auto":
         assert chosen == oracle.select_path(shape, s, s, 100)
     check_O(O, ref, "bf16", shape[3] * shape[4] * shape[5])
+
+
+# ------------------------------------- NEXT-4: zero padding inside the lowering
+# P:41 assumes I already zero-padded.  The library pads virtually; the reference
+# is the oracle on the explicitly padded array (np.pad: a host-side data step,
+# not oracle arithmetic).
+
+PAD_LOWER_CASES = [
+    # shape, s_h, s_w, pad_h, pad_w
+    ((2, 9, 11, 3, 3, 3, 1), 1, 1, 1, 1),      # i_c = 3, general (word-table) path
+    ((2, 14, 14, 64, 3, 3, 1), 1, 1, 1, 1),    # aligned (128-bit) path
+    ((1, 20, 17, 3, 7, 7, 1), 2, 2, 3, 3),     # ResNet conv1-like, stride 2
+    ((2, 12, 10, 5, 5, 3, 1), 2, 1, 2, 0),     # asymmetric pads
+    ((1, 7, 7, 1, 3, 3, 1), 1, 1, 0, 2),       # width padding only
+]
+
+
+def _pad(a, ph, pw):
+    return np.pad(a, ((0, 0), (ph, ph), (pw, pw), (0, 0)))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("case", range(len(PAD_LOWER_CASES)))
+def test_padded_lowering_bit_exact(cuda_ok, case, dtype):
+    shape, s_h, s_w, ph, pw = PAD_LOWER_CASES[case]
+    i_n, i_h, i_w, i_c, k_h, k_w, _ = shape
+    rng = np.random.default_rng(100 + case)
+    if dtype == "bf16":
+        bits = rng.integers(0, 2**16, (i_n, i_h, i_w, i_c), dtype=np.uint16)
+        Id = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.bfloat16)
+    else:
+        bits = rng.integers(0, 2**32, (i_n, i_h, i_w, i_c), dtype=np.uint32)
+        Id = torch.from_numpy(bits.view(np.int32)).cuda().view(torch.float32)
+    L = mec.lower(Id, k_h, k_w, s_h, s_w, pad_h=ph, pad_w=pw)
+    ref = oracle.lower(_pad(bits, ph, pw), k_h, k_w, s_h, s_w)
+    got = L.cpu().view(torch.int16 if dtype == "bf16" else torch.int32).numpy()
+    np.testing.assert_array_equal(got.view(ref.dtype), ref)
+
+
+PAD_CONV_CASES = [
+    # shape, s, pad_h, pad_w
+    ((2, 14, 14, 64, 3, 3, 64), 1, 1, 1),      # ResNet 3x3 "same"
+    ((2, 32, 32, 3, 7, 7, 64), 2, 3, 3),       # ResNet conv1 geometry (reduced)
+    ((3, 11, 13, 8, 5, 3, 24), 2, 2, 1),       # asymmetric, k_c not a multiple of 16
+    ((2, 9, 9, 128, 3, 3, 32), 2, 1, 1),       # fused TMA variant eligible (i_c elt = 256 B)
+]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("path", ["A", "B", "fused"])
+@pytest.mark.parametrize("case", range(len(PAD_CONV_CASES)))
+def test_padded_conv(cuda_ok, case, path, dtype):
+    from paper_1706_06873_b200._lib import MEC_PATH_FUSED
+    shape, s, ph, pw = PAD_CONV_CASES[case]
+    I, K = make_inputs(shape, dtype, seed=300 + case)
+    ref = oracle.direct_conv(_pad(I, ph, pw), K, s, s, n_threads=8)
+    p = {"A": MEC_PATH_SOLUTION_A, "B": MEC_PATH_SOLUTION_B, "fused": MEC_PATH_FUSED}[path]
+    i_c = shape[3]
+    if path == "fused" and (i_c * (2 if dtype == "bf16" else 4)) % 128 != 0:
+        # the gather variant copies staged rows verbatim: padded problems are refused
+        with pytest.raises(MecError):
+            mec.conv_forward(to_dev(I, dtype), to_dev(K, dtype), s, s, path=p, pad_h=ph, pad_w=pw)
+        return
+    O = mec.conv_forward(to_dev(I, dtype), to_dev(K, dtype), s, s, path=p, pad_h=ph, pad_w=pw)
+    torch.cuda.synchronize()
+    check_O(O, ref, dtype, shape[3] * shape[4] * shape[5])
+
+
+# --------------------- NEXT-4: pooling consumes Solution A's h-n-w-c
+
+def _maxpool_ref(X, p_h, p_w, s_h, s_w):
+    """Definition: Y[n,y,x,c] = max over the p_h x p_w window at (y s_h, x s_w)."""
+    from numpy.lib.stride_tricks import sliding_window_view
+    win = sliding_window_view(X, (p_h, p_w), axis=(1, 2))[:, ::s_h, ::s_w]
+    return win.max(axis=(-2, -1))
+
+
+POOL_CASES = [
+    # conv shape, conv stride, (pool window, pool stride)
+    ((2, 35, 35, 3, 11, 11, 96), 4, (3, 2)),   # AlexNet conv1 -> pool1 geometry (reduced)
+    ((3, 20, 20, 16, 3, 3, 64), 1, (2, 2)),
+    ((2, 16, 19, 8, 3, 3, 32), 1, (3, 3)),
+]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("case", range(len(POOL_CASES)))
+def test_maxpool_consumes_hnwc(cuda_ok, case, dtype):
+    shape, s, (pk, ps) = POOL_CASES[case]
+    i_n, i_h, i_w, i_c, k_h, k_w, k_c = shape
+    I, K = make_inputs(shape, dtype, seed=400 + case)
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    O_nhwc = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_SOLUTION_A, sola_fix=MEC_SOLA_FIX_EPILOGUE)
+    O_raw = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_SOLUTION_A, sola_fix=MEC_SOLA_FIX_NONE)
+    o_h, o_w = O_nhwc.shape[1], O_nhwc.shape[2]
+    O_hnwc = O_raw.view(o_h, i_n, o_w, k_c)  # Alg.2 l.10: O as o_h x i_n o_w k_c
+    assert torch.equal(O_hnwc.permute(1, 0, 2, 3), O_nhwc)
+    Y_h = mec.maxpool(O_hnwc, pk, pk, ps, ps, hnwc=True)
+    Y_n = mec.maxpool(O_nhwc, pk, pk, ps, ps)
+    torch.cuda.synchronize()
+    assert torch.equal(Y_h, Y_n)  # the transpose was never needed
+    np.testing.assert_array_equal(Y_n.float().cpu().numpy(),
+                                  _maxpool_ref(O_nhwc.float().cpu().numpy(), pk, pk, ps, ps))
+    ref = _maxpool_ref(oracle.direct_conv(I, K, s, s, n_threads=8), pk, pk, ps, ps)
+    check_O(Y_n, ref, dtype, i_c * k_h * k_w)

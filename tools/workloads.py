@@ -3,6 +3,7 @@
   python tools/workloads.py resnet101 [--batch 32]   # NEXT-1: Table 3 weighted workload
   python tools/workloads.py stride    [--batch 32]   # NEXT-2: cv1, s = 1..10 (Fig. 4(a))
   python tools/workloads.py paths     [--batch 128]  # NEXT-3: Solution A vs B vs fused per layer
+  python tools/workloads.py next4     [--batch 32]   # NEXT-4: pool consumer of h-n-w-c; virtual padding
 
 Every conv goes through the C ABI (mec_conv_forward_ex) on device-generated
 synthetic inputs; each timed call is preceded by an L2 flush outside its CUDA
@@ -29,7 +30,8 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 from paper_1706_06873_b200 import mec  # noqa: E402
 from paper_1706_06873_b200._lib import (MEC_PATH_AUTO, MEC_PATH_FUSED, MEC_PATH_SOLUTION_A,  # noqa: E402
-                                        MEC_PATH_SOLUTION_B, MecError)
+                                        MEC_PATH_SOLUTION_B, MEC_SOLA_FIX_EPILOGUE, MEC_SOLA_FIX_LITERAL,
+                                        MEC_SOLA_FIX_NONE, MecError)
 
 PATHS = {"auto": MEC_PATH_AUTO, "A": MEC_PATH_SOLUTION_A, "B": MEC_PATH_SOLUTION_B, "fused": MEC_PATH_FUSED}
 NAMES = {MEC_PATH_SOLUTION_A: "A", MEC_PATH_SOLUTION_B: "B", MEC_PATH_FUSED: "fused"}
@@ -164,9 +166,78 @@ def paths(args, tm):
     return {"rows": rows}
 
 
+def timed(tm, fn):
+    """Median device ms of fn() (L2 flushed before each call, outside the events)."""
+    for _ in range(tm.warmup):
+        fn()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(tm.steps)]
+    for a, b in ev:
+        mec.l2_flush(tm.flush)
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    return statistics.median(a.elapsed_time(b) for a, b in ev)
+
+
+def next4(args, tm):
+    rows = []
+    # (1) AlexNet conv1 -> pool1 (3x3, stride 2): Solution A's output consumed by pooling
+    i_h, i_w, i_c, k_h, k_w, k_c, s = synth.TABLE2["cv1"]
+    shape = (args.batch, i_h, i_w, i_c, k_h, k_w, k_c)
+    o_h, o_w = dims(shape, s)
+    I = torch.empty(shape[:4], dtype=torch.bfloat16, device="cuda")
+    K = torch.empty((k_h, k_w, i_c, k_c), dtype=torch.bfloat16, device="cuda")
+    mec.synth_fill(I, 1, synth.TENSOR_I, synth.KIND_GRID8)
+    mec.synth_fill(K, 1, synth.TENSOR_K, synth.KIND_GRID8)
+    O = torch.empty((args.batch, o_h, o_w, k_c), dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(mec.workspace_bytes(shape, s, s, torch.bfloat16), dtype=torch.uint8, device="cuda")
+    variants = {
+        "literal_fix_then_pool": (MEC_SOLA_FIX_LITERAL, False),   # the paper's Alg.2 l.13-19, then pool
+        "epilogue_fix_then_pool": (MEC_SOLA_FIX_EPILOGUE, False), # permutation in the GEMM epilogue
+        "hnwc_pool_no_fix": (MEC_SOLA_FIX_NONE, True),            # P:205: pool consumes h-n-w-c
+    }
+    for name, (fix, hnwc) in variants.items():
+        def step(fix=fix, hnwc=hnwc):
+            mec.conv_forward(I, K, s, s, out=O, path=MEC_PATH_SOLUTION_A, sola_fix=fix, workspace=ws)
+            X = O.view(o_h, args.batch, o_w, k_c) if hnwc else O
+            mec.maxpool(X, 3, 3, 2, 2, hnwc=hnwc)
+        row = {"case": "cv1 + maxpool 3x3/2", "variant": name, "batch": args.batch, "ms": timed(tm, step)}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    del I, K, O, ws
+    # (2) ResNet-50 conv1: 224x224x3, 7x7 stride 2, pad 3, 64 filters -- virtual padding vs a
+    # materialised padded copy of I
+    shape = (args.batch, 224, 224, 3, 7, 7, 64)
+    I = torch.empty(shape[:4], dtype=torch.bfloat16, device="cuda")
+    K = torch.empty((7, 7, 3, 64), dtype=torch.bfloat16, device="cuda")
+    mec.synth_fill(I, 1, synth.TENSOR_I, synth.KIND_GRID8)
+    mec.synth_fill(K, 1, synth.TENSOR_K, synth.KIND_GRID8)
+    o = (224 + 6 - 7) // 2 + 1
+    O = torch.empty((args.batch, o, o, 64), dtype=torch.bfloat16, device="cuda")
+    Ip = torch.zeros((args.batch, 230, 230, 3), dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(mec.workspace_bytes((args.batch, 230, 230, 3, 7, 7, 64), 2, 2, torch.bfloat16),
+                     dtype=torch.uint8, device="cuda")
+
+    def virtual():
+        mec.conv_forward(I, K, 2, 2, out=O, workspace=ws, pad_h=3, pad_w=3)
+
+    def materialised():
+        Ip[:, 3:227, 3:227, :].copy_(I)  # the padded copy the paper assumes (border stays zero)
+        mec.conv_forward(Ip, K, 2, 2, out=O, workspace=ws)
+
+    for name, fn in (("virtual_padding", virtual), ("materialised_padded_copy", materialised)):
+        row = {"case": "ResNet-50 conv1 224x224x3 7x7/2 pad 3", "variant": name, "batch": args.batch,
+               "ms": timed(tm, fn),
+               "extra_bytes": 0 if name == "virtual_padding" else Ip.numel() * 2}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    return {"rows": rows}
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["resnet101", "stride", "paths"])
+    ap.add_argument("mode", choices=["resnet101", "stride", "paths", "next4"])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
@@ -175,7 +246,7 @@ def main():
     if args.batch is None:
         args.batch = 128 if args.mode == "paths" else 32
     tm = Timer(args.steps, args.warmup)
-    res = {"resnet101": resnet101, "stride": stride, "paths": paths}[args.mode](args, tm)
+    res = {"resnet101": resnet101, "stride": stride, "paths": paths, "next4": next4}[args.mode](args, tm)
     res["gpu"] = torch.cuda.get_device_name(0)
     out = args.out or os.path.join(ROOT, "gpurun_out", f"r1_next_{args.mode}.json")
     os.makedirs(os.path.dirname(out), exist_ok=True)
