@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--path", choices=["auto", "A", "B", "fused"], default="auto")
     ap.add_argument("--sola-fix", choices=["epilogue", "literal"], default="epilogue")
     ap.add_argument("--T", type=int, default=100)
+    ap.add_argument("--rows-per-tile", type=int, default=0,
+                    help="window GEMM output rows per tile (multi-row schedule; 0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="(diagnostic) do not flush L2")
@@ -271,13 +273,13 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def step(evs=None):
-        return mec.conv_forward(I, K, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix,
+        return mec.conv_forward(I, K, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, rows_per_tile=args.rows_per_tile,
                                 workspace=workspace, stage_events=evs, return_path=True)
 
     # ---- memory: device-memory delta of one pooled call (library allocates L itself)
     torch.cuda.synchronize()
     free0 = torch.cuda.mem_get_info(dev)[0]
-    mec.conv_forward(I, K, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix)
+    mec.conv_forward(I, K, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, rows_per_tile=args.rows_per_tile)
     torch.cuda.synchronize()
     free1 = torch.cuda.mem_get_info(dev)[0]
     pooled_delta = max(0, free0 - free1)
@@ -290,12 +292,11 @@ def main():
     torch.cuda.synchronize()
     launches_per_step = mec.last_launch_count()
 
-    # ---- timed region: K steps, CUDA events on the launching stream
+    # ---- timed region: K steps, CUDA events on the launching stream around each
+    # step only (events between the step's kernels would serialise the window
+    # GEMM's programmatic dependent launch)
     K_steps = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K_steps)]
-    for e4 in evs:  # torch creates events lazily: create them now; the library re-records them
-        for e in e4:
-            e.record()
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K_steps)]
     sampler = ClockSampler(dev.index)
     dist.barrier()
     torch.cuda.synchronize()
@@ -303,15 +304,30 @@ def main():
         for k in range(K_steps):
             if not args.no_flush:
                 mec.l2_flush(flush)
-            step(evs[k])
+            sev[k][0].record()
+            step()
+            sev[k][1].record()
         torch.cuda.synchronize()
     dist.barrier()
-    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    step_ms = [a.elapsed_time(b) for a, b in sev]
+    tot_ms = dist.max_over_ranks(sum(step_ms), dev)
+    value = w["flops"] * ws * K_steps / (tot_ms * 1e-3) / 1e12
+
+    # ---- per-kernel times (roofline): K more steps with the library's stage
+    # events between the kernels (kernels serialised, so each is timed alone)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K_steps)]
+    for e4 in evs:  # torch creates events lazily: create them now; the library re-records them
+        for e in e4:
+            e.record()
+    torch.cuda.synchronize()
+    for k in range(K_steps):
+        if not args.no_flush:
+            mec.l2_flush(flush)
+        step(evs[k])
+    torch.cuda.synchronize()
     lower_ms = [e[0].elapsed_time(e[1]) for e in evs]
     gemm_ms = [e[1].elapsed_time(e[2]) for e in evs]
     fix_ms = [e[2].elapsed_time(e[3]) for e in evs]
-    tot_ms = dist.max_over_ranks(sum(step_ms), dev)
-    value = w["flops"] * ws * K_steps / (tot_ms * 1e-3) / 1e12
 
     # ---- CUDA-graph replay of the same step (launch gaps removed), diagnostic
     graph_ms = None
@@ -351,7 +367,7 @@ def main():
         for _ in range(2):
             I2.copy_(I_h, non_blocking=True)
             K2.copy_(K_h, non_blocking=True)
-            mec.conv_forward(I2, K2, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, workspace=workspace)
+            mec.conv_forward(I2, K2, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, workspace=workspace, rows_per_tile=args.rows_per_tile)
             O_h.copy_(O, non_blocking=True)
         dist.barrier()
         torch.cuda.synchronize()
@@ -361,7 +377,7 @@ def main():
             a.record()
             I2.copy_(I_h, non_blocking=True)
             K2.copy_(K_h, non_blocking=True)
-            mec.conv_forward(I2, K2, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, workspace=workspace)
+            mec.conv_forward(I2, K2, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, workspace=workspace, rows_per_tile=args.rows_per_tile)
             O_h.copy_(O, non_blocking=True)
             b.record()
         torch.cuda.synchronize()
@@ -445,6 +461,8 @@ def main():
             "pooled_call_device_mem_delta": pooled_delta,
         },
         "stages_ms": {"lower": mean_lower, "gemm": mean_gemm, "format_fix": mean_fix},
+        "stages_timing": "per-kernel CUDA events in a separate run of K steps (kernels serialised); "
+                         "value / ms_per_step time whole steps with no events inside them",
         "graph_ms_per_step": graph_ms,
         "roofline": roof,
         "cpu_baseline": cpu,

@@ -28,8 +28,10 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "mec_internal.h"
+#include "ptx.cuh"
 
 namespace mec {
 namespace {
@@ -97,9 +99,12 @@ __device__ __forceinline__ void prep_weight_tile(const LowerParams& p, int64_t t
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) lower_kernel(const LowerParams p) {
+__global__ void __launch_bounds__(512) lower_kernel(const LowerParams p) {
   constexpr uint32_t VEC = 16 / sizeof(T);
   extern __shared__ __align__(16) unsigned char smem[];
+  // the window GEMM that follows is launched as a programmatic dependent: let
+  // its prologue start now (its loads of L / Kt wait for this grid to finish)
+  ptx::griddep_launch_dependents();
 
   if (blockIdx.x >= p.n_lower_blocks) {
     const int64_t n_tiles = p.n_var * ((p.kdim_pad + 31) / 32) * ((p.kc_pad + 31) / 32);
@@ -251,7 +256,11 @@ __global__ void __launch_bounds__(256) lower_kernel(const LowerParams p) {
     // the number of column blocks)
     const uint32_t nblk = (seg_words + 31) / 32;
     const uint32_t full_words = odd_tail ? seg_words - 1 : seg_words;
-    for (uint32_t jb = warp; jb < nblk; jb += nwarps) {
+    // warps beyond the column blocks split the w loop: warp = jb + nblk * wpart
+    const uint32_t wsplit = nwarps >= nblk ? nwarps / nblk : 1u;
+    const uint32_t wpart = warp / nblk;
+    if (wpart >= wsplit) return;
+    for (uint32_t jb = warp - wpart * nblk; jb < nblk; jb += (wsplit == 1 ? nwarps : nblk * 1000000u)) {
       const uint32_t j = jb * 32 + lane;
       const bool active = j < full_words;
       const uint32_t jj = j < seg_words ? j : seg_words - 1;
@@ -260,43 +269,46 @@ __global__ void __launch_bounds__(256) lower_kernel(const LowerParams p) {
       const uint32_t a1 = e1 & 0x7FFFu, b1 = (e1 >> 15) & 0x7FFFu;
       const uint32_t s0 = ((e0 >> 30) & 1u ? 0x0032u : 0x0010u) | ((e0 >> 31) ? 0x7600u : 0x5400u);
       const uint32_t s1 = ((e1 >> 30) & 1u ? 0x0032u : 0x0010u) | ((e1 >> 31) ? 0x7600u : 0x5400u);
-      uint32_t wbyte = 0;
-      uint32_t* dst = reinterpret_cast<uint32_t*>(L0 + 4 * jj);
+      // this warp's columns w = wpart, wpart + wsplit, ...
+      uint32_t wbyte = wpart * wstep_bytes;
+      uint32_t* dst = reinterpret_cast<uint32_t*>(L0 + 4 * jj + static_cast<size_t>(wpart) * pitch_bytes);
+      const uint32_t dst_step = pitch_bytes * wsplit;
+      const uint32_t wb_step = wstep_bytes * wsplit;
       if (active && (wstep_bytes & 3u) == 0) {
         // word-aligned column step (e.g. AlexNet conv1: 24 B): parity 0 always
-        const uint32_t wstep_words = wstep_bytes >> 2;
-        const uint32_t* xa = W + a0;
-        const uint32_t* xb = W + b0;
+        const uint32_t wstep_words = (wstep_bytes >> 2) * wsplit;
+        const uint32_t* xa = W + a0 + (wbyte >> 2);
+        const uint32_t* xb = W + b0 + (wbyte >> 2);
         const uint32_t n_w = static_cast<uint32_t>(p.o_w);
 #pragma unroll 4
-        for (uint32_t w = 0; w < n_w; ++w) {
+        for (uint32_t w = wpart; w < n_w; w += wsplit) {
           const uint32_t x = *xa;
           uint32_t val = x;
           if constexpr (sizeof(T) == 2) val = __byte_perm(x, *xb, s0);
           *dst = val;
           xa += wstep_words;
           xb += wstep_words;
-          dst = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst) + pitch_bytes);
+          dst = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst) + dst_step);
         }
       } else if (active) {
-        for (uint32_t w = 0; w < static_cast<uint32_t>(p.o_w); ++w) {
+        for (uint32_t w = wpart; w < static_cast<uint32_t>(p.o_w); w += wsplit) {
           const bool par = (wbyte >> 1) & 1u;
           const uint32_t* Wb = W + (wbyte >> 2);
           const uint32_t x = Wb[par ? a1 : a0];
           uint32_t val = x;
           if constexpr (sizeof(T) == 2) val = __byte_perm(x, Wb[par ? b1 : b0], par ? s1 : s0);
           *dst = val;
-          wbyte += wstep_bytes;
-          dst = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst) + pitch_bytes);
+          wbyte += wb_step;
+          dst = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst) + dst_step);
         }
       } else if (odd_tail && j == seg_words - 1) {  // the segment's last 2-byte element
-        for (uint32_t w = 0; w < static_cast<uint32_t>(p.o_w); ++w) {
+        for (uint32_t w = wpart; w < static_cast<uint32_t>(p.o_w); w += wsplit) {
           const bool par = (wbyte >> 1) & 1u;
           const uint32_t x = W[(wbyte >> 2) + (par ? a1 : a0)];
           const uint32_t lo = ((par ? e1 : e0) >> 30) & 1u ? (x >> 16) : (x & 0xFFFFu);
           *reinterpret_cast<uint16_t*>(dst) = static_cast<uint16_t>(lo);
-          wbyte += wstep_bytes;
-          dst = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst) + pitch_bytes);
+          wbyte += wb_step;
+          dst = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst) + dst_step);
         }
       }
     }
@@ -446,8 +458,16 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   // general (word-table) path: one warp per 32-word column block of a segment
   int threads = 256;
   if (!p.aligned) {
+    // one warp per 32-word column block of a segment (up to 8), times wsplit
+    // warp groups that split the w loop (more warps per staged band)
     const int64_t words = (hb * static_cast<int64_t>(p.kwc) * pl.elt + 3) / 4;
-    threads = static_cast<int>(32 * std::min<int64_t>(8, std::max<int64_t>(2, (words + 31) / 32)));
+    const int64_t nblk = (words + 31) / 32;
+    // (measured on B200 for AlexNet conv1: splitting the w loop over more warps
+    // per band is slower -- 18.6 vs 16.5 us -- so 1 unless overridden)
+    int64_t wsplit = 1;
+    if (const char* e = getenv("MEC_LOWER_WSPLIT")) wsplit = std::max(1, atoi(e));
+    if (nblk > 8) threads = 256;
+    else threads = static_cast<int>(32 * std::max<int64_t>(2, std::min<int64_t>(16, nblk * wsplit)));
   }
   const size_t staged = static_cast<size_t>(hb * row_bytes) + 96;
   p.table_off = static_cast<uint32_t>((staged + 15) / 16 * 16);

@@ -102,6 +102,15 @@ __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// ------------------------------------------------ programmatic dependent launch
+// Primary kernel: let the next kernel on the stream start launching now.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// Dependent kernel: wait until the preceding kernel has completed and its
+// memory operations are visible (a no-op when launched without PDL).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch_desc(const void* desc) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");

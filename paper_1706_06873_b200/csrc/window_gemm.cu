@@ -346,7 +346,11 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
     if (lane == 0) {
       const uint64_t hintA = ptx::policy_evict_normal();
       const uint64_t hintB = ptx::policy_evict_last();
-      if (p.resident && t_begin < n_tiles) {
+      // L and the weight operand come from the preceding kernel (launched as its
+      // programmatic dependent): wait for it before the first TMA load.  The
+      // gather path's B is loaded by the MMA warp, so its row staging does not wait.
+      if (!kGather) ptx::griddep_wait();
+      if (!kGather && p.resident && t_begin < n_tiles) {
         ptx::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(p.n_atoms) * b_tile_bytes);
         for (int a = 0; a < p.n_atoms; ++a)
           ptx::tma_load_2d(smemB + static_cast<size_t>(a) * b_tile_bytes, &tmB, bfull, a * p.bk,
@@ -463,6 +467,15 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
     const uint64_t a_desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smemA));
     const uint64_t b_desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smemB));
     const uint32_t b_tile16 = b_tile_bytes >> 4;
+    if (kGather && p.resident && t_begin < n_tiles && lane == 0) {
+      // gather path: the resident weights (prepared by the preceding kernel) are
+      // loaded here, after the grid dependency, while the producer stages rows
+      ptx::griddep_wait();
+      ptx::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(p.n_atoms) * b_tile_bytes);
+      for (int a = 0; a < p.n_atoms; ++a)
+        ptx::tma_load_2d(smemB + static_cast<size_t>(a) * b_tile_bytes, &tmB, bfull, a * p.bk, b_row0,
+                         ptx::policy_evict_last());
+    }
     if (p.resident && t_begin < n_tiles) ptx::mbar_wait(bfull, 0);
     for (int64_t t = t_begin; t < n_tiles; t += t_step) {
       const int tl = static_cast<int>((t - t_begin) / t_step);
@@ -1174,7 +1187,20 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int threads = gather ? kernel_threads<true>() : kernel_threads<false>();
-  kern<<<static_cast<unsigned>(grid), threads, smem, st>>>(tmA, tmB, tmO, p);
+  // programmatic dependent launch: the kernel may start while the preceding
+  // lowering / weight-prep kernel finishes (only the loads of its outputs wait)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = getenv("MEC_NO_PDL") ? 0 : 1;
+  e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmO, p);
+  if (e != cudaSuccess) return e;
   if (launches) ++*launches;
   return cudaGetLastError();
 }
