@@ -503,11 +503,7 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
             // A atom in TMEM columns a_col0 + 32 stage .. + 31: 4 MMAs of K = 32 bytes
             const uint32_t a_tm = tmem_base + p.a_col0 + static_cast<uint32_t>(stage * 32);
             const uint64_t bd = b_desc0 + static_cast<uint32_t>(ks) * b_tile16;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (p.dbg & 2) break;
-              ptx::mma_ts_elect<kTF32>(d_set, a_tm + 8 * k, bd + 2 * k, p.idesc, (ks | k) != 0 ? 1u : 0u);
-            }
+            if (!(p.dbg & 2)) ptx::mma_ts_atom_elect<kTF32>(d_set, a_tm, bd, p.idesc, ks != 0 ? 1u : 0u);
           }
           for (int a = 0; !kGather && a < na; ++a) {
             const uint64_t ad = a_desc0 + a_off + static_cast<uint32_t>(a * (kAtomBytes >> 4));
@@ -644,7 +640,6 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
             if (p.spin) ptx::mbar_spin(&empty[stage], phase ^ 1);  // the MMAs that read this stage are done
             else ptx::mbar_wait(&empty[stage], phase ^ 1);
             ptx::tc_fence_after();
-            if (quarter == 0 && lane == 0) MEC_TRACE_EV2(tl, atom);
           }
 #ifdef MEC_TRACE
           if (p.dbg & 16) {  // trace builds: 16 = no TMEM stores
@@ -661,7 +656,7 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&full[stage]);
-        if (quarter == 0 && lane == 0) MEC_TRACE_EV2(tl, 8 + atom);
+        if (lane == 0 && atom < 4) MEC_TRACE_EV2(tl, quarter * 4 + atom);
       }
       seq += static_cast<uint32_t>(p.n_atoms);
       seq_mod = (seq_mod + static_cast<uint32_t>(p.n_atoms)) % kBuildGroups;

@@ -29,7 +29,7 @@ host = np.zeros(nbytes.value // 8, dtype=np.uint64)
 L.mec_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
 assert L.mec_trace_read(host.ctypes.data, buf, nbytes) == 0
 tr = host.reshape(1024, 64, 16).astype(np.int64)
-ctas = np.where(tr[:, 0, 7] > 0)[0]
+ctas = np.where(tr[:512, 0, 7] > 0)[0]
 t0 = tr[ctas, 0, 7].min()
 names = ["P_start", "P_issued", "M_tempty", "M_full0", "M_commit", "E_tfull", "E_done"]
 print("ctas", len(ctas), "MEC_DEBUG_FLAGS", os.environ.get("MEC_DEBUG_FLAGS"))
@@ -60,13 +60,13 @@ if (sub[:, :, 15] > 0).any():
         med(7, 15), med(15, 0), med(0, 1)))
     print("gather: built(t-2) -> rempty(t) passed %.3f" % np.median(((sub[:, 2:, 7] - sub[:, :-2, 1]))[(sub[:, 2:, 7] > 0) & (sub[:, :-2, 1] > 0)] / 1e3))
 b2 = tr[512 + ctas][:, 1:, :]
-if (b2[:, :, 8] > 0).any():
+if (b2[:, :, 0] > 0).any():
     def med2(bank_a, ia, bank_b, ib):
         A = bank_a[:, :, ia]; B = bank_b[:, :, ib]; m = (A > 0) & (B > 0)
         return np.median((B - A)[m]) / 1e3 if m.any() else float('nan')
-    print("builder per atom (us after M_tempty): empty passed:", " ".join("%.2f" % med2(sub, 2, b2, k) for k in range(7)))
-    print("builder per atom (us after M_tempty): full arrived:", " ".join("%.2f" % med2(sub, 2, b2, 8 + k) for k in range(7)))
-    print("builder build time per atom (empty passed -> arrived):", " ".join("%.2f" % med2(b2, k, b2, 8 + k) for k in range(7)))
+    for q in range(4):
+        print(f"builder quarter {q} full arrived (us after M_tempty), atoms 0-3:",
+              " ".join("%.2f" % med2(sub, 2, b2, q * 4 + k) for k in range(4)))
 if (sub[:, :, 14] > 0).any():
     print("gather MMA full-wait passes (us after tempty), median per atom:",
           " ".join("%.2f" % med(2, 8 + k) for k in range(7)))
