@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="(diagnostic) do not flush L2")
+    ap.add_argument("--no-fused-alt", action="store_true",
+                    help="with --path auto, skip measuring the fused path alongside (north_star (3))")
     return ap.parse_args()
 
 
@@ -236,7 +238,8 @@ def main():
     import synth
     from paper_1706_06873_b200 import dist, mec
     from paper_1706_06873_b200._lib import (MEC_PATH_AUTO, MEC_PATH_FUSED, MEC_PATH_SOLUTION_A,
-                                            MEC_PATH_SOLUTION_B, MEC_SOLA_FIX_EPILOGUE, MEC_SOLA_FIX_LITERAL)
+                                            MEC_PATH_SOLUTION_B, MEC_SOLA_FIX_EPILOGUE, MEC_SOLA_FIX_LITERAL,
+                                            MecError)
 
     rank, ws, dev = dist.init()
     if dev.type != "cuda":
@@ -429,6 +432,58 @@ def main():
             "all_kernels": {k: {"ms": v[0], "bound": v[1], "achieved": v[2], "unit": v[4],
                                 "frac": v[2] / v[3]} for k, v in kernels.items()}}
 
+    # ---- north_star (3): the optional fused path measured against the two-kernel
+    # path, same workload, same timing rules (reported alongside; `value` stays the
+    # paper's path of Alg.2 l.8)
+    fused_alt = None
+    if args.path == "auto" and not args.no_fused_alt:
+        def fstep(evs=None):
+            return mec.conv_forward(I, K, s_h, s_w, out=O, path=MEC_PATH_FUSED, workspace=workspace,
+                                    stage_events=evs, return_path=True)
+        try:
+            for _ in range(max(args.warmup, 0)):
+                if not args.no_flush:
+                    mec.l2_flush(flush)
+                fstep()
+            fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(K_steps)]
+            torch.cuda.synchronize()
+            for a, b in fev:
+                if not args.no_flush:
+                    mec.l2_flush(flush)
+                a.record()
+                fstep()
+                b.record()
+            torch.cuda.synchronize()
+            f_tot = dist.max_over_ranks(sum(a.elapsed_time(b) for a, b in fev), dev)
+            fse = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K_steps)]
+            for e4 in fse:
+                for e in e4:
+                    e.record()
+            torch.cuda.synchronize()
+            for k in range(K_steps):
+                if not args.no_flush:
+                    mec.l2_flush(flush)
+                fstep(fse[k])
+            torch.cuda.synchronize()
+            f_prep = statistics.mean(e[0].elapsed_time(e[1]) for e in fse)
+            f_gemm = statistics.mean(e[1].elapsed_time(e[2]) for e in fse)
+            fb = (w["nI"] + w["nK"] + w["nO"]) * elt
+            if fb / (hbm * 1e9) >= flops / (tc * 1e12):
+                f_roof = {"kernel": "fused_window_gemm", "bound": "hbm", "unit": "GB/s",
+                          "achieved": fb / (f_gemm * 1e-3) / 1e9, "peak": hbm}
+            else:
+                f_roof = {"kernel": "fused_window_gemm", "bound": "tensor", "unit": "TFLOP/s",
+                          "achieved": flops / (f_gemm * 1e-3) / 1e12, "peak": tc}
+            f_roof["frac"] = f_roof["achieved"] / f_roof["peak"]
+            fused_alt = {"path": "fused_lowering_in_gemm",
+                         "value": w["flops"] * ws * K_steps / (f_tot * 1e-3) / 1e12, "unit": "TFLOP/s",
+                         "ms_per_step": f_tot / K_steps,
+                         "stages_ms": {"weight_prep": f_prep, "fused_window_gemm": f_gemm},
+                         "roofline": f_roof, "gpu_launches": mec.last_launch_count() * K_steps}
+        except MecError as e:
+            fused_alt = {"path": "fused_lowering_in_gemm", "unavailable": str(e)}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
@@ -467,6 +522,7 @@ def main():
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "fused_path": fused_alt,
         "gpu_launches": launches_per_step * K_steps,
         "gpu_launches_detail": {"per_step": launches_per_step, "l2_flush_kernels": 0 if args.no_flush else K_steps},
         "clocks": sampler.summary(),
