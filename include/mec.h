@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define MEC_ABI_VERSION 2
+#define MEC_ABI_VERSION 3
 
 typedef enum {
   MEC_OK = 0,
@@ -154,6 +154,17 @@ size_t mec_workspace_bytes_ex(const mec_shape_t* s, int s_h, int s_w, mec_dtype_
  * mec_lower.  Errors as mec_lower (negative pads: MEC_ERR_INVALID_ARG). */
 mec_status_t mec_lower_padded(const void* I, void* L, const mec_shape_t* s, int s_h, int s_w,
                               int pad_h, int pad_w, mec_dtype_t dt, void* stream);
+
+/* Compact lowering into a caller-chosen row pitch (ABI 3): as mec_lower, but
+ * row (n, w) of L (its i_h k_w i_c elements, Alg.2 l.9's L matrix row) starts
+ * at element (n o_w + w) * pitch; the pitch - i_h k_w i_c trailing elements
+ * of a row are unspecified on return (they may be overwritten).  This is the
+ * layout the conv path lowers into (pitch = i_h k_w i_c rounded up to 16
+ * bytes, the TMA stride rule), exposed so it can be checked bit for bit.
+ * pitch < i_h k_w i_c: MEC_ERR_INVALID_ARG; pitch elt not a multiple of 16 B:
+ * MEC_ERR_MISALIGNED. */
+mec_status_t mec_lower_pitched(const void* I, void* L, const mec_shape_t* s, int s_h, int s_w,
+                               int64_t pitch, mec_dtype_t dt, void* stream);
 
 /* O = MEC(I, K, s) (Algorithm 2): lowering, then the window GEMMs
  * of the path picked by Alg.2 l.8 with T = 100, then (Solution A) the format

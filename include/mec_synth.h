@@ -27,9 +27,12 @@ mec_status_t mec_synth_fill(void* dst, int64_t count, uint64_t seed, int tensor_
                             uint64_t index_offset, int kind, mec_dtype_t out_dtype,
                             void* stream);
 
-/* L2 flush helper: overwrites `bytes` of the device scratch buffer `scratch`
- * (>= 2x the L2 size) on `stream`, so the bench can evict L2 between timed
- * iterations.  MEC_ERR_INVALID_ARG for a NULL scratch. */
+/* L2 flush helper, on `stream`: overwrites the first half of the device
+ * scratch buffer `scratch` (`bytes` >= 4x the L2 size), then reads its second
+ * half.  The write evicts everything the previous step left in L2; the read
+ * then evicts the write's own dirty lines (their write-back happens here, not
+ * inside the next timed step), so the timed step starts with an L2 holding
+ * only clean lines of `scratch`.  MEC_ERR_INVALID_ARG for a NULL scratch. */
 mec_status_t mec_l2_flush(void* scratch, size_t bytes, void* stream);
 
 #ifdef __cplusplus

@@ -42,7 +42,7 @@ EXPORTED = (
     "mec_im2col_elems", "mec_workspace_bytes", "mec_lower", "mec_conv_forward",
     "mec_conv_forward_ex", "mec_last_launch_count", "mec_status_string",
     "mec_last_error_message", "mec_abi_version", "mec_synth_fill", "mec_l2_flush",
-    "mec_workspace_bytes_ex", "mec_lower_padded", "mec_maxpool",
+    "mec_workspace_bytes_ex", "mec_lower_padded", "mec_maxpool", "mec_lower_pitched",
 )
 # mec_layout_t
 MEC_LAYOUT_NHWC = 0
@@ -108,6 +108,8 @@ def lib():
         L.mec_lower.restype = ci
         L.mec_lower_padded.argtypes = [vp, vp, sp, ci, ci, ci, ci, ci, vp]
         L.mec_lower_padded.restype = ci
+        L.mec_lower_pitched.argtypes = [vp, vp, sp, ci, ci, i64, ci, vp]
+        L.mec_lower_pitched.restype = ci
         L.mec_workspace_bytes_ex.argtypes = [sp, ci, ci, ci, P(MecOptions)]
         L.mec_workspace_bytes_ex.restype = ctypes.c_size_t
         L.mec_maxpool.argtypes = [vp, vp, i64, i64, i64, i64, ci, ci, ci, ci, ci, ci, vp]

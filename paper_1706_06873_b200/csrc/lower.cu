@@ -28,13 +28,61 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "mec_internal.h"
 #include "ptx.cuh"
 
+#ifdef MEC_TRACE
+// Debug-only per-CTA timestamps of the lowering (separate libmec_trace.so,
+// tools/trace_lower.py): [band][0] staged rows arrived, [1] copies built,
+// [2] band written, [3] SM id
+__device__ unsigned long long* g_lower_trace = nullptr;
+extern "C" int mec_lower_trace_enable(void** dev_buf_out, size_t* bytes_out) {
+  const size_t bytes = static_cast<size_t>(1 << 16) * 4 * 8;
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, bytes) != cudaSuccess) return 1;
+  cudaMemset(buf, 0, bytes);
+  if (cudaMemcpyToSymbol(g_lower_trace, &buf, sizeof(buf)) != cudaSuccess) return 2;
+  *dev_buf_out = buf;
+  *bytes_out = bytes;
+  return 0;
+}
+__device__ __forceinline__ void lower_trace(int ev, long long idx) {
+  unsigned long long* b = g_lower_trace;
+  if (b != nullptr && threadIdx.x == 0 && idx < (1 << 16)) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    b[idx * 4 + ev] = t;
+    if (ev == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      b[idx * 4 + 3] = smid;
+    }
+  }
+}
+#define LOWER_TRACE(ev) lower_trace(ev, b)
+#else
+#define LOWER_TRACE(ev) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace mec {
 namespace {
+
+// host: a failed attribute / occupancy call is reported (MEC_DEBUG_ERRORS=1)
+// and its error cleared, so it is not mistaken for a launch error later
+inline cudaError_t host_ck(cudaError_t e, int line) {
+  if (e != cudaSuccess) {
+    if (getenv("MEC_DEBUG_ERRORS"))
+      fprintf(stderr, "lower.cu:%d: %s\n", line, cudaGetErrorString(e));
+    cudaGetLastError();
+  }
+  return e;
+}
+#define HOST_CK(x) host_ck((x), __LINE__)
 
 struct LowerParams {
   const unsigned char* I;
@@ -63,6 +111,17 @@ struct LowerParams {
   int64_t src_h, pad_h;
   uint32_t src_iwc, pad_wc;  // pad_wc = pad_w i_c elements
   bool aligned;   // fast path: every strip and segment 16-byte aligned
+  // aligned-copies path (strips not 16-byte aligned, segments are; see
+  // lower_copies): ncls staged copies of the band, copy k placed so that
+  // every 16-byte output granule of the output columns of class k is one
+  // aligned 16-byte shared-memory word
+  int ncls;           // 0: path off
+  int gcls_log2;      // log2 of g = gcd(delta16, wstep_b, 16); class value v = k g
+  uint32_t copy_bytes;  // smem bytes per copy region
+  uint32_t delta16;   // (i_w - k_w) i_c elt mod 16
+  int wcls;           // column-class period 16 / gcd(wstep_b, 16)
+  uint32_t raw_bytes;   // smem bytes per raw band buffer (two, double-buffered)
+  int64_t total_bands;  // i_n bands (the persistent CTAs loop over them)
 };
 
 template <typename T>
@@ -98,6 +157,183 @@ __device__ __forceinline__ void prep_weight_tile(const LowerParams& p, int64_t t
   __syncthreads();
 }
 
+// bytes [4 KK + sh_b / 8, + 16) of the 32-byte little-endian string x:y
+template <int KK>
+__device__ __forceinline__ uint4 extract16(uint4 x, uint4 y, uint32_t sh_b) {
+  const uint32_t a[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+  return make_uint4(__funnelshift_r(a[KK], a[KK + 1], sh_b), __funnelshift_r(a[KK + 1], a[KK + 2], sh_b),
+                    __funnelshift_r(a[KK + 2], a[KK + 3], sh_b), __funnelshift_r(a[KK + 3], a[KK + 4], sh_b));
+}
+
+// Build one copy from the raw staged band: smem granule m (dst + 16 m) =
+// raw bytes [r0 + 16 m, + 16), r0 = 16 KK' + sh_b / 8 relative to the
+// 16-aligned raw address src (KK, sh_b uniform over the CTA).
+template <int KK>
+__device__ __forceinline__ void build_copy(uint32_t dst, uint32_t src, uint32_t sh_b, uint32_t n16) {
+  for (uint32_t m = threadIdx.x; m < n16; m += blockDim.x) {
+    const uint4 x = ptx::ld_shared_v4(src + 16 * m);
+    const uint4 y = ptx::ld_shared_v4(src + 16 * m + 16);
+    const uint4 v = extract16<KK>(x, y, sh_b);
+    ptx::st_shared_v4(dst + 16 * m, v.x, v.y, v.z, v.w);
+  }
+}
+
+// Aligned-copies lowering (strips of k_w i_c elements that are not 16-byte
+// aligned, e.g. AlexNet conv1's 66-byte strips, into a segment-aligned L).
+// Output granule q (16 bytes) of segment L[n, w, h0 : h0 + rows] holds bytes
+// of strip hh = 16q / kwc_b (and, if it straddles, of strip hh + 1).  Strip
+// hh of column w starts at band byte  hh iwc_b + w wstep_b  and at segment
+// byte hh kwc_b, so source and destination differ by
+//   v = hh (iwc_b - kwc_b) + w wstep_b  (mod 16), a multiple of g.
+// Copy k = v / g of the band is staged at offset (16 - v) mod 16 inside its
+// 16-aligned region: the granule is then one aligned LDS.128 (two, merged by
+// a byte mask, when it straddles) and one STG.128 -- no per-byte shuffling in
+// the output loop (the word-table path is instruction-bound on that).
+//
+// Persistent CTAs loop over the bands.  Band i + 1 is bulk-copied
+// (cp.async.bulk, one DMA of the contiguous rows) into the other raw buffer
+// while band i is built and written, so the HBM latency of the staging is
+// hidden (a per-thread load loop serialised ~6 latencies per band: measured
+// 5 us of a 15 us kernel for C1).
+// Threads: granule q = tid mod nch, columns w = tid / nch + i wpar, with wpar
+// a multiple of the column-class period 16 / gcd(wstep_b, 16), so a thread's
+// copy never changes along its w loop (constant address increments).
+template <typename T>
+__device__ __forceinline__ void lower_copies(const LowerParams& p, unsigned char* smem, int64_t cta) {
+  const uint32_t iwc_b = p.iwc * sizeof(T), kwc_b = p.kwc * sizeof(T);
+  const uint32_t wstep_b = p.wstep * sizeof(T);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  const uint32_t s_base = ptx::smem_u32(smem);
+  const uint32_t raw0 = s_base + 128 + 32;  // raw buffer b at raw0 + b raw_bytes (32 B slack before)
+  const uint32_t cps = s_base + 128 + 2 * p.raw_bytes;
+  const int64_t nb = p.total_bands;
+  const int64_t b0 = cta, bstep = p.n_lower_blocks;
+#ifdef MEC_TRACE
+  lower_trace(0, 32768 + cta);  // CTA entry (bank 2: per persistent CTA)
+#endif
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bars[0], 1);
+    ptx::mbar_init(&bars[1], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  // band -> (image, first row, rows, global start); issues its raw DMA
+  auto band_src = [&](int64_t b, const unsigned char*& G, uint32_t& rows, int64_t& n, int64_t& h0) {
+    n = b / p.bands;
+    h0 = (b - n * p.bands) * static_cast<int64_t>(p.hb);
+    rows = static_cast<uint32_t>(min(static_cast<int64_t>(p.hb), p.i_h - h0));
+    G = p.I + static_cast<size_t>((n * p.i_h + h0) * p.iwc) * sizeof(T);
+  };
+  auto issue = [&](int64_t b, int buf) {
+    const unsigned char* G;
+    uint32_t rows;
+    int64_t n, h0;
+    band_src(b, G, rows, n, h0);
+    const uintptr_t g = reinterpret_cast<uintptr_t>(G);
+    const unsigned char* al = reinterpret_cast<const unsigned char*>(g & ~uintptr_t(15));
+    const unsigned char* end = G + rows * iwc_b;
+    const unsigned char* bulk_end =
+        reinterpret_cast<const unsigned char*>(reinterpret_cast<uintptr_t>(end < p.I_end ? end + 15 : p.I_end) &
+                                               ~uintptr_t(15));
+    const uint32_t bytes = static_cast<uint32_t>(bulk_end - al);
+    unsigned char* dst = smem + 128 + 32 + static_cast<size_t>(buf) * p.raw_bytes;
+    // the very end of I may fall inside a 16-byte granule: its last bytes by plain loads
+    for (const unsigned char* t = bulk_end; t < end; ++t) dst[t - al] = *t;
+    ptx::mbar_arrive_expect_tx(&bars[buf], bytes);
+    if (bytes > 0) ptx::bulk_load(dst, al, bytes, &bars[buf]);
+  };
+  if (threadIdx.x == 0 && b0 < nb) issue(b0, 0);
+
+  // per-thread granule setup, cached per band height
+  uint32_t set_rows = 0, wpar = 0, x0 = 0, off1 = 0, off2 = 0, m0 = 0, m1 = 0, m2 = 0, m3 = 0, n_it = 0;
+  uint32_t wi = 0;
+  bool idle = true;
+  const uint32_t gsh = static_cast<uint32_t>(p.gcls_log2);
+  int it = 0;
+  for (int64_t b = b0; b < nb; b += bstep, ++it) {
+    const int buf = it & 1;
+    if (threadIdx.x == 0 && b + bstep < nb) issue(b + bstep, buf ^ 1);
+    const unsigned char* G;
+    uint32_t rows;
+    int64_t n, h0;
+    band_src(b, G, rows, n, h0);
+    if (rows != set_rows) {
+      set_rows = rows;
+      const uint32_t nch = (rows * kwc_b + 15) / 16;
+      wpar = blockDim.x / nch;
+      wpar -= wpar % static_cast<uint32_t>(p.wcls);  // >= wcls (host: nch(hb) wcls <= blockDim)
+      const uint32_t q = threadIdx.x % nch;
+      wi = threadIdx.x / nch;
+      idle = wi >= wpar || wi >= static_cast<uint32_t>(p.o_w);
+      x0 = 16 * q;
+      const uint32_t hh = x0 / kwc_b, r0 = x0 - hh * kwc_b;
+      uint32_t cut = kwc_b - r0;  // granule bytes in strip hh
+      if (cut > 16 || hh + 1 >= rows) cut = 16;  // (past the last strip: pitch padding)
+      m0 = cut >= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (32 - 8 * cut));
+      m1 = cut >= 8 ? 0xFFFFFFFFu : (cut <= 4 ? 0u : (0xFFFFFFFFu >> (32 - 8 * (cut - 4))));
+      m2 = cut >= 12 ? 0xFFFFFFFFu : (cut <= 8 ? 0u : (0xFFFFFFFFu >> (32 - 8 * (cut - 8))));
+      m3 = cut >= 16 ? 0xFFFFFFFFu : (cut <= 12 ? 0u : (0xFFFFFFFFu >> (32 - 8 * (cut - 12))));
+      // band byte y of copy k sits at cps + k copy_bytes + 16 + o_k + y
+      const uint32_t y1 = hh * iwc_b + r0 + wi * wstep_b;  // part 1: band byte of granule byte 0
+      const uint32_t v1 = (hh * p.delta16 + wi * wstep_b) & 15u;
+      off1 = (v1 >> gsh) * p.copy_bytes + 16u + ((16u - v1) & 15u) + y1;
+      off2 = off1;  // part 2 (strip hh + 1), = part 1 if unused
+      if (cut < 16) {
+        const uint32_t y2 = y1 + iwc_b - kwc_b;
+        const uint32_t v2 = (v1 + p.delta16) & 15u;
+        off2 = (v2 >> gsh) * p.copy_bytes + 16u + ((16u - v2) & 15u) + y2;
+      }
+      n_it = idle ? 0u : (static_cast<uint32_t>(p.o_w) - wi + wpar - 1) / wpar;
+    }
+    ptx::mbar_wait(&bars[buf], static_cast<uint32_t>(it >> 1) & 1u);
+    LOWER_TRACE(0);
+    // ---- build the copies: copy k granule m = band bytes [16 m - 16 - o_k, + 16) ----
+    const uint32_t band_b = rows * iwc_b;
+    const uint32_t n16 = (band_b + 31) / 16 + 2;
+    const uint32_t g15 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(G) & 15);
+    const uint32_t rawb = raw0 + static_cast<uint32_t>(buf) * p.raw_bytes;  // band byte y at rawb + g15 + y
+    for (int k = 0; k < p.ncls; ++k) {
+      const uint32_t o_k = (16u - (static_cast<uint32_t>(k) << gsh)) & 15u;
+      const uint32_t r = rawb + g15 - 16u - o_k;  // raw address of copy granule 0 (>= raw0 - 32)
+      const uint32_t src = r & ~15u, sh = r & 15u, sh_b = (sh & 3u) * 8u;
+      const uint32_t dst = cps + static_cast<uint32_t>(k) * p.copy_bytes;
+      switch (sh >> 2) {
+        case 0: build_copy<0>(dst, src, sh_b, n16); break;
+        case 1: build_copy<1>(dst, src, sh_b, n16); break;
+        case 2: build_copy<2>(dst, src, sh_b, n16); break;
+        default: build_copy<3>(dst, src, sh_b, n16); break;
+      }
+    }
+    __syncthreads();
+    LOWER_TRACE(1);
+    // ---- output ----
+    uint32_t a1 = cps + off1, a2 = cps + off2;
+    const uint32_t da = wpar * wstep_b;  // a multiple of 16: same copy every iteration
+    const size_t pitch_b = static_cast<size_t>(p.pitch) * sizeof(T);
+    unsigned char* dst = p.L + ((n * p.o_w + wi) * p.pitch + h0 * p.kwc) * sizeof(T) + x0;
+    const size_t dstep = pitch_b * wpar;
+#pragma unroll 4
+    for (uint32_t i = 0; i < n_it; ++i) {
+      const uint4 x = ptx::ld_shared_v4(a1);
+      const uint4 y = ptx::ld_shared_v4(a2);
+      uint4 o;
+      o.x = (x.x & m0) | (y.x & ~m0);
+      o.y = (x.y & m1) | (y.y & ~m1);
+      o.z = (x.z & m2) | (y.z & ~m2);
+      o.w = (x.w & m3) | (y.w & ~m3);
+      *reinterpret_cast<uint4*>(dst) = o;
+      a1 += da;
+      a2 += da;
+      dst += dstep;
+    }
+    __syncthreads();  // the copies and this raw buffer are rewritten next
+    LOWER_TRACE(2);
+  }
+#ifdef MEC_TRACE
+  lower_trace(2, 32768 + cta);  // CTA exit
+#endif
+}
+
 template <typename T>
 __global__ void __launch_bounds__(512) lower_kernel(const LowerParams p) {
   constexpr uint32_t VEC = 16 / sizeof(T);
@@ -106,6 +342,18 @@ __global__ void __launch_bounds__(512) lower_kernel(const LowerParams p) {
   // its prologue start now (its loads of L / Kt wait for this grid to finish)
   ptx::griddep_launch_dependents();
 
+  if (p.ncls > 0) {
+    // persistent lowering CTAs after the weight-prep CTAs, which are thus
+    // scheduled first instead of waiting for a free slot at the end
+    const int64_t n_prep = gridDim.x - p.n_lower_blocks;
+    if (blockIdx.x < n_prep) {
+      const int64_t n_tiles = p.n_var * ((p.kdim_pad + 31) / 32) * ((p.kc_pad + 31) / 32);
+      for (int64_t t = blockIdx.x; t < n_tiles; t += n_prep) prep_weight_tile<T>(p, t);
+      return;
+    }
+    lower_copies<T>(p, smem, static_cast<int64_t>(blockIdx.x) - n_prep);
+    return;
+  }
   if (blockIdx.x >= p.n_lower_blocks) {
     const int64_t n_tiles = p.n_var * ((p.kdim_pad + 31) / 32) * ((p.kc_pad + 31) / 32);
     for (int64_t t = blockIdx.x - p.n_lower_blocks; t < n_tiles;
@@ -352,6 +600,26 @@ __global__ void __launch_bounds__(256) lower_direct_kernel(const T* __restrict__
 
 }  // namespace
 
+// Kernel attributes, set once per process: the largest dynamic shared memory
+// any lowering launch uses (setting it per call to that call's size would
+// LOWER it for the next, larger launch -- a launch failure seen in the tests),
+// and an all-shared carveout (the copies path sizes its grid to the resident
+// CTAs; with the default L1-leaning carveout C1's bands took 2.25 waves).
+constexpr size_t kLowerMaxSmem = 200 * 1024;
+void set_lower_attributes() {
+  static bool done = false;
+  if (done) return;
+  HOST_CK(cudaFuncSetAttribute(lower_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(kLowerMaxSmem)));
+  HOST_CK(cudaFuncSetAttribute(lower_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(kLowerMaxSmem)));
+  HOST_CK(cudaFuncSetAttribute(lower_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared));
+  HOST_CK(cudaFuncSetAttribute(lower_kernel<uint32_t>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared));
+  done = true;
+}
+
 cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, const void* K,
                          void* Kt, cudaStream_t st, int* launches, bool gather_kt) {
   const mec_shape_t& s = pl.s;
@@ -472,20 +740,81 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   const size_t staged = static_cast<size_t>(hb * row_bytes) + 96;
   p.table_off = static_cast<uint32_t>((staged + 15) / 16 * 16);
   const size_t seg_words = (static_cast<size_t>(hb) * p.kwc * pl.elt + 3) / 4;
-  const size_t smem = p.table_off + (p.aligned ? 0 : 2 * seg_words * 4);
+  size_t smem = p.table_off + (p.aligned ? 0 : 2 * seg_words * 4);
+
+  // aligned-copies path (see lower_copies): strips of >= 16 bytes that are not
+  // 16-byte aligned, 16-byte-aligned segments (pitch-padded L), few classes
+  p.ncls = 0;
+  if (!p.aligned && !p.padded && base_ok && !getenv("MEC_LOWER_NO_COPIES")) {
+    const uint32_t kwc_b = p.kwc * pl.elt, iwc_b = p.iwc * pl.elt, ws_b = p.wstep * pl.elt;
+    const uint32_t seg_b = static_cast<uint32_t>(hb) * kwc_b;
+    const bool seg_aligned = (pitch * pl.elt) % 16 == 0 && seg_b % 16 == 0;
+    const uint32_t d16 = (iwc_b - kwc_b) & 15u;
+    uint32_t g = 16;
+    for (uint32_t x : {d16, ws_b & 15u}) {
+      uint32_t a = g, b = x;
+      while (b) { const uint32_t t = a % b; a = b; b = t; }
+      g = a;
+    }
+    const int ncls = static_cast<int>(16 / g);
+    const uint32_t n16 = (static_cast<uint32_t>(hb) * iwc_b + 31) / 16 + 2;
+    const size_t csmem = static_cast<size_t>(ncls) * 16 * n16;
+    const uint32_t nch = (seg_b + 15) / 16;
+    uint32_t gw = 16, bw = ws_b & 15u;
+    while (bw) { const uint32_t t = gw % bw; gw = bw; bw = t; }
+    const uint32_t wcls = 16 / gw;
+    const size_t raw_b = (32 + static_cast<size_t>(hb) * iwc_b + 128 + 15) / 16 * 16;
+    if (kwc_b >= 16 && seg_aligned && ncls <= 4 && 128 + 2 * raw_b + csmem <= kLowerMaxSmem &&
+        nch * wcls <= 512) {
+      p.ncls = ncls;
+      int lg = 0;
+      while ((1u << lg) < g) ++lg;
+      p.gcls_log2 = lg;
+      p.copy_bytes = 16 * n16;
+      p.delta16 = d16;
+      p.wcls = static_cast<int>(wcls);
+      // columns per granule: a multiple of wcls; the block size with the fewest
+      // idle lanes (ties: the larger block)
+      uint32_t best_t = 0;
+      double best_eff = -1.0;
+      // (<= 256 threads: every thread then loops over several columns, which
+      // amortises its per-granule setup -- measured: 480-thread blocks with 4
+      // columns per thread spent most instructions in setup)
+      for (uint32_t wp = wcls; nch * wp <= 256 || wp == wcls; wp += wcls) {
+        const uint32_t t = (nch * wp + 31) / 32 * 32;
+        const double eff = static_cast<double>(nch * wp) / t;
+        if (eff >= best_eff - 1e-9) { best_eff = eff; best_t = t; }
+        if (wp >= static_cast<uint32_t>(pl.o_w)) break;
+      }
+      threads = static_cast<int>(std::max<uint32_t>(best_t, 64));
+      p.raw_bytes = static_cast<uint32_t>(raw_b);
+      smem = 128 + 2 * static_cast<size_t>(p.raw_bytes) + csmem;
+      p.total_bands = p.n_lower_blocks;
+      // persistent CTAs: as many as are co-resident (each loops over bands,
+      // prefetching the next band's rows while it writes the current one)
+      int occ = 0;
+      set_lower_attributes();
+      if (pl.elt == 2)
+        HOST_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lower_kernel<uint16_t>, threads, smem));
+      else
+        HOST_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lower_kernel<uint32_t>, threads, smem));
+      occ = std::max(1, occ);
+      if (const char* e = getenv("MEC_LOWER_CTAS_PER_SM")) occ = std::max(1, std::min(occ, atoi(e)));
+      // equal band counts per CTA (a ragged last round of bands left most CTAs
+      // idle while a quarter of them processed a second band: measured)
+      const int64_t slots = static_cast<int64_t>(occ) * num_sms();
+      const int64_t per = (p.total_bands + slots - 1) / slots;
+      p.n_lower_blocks = (p.total_bands + per - 1) / per;
+    }
+  }
   const int64_t grid = p.n_lower_blocks + prep_blocks;
   if (grid > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
-  if (pl.elt == 2) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(lower_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem));
+  set_lower_attributes();
+  if (smem > kLowerMaxSmem) return cudaErrorInvalidConfiguration;
+  if (pl.elt == 2)
     lower_kernel<uint16_t><<<static_cast<unsigned>(grid), threads, smem, st>>>(p);
-  } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(lower_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem));
+  else
     lower_kernel<uint32_t><<<static_cast<unsigned>(grid), threads, smem, st>>>(p);
-  }
   if (launches) ++*launches;
   return cudaGetLastError();
 }

@@ -296,6 +296,21 @@ mec_status_t mec_lower_padded(const void* I, void* L, const mec_shape_t* s, int 
   return MEC_OK;
 }
 
+mec_status_t mec_lower_pitched(const void* I, void* L, const mec_shape_t* s, int s_h, int s_w,
+                               int64_t pitch, mec_dtype_t dt, void* stream) {
+  Plan p;
+  mec_status_t st = mec::make_plan(s, s_h, s_w, dt, &p, 0, 0);
+  if (st != MEC_OK) return st;
+  if (!I || !L || pitch < p.l_cols) return MEC_ERR_INVALID_ARG;
+  if (!mec::aligned16(I) || !mec::aligned16(L) || (pitch * p.elt) % 16 != 0) return MEC_ERR_MISALIGNED;
+  int launches = 0;
+  cudaError_t e = mec::launch_lower(p, I, L, pitch, nullptr, nullptr, static_cast<cudaStream_t>(stream),
+                                    &launches);
+  if (e != cudaSuccess) return mec::cuda_fail(e, "mec_lower_pitched");
+  mec::g_launches = launches;
+  return MEC_OK;
+}
+
 mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const mec_shape_t* s,
                                  int s_h, int s_w, mec_dtype_t dt, void* stream,
                                  mec_options_t* opt) {
@@ -393,6 +408,9 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
   return MEC_OK;
 fail:
   if (pooled) cudaFreeAsync(ws, stream_);
+  if (getenv("MEC_DEBUG_ERRORS"))
+    fprintf(stderr, "mec_conv_forward: failed after %d launches (path %d): %s\n", launches, path,
+            cudaGetErrorString(e));
   return mec::cuda_fail(e, "mec_conv_forward");
 }
 

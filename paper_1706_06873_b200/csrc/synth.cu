@@ -49,6 +49,19 @@ __global__ void flush_kernel(uint4* dst, int64_t n16, uint32_t salt) {
     dst[i] = make_uint4(salt, static_cast<uint32_t>(i), salt, 0u);
 }
 
+// reads src (evicting dirty lines); the XOR is stored only if it matches a
+// value it never takes in practice, so the loads cannot be dropped
+__global__ void flush_read_kernel(const uint4* src, int64_t n16, uint32_t salt, uint32_t* sink) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  uint32_t acc = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += stride) {
+    const uint4 v = __ldcg(src + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == (salt ^ 0x9E3779B9u) && sink != nullptr) *sink = acc;
+}
+
 }  // namespace
 }  // namespace mec
 
@@ -73,10 +86,14 @@ extern "C" mec_status_t mec_synth_fill(void* dst, int64_t count, uint64_t seed, 
 extern "C" mec_status_t mec_l2_flush(void* scratch, size_t bytes, void* stream) {
   static uint32_t salt = 1;
   if (scratch == nullptr) return MEC_ERR_INVALID_ARG;
-  const int64_t n16 = static_cast<int64_t>(bytes / 16);
-  if (n16 == 0) return MEC_OK;
-  const int64_t grid = std::min<int64_t>((n16 + 255) / 256, 8LL * mec::num_sms());
-  mec::flush_kernel<<<static_cast<unsigned>(grid), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<uint4*>(scratch), n16, salt++);
+  const int64_t half16 = static_cast<int64_t>(bytes / 32);
+  if (half16 == 0) return MEC_OK;
+  const int64_t grid = std::min<int64_t>((half16 + 255) / 256, 8LL * mec::num_sms());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint4* base = static_cast<uint4*>(scratch);
+  mec::flush_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(base, half16, salt);
+  mec::flush_read_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
+      base + half16, half16, salt, reinterpret_cast<uint32_t*>(base));
+  ++salt;
   return cudaGetLastError() == cudaSuccess ? MEC_OK : MEC_ERR_CUDA;
 }

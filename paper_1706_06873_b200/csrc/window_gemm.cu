@@ -177,6 +177,7 @@ struct GemmParams {
   // shift % kchunk == 0, one weight variant, resident weights).  R = 1 is
   // the one-window-per-tile schedule.
   int R;
+  int shift_atoms;  // multi-row: shift / bk (window start advance per output row, in K-atoms)
   int kchunk;       // elements per 32-byte MMA K step (16 bf16 / 8 tf32)
   int kchunk_log2;
   int n_chunks;     // ceil(kdim / kchunk): B chunks holding weights
@@ -487,7 +488,6 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
       if (lane == 0) MEC_TRACE_EV(tl, 2);
       const uint32_t d_set = tmem_base + static_cast<uint32_t>(acc * p.R * p.bn);
       const int n_ks = (c.n_a + kAtomsPerStage - 1) / kAtomsPerStage;
-      uint32_t started = 0;  // multi-row: accumulators that received an MMA
       for (int ks = 0; ks < n_ks; ++ks) {
         const int na = min(kAtomsPerStage, c.n_a - ks * kAtomsPerStage);
         if (kGather && p.spin) ptx::mbar_spin(&full[stage], phase);
@@ -518,25 +518,17 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
                                          (ks | a | k) != 0 ? 1u : 0u);
               }
             } else {
-              // atom covers window positions o .. o + bk of output row h0 + r;
-              // its K chunk k pairs with B chunk (o / kchunk) + k
-              const int col0 = (ks * kAtomsPerStage + a) * p.bk;
+              // multi-row tile (shift a multiple of the K-atom): stream atom
+              // (ks aps + a) is atom  b = stream atom - r shift_atoms  of output
+              // row h0 + r's window -- the same 4 MMAs as R = 1, into
+              // accumulator r against resident weight tile b
+              const int sa = ks * kAtomsPerStage + a;
               for (int r = 0; r < c.r_eff; ++r) {
-                const int o = col0 - r * static_cast<int>(p.shift);
-                if (o + p.bk <= 0 || o >= p.kdim || (p.dbg & 2)) continue;
-                const int c0 = o >> p.kchunk_log2;  // exact: o is a multiple of kchunk
-                const uint32_t d_tmem = d_set + static_cast<uint32_t>(r * p.bn);
-                uint32_t accf = (started >> r) & 1u;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const int ch = c0 + k;
-                  if (ch < 0 || ch >= p.n_chunks) continue;
-                  const uint64_t bd =
-                      b_desc0 + static_cast<uint32_t>((ch >> 2) * static_cast<int>(b_tile16) + (ch & 3) * 2);
-                  ptx::mma_ss_elect<kTF32>(d_tmem, ad + 2 * k, bd, p.idesc, accf);
-                  accf = 1u;
-                }
-                started |= accf << r;
+                const int b = sa - r * p.shift_atoms;
+                if (b < 0 || b >= p.n_atoms || (p.dbg & 2)) continue;
+                ptx::mma_ss_atom_elect<kTF32>(d_set + static_cast<uint32_t>(r * p.bn), ad,
+                                              b_desc0 + static_cast<uint32_t>(b) * b_tile16, p.idesc,
+                                              b != 0 ? 1u : 0u);
               }
             }
           }
@@ -1122,17 +1114,18 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   // tested, but with SS operands the extra B reads make them shared-memory-
   // bound on B200 (slower than R = 1), so auto = 1.
   p.R = 1;
-  if (a.rows_per_tile > 1 && !a.fused && pl.n_var == 1 && p.resident && pl.shift % p.kchunk == 0 &&
+  if (a.rows_per_tile > 1 && !a.fused && pl.n_var == 1 && p.resident && pl.shift % pl.bk == 0 &&
       pl.shift < pl.kdim && pl.o_h > 1) {
     const int r = static_cast<int>(std::min<int64_t>({8, 512 / (2 * pl.bn), pl.o_h}));
     p.R = std::max(1, std::min(r, a.rows_per_tile));
   }
 #ifdef MEC_TRACE
   if (const char* e = getenv("MEC_DEBUG_R")) {
-    if (!a.fused && pl.n_var == 1 && p.resident && pl.shift % p.kchunk == 0 && pl.shift < pl.kdim && pl.o_h > 1)
+    if (!a.fused && pl.n_var == 1 && p.resident && pl.shift % pl.bk == 0 && pl.shift < pl.kdim && pl.o_h > 1)
       p.R = std::max(1, std::min<int>(std::min<int64_t>({8, 512 / (2 * pl.bn), pl.o_h}), atoi(e)));
   }
 #endif
+  p.shift_atoms = static_cast<int>(pl.shift / pl.bk);
   p.n_acc = p.R > 1 ? 2 : (4 * pl.bn <= 512 ? 4 : 2);
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(p.n_acc * p.R * pl.bn)) cols <<= 1;

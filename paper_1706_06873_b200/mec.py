@@ -100,6 +100,26 @@ def lower(I: torch.Tensor, k_h: int, k_w: int, s_h: int, s_w: int, out: torch.Te
     return out
 
 
+def lower_pitched(I: torch.Tensor, k_h: int, k_w: int, s_h: int, s_w: int, pitch: int | None = None):
+    """mec_lower_pitched: the conv path's lowered layout -- i_n o_w rows of L
+    (i_h k_w i_c elements each, Alg.2 l.9) at a row pitch of `pitch` elements
+    (default: rounded up to 16 bytes, as the conv path uses).  Returns the
+    (i_n o_w, pitch) buffer; columns past i_h k_w i_c are unspecified."""
+    _cuda(I, "I")
+    i_n, i_h, i_w, i_c = I.shape
+    o_h, o_w = out_dims(i_h, i_w, k_h, k_w, s_h, s_w)
+    cols = i_h * k_w * i_c
+    if pitch is None:
+        v = 16 // I.element_size()
+        pitch = (cols + v - 1) // v * v
+    out = torch.empty((i_n * o_w, pitch), dtype=I.dtype, device=I.device)
+    _lib.check(_lib.lib().mec_lower_pitched(I.data_ptr(), out.data_ptr(),
+                                            ctypes.byref(_shape(i_n, i_h, i_w, i_c, k_h, k_w, 1)),
+                                            s_h, s_w, int(pitch), dtype_code(I.dtype), _stream(I)),
+               "mec_lower_pitched")
+    return out
+
+
 def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torch.Tensor | None = None,
                  path: int = MEC_PATH_AUTO, T: int = MEC_DEFAULT_T, sola_fix: int = MEC_SOLA_FIX_EPILOGUE,
                  workspace: torch.Tensor | None = None, stage_events=None, return_path: bool = False,

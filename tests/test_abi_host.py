@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(_lib.EXPORTED)
     for s in declared:
         assert hasattr(L, s), s
-    assert L.mec_abi_version() == 2
+    assert L.mec_abi_version() == 3
 
 
 def test_status_strings():
@@ -138,6 +138,10 @@ def test_argument_validation_without_device_work():
     opt.workspace, opt.workspace_bytes = 4096, 16
     assert L.mec_conv_forward_ex(16, 32, 48, ctypes.byref(s), 1, 1, 0, None, ctypes.byref(opt)) == \
         _lib.MEC_ERR_NO_MEMORY
+    # mec_lower_pitched: pitch below one L row, pitch not 16-byte granular, misaligned L
+    assert L.mec_lower_pitched(16, 32, ctypes.byref(s), 1, 1, 20, 0, None) == _lib.MEC_ERR_INVALID_ARG
+    assert L.mec_lower_pitched(16, 32, ctypes.byref(s), 1, 1, 21, 0, None) == _lib.MEC_ERR_MISALIGNED
+    assert L.mec_lower_pitched(16, 40, ctypes.byref(s), 1, 1, 24, 0, None) == _lib.MEC_ERR_MISALIGNED
     # synth helper validation
     assert L.mec_synth_fill(None, 10, 1, 0, 0, 0, 0, None) == _lib.MEC_ERR_INVALID_ARG
     assert L.mec_synth_fill(16, 10, 1, 0, 0, 5, 0, None) == _lib.MEC_ERR_INVALID_ARG

@@ -290,6 +290,50 @@ def test_lowering_bit_exact(cuda_ok, case, dtype):
     np.testing.assert_array_equal(got.view(ref.dtype), ref)
 
 
+PITCHED_CASES = LOWER_CASES + [
+    ((2, 227, 227, 3, 7, 7, 1), 2, 2),     # cv3: 42-byte strips, 4 alignment classes
+    ((2, 224, 224, 3, 3, 3, 1), 1, 1),     # cv7: 18-byte strips, 8 classes (word-table path)
+    ((3, 40, 37, 3, 5, 4, 1), 3, 2),       # odd extents, ragged last band
+    ((1, 19, 23, 5, 4, 3, 1), 2, 1),       # 30-byte strips, i_c = 5
+]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("case", range(len(PITCHED_CASES)))
+def test_lowering_pitched_bit_exact(cuda_ok, case, dtype):
+    """The conv path's pitch-padded L (mec_lower_pitched, the layout the window
+    GEMM reads) holds exactly the oracle's lowering in every row's first
+    i_h k_w i_c elements, for the default 16-byte pitch and a wider one."""
+    shape, s_h, s_w = PITCHED_CASES[case]
+    i_n, i_h, i_w, i_c, k_h, k_w, _ = shape
+    rng = np.random.default_rng(100 + case)
+    if dtype == "bf16":
+        bits = rng.integers(0, 2**16, (i_n, i_h, i_w, i_c), dtype=np.uint16)
+        Id = torch.from_numpy(bits.view(np.int16)).cuda().view(torch.bfloat16)
+    else:
+        bits = rng.integers(0, 2**32, (i_n, i_h, i_w, i_c), dtype=np.uint32)
+        Id = torch.from_numpy(bits.view(np.int32)).cuda().view(torch.float32)
+    ref = oracle.lower(bits, k_h, k_w, s_h, s_w)
+    cols = i_h * k_w * i_c
+    ref = ref.reshape(-1, cols)
+    v = 16 // Id.element_size()
+    for pitch in ((cols + v - 1) // v * v, (cols + v - 1) // v * v + 3 * v):
+        Lp = mec.lower_pitched(Id, k_h, k_w, s_h, s_w, pitch=pitch)
+        got = Lp.cpu().view(torch.int16 if dtype == "bf16" else torch.int32).numpy()[:, :cols]
+        np.testing.assert_array_equal(got.view(ref.dtype), ref)
+
+
+def test_lowering_pitched_full_C1_bit_exact(cuda_ok):
+    c = synth.config("C1")
+    I, _ = make_inputs((c["i_n"], c["i_h"], c["i_w"], c["i_c"], c["k_h"], c["k_w"], c["k_c"]), "bf16", seed=2)
+    Id = to_dev(I, "bf16")
+    Lp = mec.lower_pitched(Id, c["k_h"], c["k_w"], c["s_h"], c["s_w"])
+    bits = Id.view(torch.int16).cpu().numpy()
+    ref = oracle.lower(bits, c["k_h"], c["k_w"], c["s_h"], c["s_w"])
+    cols = c["i_h"] * c["k_w"] * c["i_c"]
+    np.testing.assert_array_equal(Lp.view(torch.int16).cpu().numpy()[:, :cols], ref.reshape(-1, cols))
+
+
 def test_lowering_full_C1_batch_bit_exact(cuda_ok):
     c = synth.config("C1")
     I, _ = make_inputs((c["i_n"], c["i_h"], c["i_w"], c["i_c"], c["k_h"], c["k_w"], c["k_c"]), "bf16", seed=1)

@@ -12,7 +12,7 @@ K = torch.empty((cfg["k_h"], cfg["k_w"], cfg["i_c"], cfg["k_c"]), dtype=tdt, dev
 mec.synth_fill(I, 1, 0, 0); mec.synth_fill(K, 1, 1, 0)
 s = (cfg["i_n"], cfg["i_h"], cfg["i_w"], cfg["i_c"], cfg["k_h"], cfg["k_w"], cfg["k_c"])
 ws = torch.empty(mec.workspace_bytes(s, cfg["s_h"], cfg["s_w"], tdt), dtype=torch.uint8, device="cuda")
-flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 O = mec.conv_forward(I, K, cfg["s_h"], cfg["s_w"], workspace=ws)
 def t(fn, flush_first):
     res = []

@@ -53,7 +53,7 @@ def flops(shape, s):
 class Timer:
     def __init__(self, steps, warmup):
         self.steps, self.warmup = steps, warmup
-        self.flush = torch.empty(2 * 126 * 2 ** 20, dtype=torch.uint8, device="cuda")
+        self.flush = torch.empty(4 * 126 * 2 ** 20, dtype=torch.uint8, device="cuda")
 
     def conv(self, shape, s, dtype, path):
         """Median device ms of one mec_conv_forward_ex call, and the path that ran."""
