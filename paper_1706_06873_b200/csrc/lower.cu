@@ -93,6 +93,7 @@ struct LowerParams {
   int64_t o_w;
   uint32_t iwc;   // i_w i_c   (one input row, elements)
   uint32_t kwc;   // k_w i_c   (one strip, elements)
+  uint32_t kwcs;  // strip stride in L (elements): kwc, or kwc padded with zeros (conv path, strip padding)
   uint32_t wstep; // s_w i_c   (strip start advance per output column)
   uint32_t kwc_magic;  // floor(2^32 / kwc) + 1: e / kwc == umulhi(e, magic) for e < 2^20
   int hb;         // input rows per CTA
@@ -201,6 +202,7 @@ __device__ __forceinline__ void build_copy(uint32_t dst, uint32_t src, uint32_t 
 template <typename T>
 __device__ __forceinline__ void lower_copies(const LowerParams& p, unsigned char* smem, int64_t cta) {
   const uint32_t iwc_b = p.iwc * sizeof(T), kwc_b = p.kwc * sizeof(T);
+  const uint32_t kwcs_b = p.kwcs * sizeof(T);  // strip stride in L (>= kwc_b; zero padded)
   const uint32_t wstep_b = p.wstep * sizeof(T);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   const uint32_t s_base = ptx::smem_u32(smem);
@@ -246,6 +248,7 @@ __device__ __forceinline__ void lower_copies(const LowerParams& p, unsigned char
 
   // per-thread granule setup, cached per band height
   uint32_t set_rows = 0, wpar = 0, x0 = 0, off1 = 0, off2 = 0, m0 = 0, m1 = 0, m2 = 0, m3 = 0, n_it = 0;
+  uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0;
   uint32_t wi = 0;
   bool idle = true;
   const uint32_t gsh = static_cast<uint32_t>(p.gcls_log2);
@@ -259,27 +262,40 @@ __device__ __forceinline__ void lower_copies(const LowerParams& p, unsigned char
     band_src(b, G, rows, n, h0);
     if (rows != set_rows) {
       set_rows = rows;
-      const uint32_t nch = (rows * kwc_b + 15) / 16;
+      const uint32_t nch = (rows * kwcs_b + 15) / 16;
       wpar = blockDim.x / nch;
       wpar -= wpar % static_cast<uint32_t>(p.wcls);  // >= wcls (host: nch(hb) wcls <= blockDim)
       const uint32_t q = threadIdx.x % nch;
       wi = threadIdx.x / nch;
       idle = wi >= wpar || wi >= static_cast<uint32_t>(p.o_w);
       x0 = 16 * q;
-      const uint32_t hh = x0 / kwc_b, r0 = x0 - hh * kwc_b;
-      uint32_t cut = kwc_b - r0;  // granule bytes in strip hh
-      if (cut > 16 || hh + 1 >= rows) cut = 16;  // (past the last strip: pitch padding)
-      m0 = cut >= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (32 - 8 * cut));
-      m1 = cut >= 8 ? 0xFFFFFFFFu : (cut <= 4 ? 0u : (0xFFFFFFFFu >> (32 - 8 * (cut - 4))));
-      m2 = cut >= 12 ? 0xFFFFFFFFu : (cut <= 8 ? 0u : (0xFFFFFFFFu >> (32 - 8 * (cut - 8))));
-      m3 = cut >= 16 ? 0xFFFFFFFFu : (cut <= 12 ? 0u : (0xFFFFFFFFu >> (32 - 8 * (cut - 12))));
+      const uint32_t hh = x0 / kwcs_b, r0 = x0 - hh * kwcs_b;
+      // granule byte j: strip hh data for j < cut1, zero padding for
+      // cut1 <= j < cut2, strip hh + 1 data for j >= cut2 (kwcs_b >= 16: no
+      // granule reaches strip hh + 2)
+      const uint32_t cut1 = r0 >= kwc_b ? 0u : min(16u, kwc_b - r0);
+      const uint32_t cut2 = hh + 1 >= rows ? 16u : min(16u, kwcs_b - r0);
+      auto range_mask = [](uint32_t lo, uint32_t hi, uint32_t b0) -> uint32_t {  // bytes [lo, hi) of word b0..b0+3
+        uint32_t m = 0;
+        for (uint32_t b = 0; b < 4; ++b)
+          if (b0 + b >= lo && b0 + b < hi) m |= 0xFFu << (8 * b);
+        return m;
+      };
+      m0 = range_mask(0, cut1, 0);
+      m1 = range_mask(0, cut1, 4);
+      m2 = range_mask(0, cut1, 8);
+      m3 = range_mask(0, cut1, 12);
+      n0 = range_mask(cut2, 16, 0);
+      n1 = range_mask(cut2, 16, 4);
+      n2 = range_mask(cut2, 16, 8);
+      n3 = range_mask(cut2, 16, 12);
       // band byte y of copy k sits at cps + k copy_bytes + 16 + o_k + y
       const uint32_t y1 = hh * iwc_b + r0 + wi * wstep_b;  // part 1: band byte of granule byte 0
       const uint32_t v1 = (hh * p.delta16 + wi * wstep_b) & 15u;
       off1 = (v1 >> gsh) * p.copy_bytes + 16u + ((16u - v1) & 15u) + y1;
       off2 = off1;  // part 2 (strip hh + 1), = part 1 if unused
-      if (cut < 16) {
-        const uint32_t y2 = y1 + iwc_b - kwc_b;
+      if (cut2 < 16) {
+        const uint32_t y2 = y1 + iwc_b - kwcs_b;
         const uint32_t v2 = (v1 + p.delta16) & 15u;
         off2 = (v2 >> gsh) * p.copy_bytes + 16u + ((16u - v2) & 15u) + y2;
       }
@@ -310,17 +326,17 @@ __device__ __forceinline__ void lower_copies(const LowerParams& p, unsigned char
     uint32_t a1 = cps + off1, a2 = cps + off2;
     const uint32_t da = wpar * wstep_b;  // a multiple of 16: same copy every iteration
     const size_t pitch_b = static_cast<size_t>(p.pitch) * sizeof(T);
-    unsigned char* dst = p.L + ((n * p.o_w + wi) * p.pitch + h0 * p.kwc) * sizeof(T) + x0;
+    unsigned char* dst = p.L + ((n * p.o_w + wi) * p.pitch + h0 * p.kwcs) * sizeof(T) + x0;
     const size_t dstep = pitch_b * wpar;
 #pragma unroll 4
     for (uint32_t i = 0; i < n_it; ++i) {
       const uint4 x = ptx::ld_shared_v4(a1);
       const uint4 y = ptx::ld_shared_v4(a2);
       uint4 o;
-      o.x = (x.x & m0) | (y.x & ~m0);
-      o.y = (x.y & m1) | (y.y & ~m1);
-      o.z = (x.z & m2) | (y.z & ~m2);
-      o.w = (x.w & m3) | (y.w & ~m3);
+      o.x = (x.x & m0) | (y.x & n0);
+      o.y = (x.y & m1) | (y.y & n1);
+      o.z = (x.z & m2) | (y.z & n2);
+      o.w = (x.w & m3) | (y.w & n3);
       *reinterpret_cast<uint4*>(dst) = o;
       a1 += da;
       a2 += da;
@@ -582,17 +598,19 @@ __global__ void __launch_bounds__(256) lower_direct_kernel(const T* __restrict__
                                                            int64_t i_n, int64_t i_h, int64_t i_w,
                                                            int64_t i_c, int64_t k_w, int64_t s_w,
                                                            int64_t o_w, int64_t pitch, int64_t src_h,
-                                                           int64_t src_w, int64_t pad_h, int64_t pad_w) {
-  // i_h / i_w: padded extents; I has src_h x src_w pixels (zero outside)
-  const int64_t kwc = k_w * i_c, row = i_h * kwc;
+                                                           int64_t src_w, int64_t pad_h, int64_t pad_w,
+                                                           int64_t kwcs) {
+  // i_h / i_w: padded extents; I has src_h x src_w pixels (zero outside);
+  // strips of k_w i_c elements at a stride of kwcs (>= k_w i_c, zero filled)
+  const int64_t kwc = k_w * i_c, row = i_h * kwcs;
   const int64_t total = i_n * o_w * row;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t nw = e / row, rem = e - nw * row;
     const int64_t n = nw / o_w, w = nw - n * o_w;
-    const int64_t h = rem / kwc, r = rem - h * kwc;
+    const int64_t h = rem / kwcs, r = rem - h * kwcs;
     const int64_t y = h - pad_h, x = s_w * w + r / i_c - pad_w;
-    L[nw * pitch + rem] = (y >= 0 && y < src_h && x >= 0 && x < src_w)
+    L[nw * pitch + rem] = (r < kwc && y >= 0 && y < src_h && x >= 0 && x < src_w)
                               ? I[((n * src_h + y) * src_w + x) * i_c + r % i_c]
                               : T(0);
   }
@@ -637,6 +655,8 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   p.pitch = pitch;
   p.iwc = static_cast<uint32_t>(s.i_w * s.i_c);
   p.kwc = static_cast<uint32_t>(s.k_w * s.i_c);
+  p.kwcs = static_cast<uint32_t>(pl.strip);
+  const bool spad = p.kwcs != p.kwc;  // strip-padded conv-path L (Plan::kwc_s)
   p.wstep = static_cast<uint32_t>(pl.s_w * s.i_c);
   p.kwc_magic = p.kwc > 1 ? static_cast<uint32_t>((1ull << 32) / p.kwc + 1) : 0u;  // 0: kwc == 1
   p.K = static_cast<const unsigned char*>(K);
@@ -652,6 +672,12 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
     p.kdim_pad = pl.kdim_g;
     p.kwc_src = s.k_w * s.i_c;
     p.kwc_pad = pl.kwc_p;
+  } else if (spad) {
+    // strip-padded L: Kt column a kwc_s + j <- K_mat row a k_w i_c + j (same
+    // layout as the gather path's operand), zero in the pad columns
+    p.kdim = pl.kdim_src;
+    p.kwc_src = s.k_w * s.i_c;
+    p.kwc_pad = pl.kwc_s;
   }
 
   int64_t prep_blocks = 0;
@@ -673,8 +699,10 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
 
   const int64_t row_bytes = static_cast<int64_t>(p.iwc) * pl.elt;
   const int64_t max_smem = 96 * 1024;
-  const bool use_smem = row_bytes + 64 <= max_smem && s.k_w * s.i_c < (1 << 20) && p.iwc < (1u << 24);
-  if (!use_smem) {
+  bool use_smem = row_bytes + 64 <= max_smem && s.k_w * s.i_c < (1 << 20) && p.iwc < (1u << 24);
+  // (the strip-padded layout is written by the aligned-copies path only, else
+  // by the direct kernel: see below, after the band height is known)
+  auto launch_direct = [&]() -> cudaError_t {
     // weight prep still needs the main kernel's prep blocks: run them with a 1-band grid
     if (Kt != nullptr) {
       LowerParams q = p;
@@ -690,21 +718,22 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
     if (pl.elt == 2)
       lower_direct_kernel<uint16_t><<<static_cast<unsigned>(grid), 256, 0, st>>>(
           static_cast<const uint16_t*>(I), static_cast<uint16_t*>(L), s.i_n, s.i_h, s.i_w, s.i_c,
-          s.k_w, pl.s_w, pl.o_w, pitch, pl.src_h, pl.src_w, pl.pad_h, pl.pad_w);
+          s.k_w, pl.s_w, pl.o_w, pitch, pl.src_h, pl.src_w, pl.pad_h, pl.pad_w, p.kwcs);
     else
       lower_direct_kernel<uint32_t><<<static_cast<unsigned>(grid), 256, 0, st>>>(
           static_cast<const uint32_t*>(I), static_cast<uint32_t*>(L), s.i_n, s.i_h, s.i_w, s.i_c,
-          s.k_w, pl.s_w, pl.o_w, pitch, pl.src_h, pl.src_w, pl.pad_h, pl.pad_w);
+          s.k_w, pl.s_w, pl.o_w, pitch, pl.src_h, pl.src_w, pl.pad_h, pl.pad_w, p.kwcs);
     if (launches) ++*launches;
     return cudaGetLastError();
-  }
+  };
+  if (!use_smem) return launch_direct();
 
   // Rows per CTA: stage <= ~24 KB of input (several CTAs per SM), enough CTAs
   // for >= ~4 per SM, and HB a multiple of the alignment period so segments of
   // a 16-byte-pitched L start 16-byte aligned.
   const int vec = 16 / pl.elt;
   int64_t period = 1;
-  while ((period * p.kwc) % vec != 0) ++period;  // <= vec
+  while ((period * p.kwcs) % vec != 0) ++period;  // <= vec
   const int64_t max_rows_smem = std::max<int64_t>(1, (24 * 1024) / row_bytes);
   const int64_t want_blocks = 4LL * num_sms();
   int64_t hb = std::min<int64_t>(s.i_h, max_rows_smem);
@@ -720,7 +749,7 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
 
   const bool base_ok = (reinterpret_cast<uintptr_t>(I) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(L) % 16 == 0);
-  p.aligned = base_ok && (p.kwc % vec == 0) && (p.wstep % vec == 0) && (p.iwc % vec == 0) &&
+  p.aligned = !spad && base_ok && (p.kwc % vec == 0) && (p.wstep % vec == 0) && (p.iwc % vec == 0) &&
               (pitch % vec == 0);
 
   // general (word-table) path: one warp per 32-word column block of a segment
@@ -746,7 +775,7 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   // 16-byte aligned, 16-byte-aligned segments (pitch-padded L), few classes
   p.ncls = 0;
   if (!p.aligned && !p.padded && base_ok && !getenv("MEC_LOWER_NO_COPIES")) {
-    const uint32_t kwc_b = p.kwc * pl.elt, iwc_b = p.iwc * pl.elt, ws_b = p.wstep * pl.elt;
+    const uint32_t kwc_b = p.kwcs * pl.elt, iwc_b = p.iwc * pl.elt, ws_b = p.wstep * pl.elt;  // (strip stride)
     const uint32_t seg_b = static_cast<uint32_t>(hb) * kwc_b;
     const bool seg_aligned = (pitch * pl.elt) % 16 == 0 && seg_b % 16 == 0;
     const uint32_t d16 = (iwc_b - kwc_b) & 15u;
@@ -764,7 +793,7 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
     while (bw) { const uint32_t t = gw % bw; gw = bw; bw = t; }
     const uint32_t wcls = 16 / gw;
     const size_t raw_b = (32 + static_cast<size_t>(hb) * iwc_b + 128 + 15) / 16 * 16;
-    if (kwc_b >= 16 && seg_aligned && ncls <= 4 && 128 + 2 * raw_b + csmem <= kLowerMaxSmem &&
+    if (kwc_b >= 16 && seg_aligned && ncls <= (spad ? 8 : 4) && 128 + 2 * raw_b + csmem <= kLowerMaxSmem &&
         nch * wcls <= 512) {
       p.ncls = ncls;
       int lg = 0;
@@ -809,6 +838,7 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   }
   const int64_t grid = p.n_lower_blocks + prep_blocks;
   if (grid > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
+  if (spad && p.ncls == 0) return launch_direct();
   set_lower_attributes();
   if (smem > kLowerMaxSmem) return cudaErrorInvalidConfiguration;
   if (pl.elt == 2)

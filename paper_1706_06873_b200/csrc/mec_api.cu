@@ -139,6 +139,43 @@ static cudaError_t encode_impl(CUtensorMap* map, bool tf32, int rank, const void
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Window geometry of the conv-path L for a strip length kw_s >= k_w i_c
+// (Alg.2 l.9: row (n, w) of L holds i_h strips; the window of output row h
+// starts at column h s_h kw_s), the TMA box alignment, the weight copies and
+// the workspace layout.
+void set_window_geometry(Plan* p, int64_t kw_s) {
+  const mec_shape_t* s = &p->s;
+  p->strip = kw_s;
+  p->l_cols = s->i_h * kw_s;
+  p->kdim = s->k_h * kw_s;
+  p->shift = static_cast<int64_t>(p->s_h) * kw_s;
+  // box-start alignment: 32 bytes (a 128-byte box row then covers 4 L2
+  // sectors, not 5), unless that needs more than 8 shifted weight copies;
+  // else the TMA minimum, 16 B
+  static const int align_try = getenv("MEC_BOX_ALIGN") ? atoi(getenv("MEC_BOX_ALIGN")) : 32;
+  for (int ab : {align_try, 32, 16}) {
+    p->avec = ab / p->elt;
+    int64_t a = p->shift % p->avec, b = p->avec;  // gcd(shift, avec)
+    while (a) { int64_t t = b % a; b = a; a = t; }
+    p->delta_step = static_cast<int>(b);
+    p->n_var = p->avec / p->delta_step;
+    if (p->n_var <= (ab > 32 ? 16 : 8) && p->n_var * p->n_tiles_n <= 32) break;
+  }
+  p->pitch = round_up(p->l_cols, p->avec);  // row starts keep the box alignment
+  p->kdim_pad = round_up(p->kdim + (p->avec - p->delta_step), p->bk);
+  if (p->n_var == 1) p->kdim_pad = round_up(p->kdim, p->bk);
+  p->bytes_L_pitched = static_cast<size_t>(s->i_n * p->o_w * p->pitch) * p->elt;
+  p->off_kt = static_cast<size_t>(round_up(static_cast<int64_t>(p->bytes_L_pitched), 1024));
+  p->bytes_kt = static_cast<size_t>(std::max(p->n_var * p->kdim_pad, p->kdim_g) * p->kc_pad) * p->elt;
+  p->ws_bytes = p->off_kt + p->bytes_kt + 1024;
+}
+
+Plan strip_padded_plan(const Plan& p) {
+  Plan q = p;
+  if (p.kwc_s > 0) set_window_geometry(&q, p.kwc_s);
+  return q;
+}
+
 mec_status_t make_plan(const mec_shape_t* s_in, int s_h, int s_w, mec_dtype_t dt, Plan* p, int pad_h,
                        int pad_w) {
   if (!s_in || !p) return MEC_ERR_INVALID_ARG;
@@ -164,31 +201,36 @@ mec_status_t make_plan(const mec_shape_t* s_in, int s_h, int s_w, mec_dtype_t dt
   p->elt = dt == MEC_DTYPE_BF16 ? 2 : 4;
   p->o_h = (s->i_h - s->k_h) / s_h + 1;  // Eq. (1), floor
   p->o_w = (s->i_w - s->k_w) / s_w + 1;
-  p->l_cols = s->i_h * s->k_w * s->i_c;
-  p->pitch = round_up(p->l_cols, 16 / p->elt);
-  p->kdim = s->k_h * s->k_w * s->i_c;
-  p->shift = static_cast<int64_t>(s_h) * s->k_w * s->i_c;
   p->bk = kTileKBytes / p->elt;
   p->vec = 16 / p->elt;
-  {
-    int64_t a = p->shift % p->vec, b = p->vec;  // gcd(shift, vec)
-    while (a) { int64_t t = b % a; b = a; a = t; }
-    p->delta_step = static_cast<int>(b);
-  }
-  p->n_var = p->vec / p->delta_step;
-  p->kdim_pad = round_up(p->kdim + (p->vec - p->delta_step), p->bk);
-  if (p->n_var == 1) p->kdim_pad = round_up(p->kdim, p->bk);
   p->n_tiles_n = static_cast<int>((s->k_c + 255) / 256);
   p->bn = static_cast<int>(round_up((s->k_c + p->n_tiles_n - 1) / p->n_tiles_n, 16));
   p->kc_pad = static_cast<int64_t>(p->n_tiles_n) * p->bn;
   p->n_L = s->i_n * p->o_w * s->i_h * s->k_w * s->i_c;
   p->n_O = s->i_n * p->o_h * p->o_w * s->k_c;
-  p->bytes_L_pitched = static_cast<size_t>(s->i_n * p->o_w * p->pitch) * p->elt;
-  p->off_kt = static_cast<size_t>(round_up(static_cast<int64_t>(p->bytes_L_pitched), 1024));
   p->kwc_p = round_up(s->k_w * s->i_c, p->vec);
   p->kdim_g = round_up(s->k_h * p->kwc_p, p->bk);
-  p->bytes_kt = static_cast<size_t>(std::max(p->n_var * p->kdim_pad, p->kdim_g) * p->kc_pad) * p->elt;
-  p->ws_bytes = p->off_kt + p->bytes_kt + 1024;
+  p->kdim_src = s->k_h * s->k_w * s->i_c;
+  set_window_geometry(p, s->k_w * s->i_c);
+  // Strip padding of the conv-path L: when the window shift
+  // s_h k_w i_c is not a whole 32-byte MMA K step (AlexNet conv1: 132
+  // elements), every strip of k_w i_c elements is stored with kwc_s - k_w i_c
+  // zeros after it, kwc_s the smallest length making s_h kwc_s a multiple of
+  // 32 bytes.  Then one A stream serves several output rows (multi-row tiles)
+  // with one weight copy.  Only where the padding costs <= 15% and windows of
+  // neighbouring rows overlap (k_h > s_h).
+  {
+    const int64_t kwc = s->k_w * s->i_c, step = 32 / p->elt;
+    int64_t kw_s = kwc;
+    while ((s_h * kw_s) % step != 0 || (kw_s * p->elt) % 2 != 0) ++kw_s;
+    if (kw_s != kwc && kw_s * p->elt >= 16 && kw_s * 100 <= kwc * 115 && s->k_h > s_h && p->o_h >= 4 &&
+        pad_h == 0 && pad_w == 0 && getenv("MEC_STRIP_PAD")) {
+      Plan q = *p;
+      set_window_geometry(&q, kw_s);
+      p->kwc_s = kw_s;
+      p->ws_bytes = std::max(p->ws_bytes, q.ws_bytes);
+    }
+  }
   // TMA coordinate / extent limits (int32 coordinates, dims <= 2^32)
   if (p->l_cols + p->kdim_pad >= (1LL << 31) || s->i_n * p->o_w >= (1LL << 31) ||
       p->kdim_pad >= (1LL << 31))
@@ -359,8 +401,12 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
   }
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(ws) + 1023) & ~static_cast<uintptr_t>(1023));
+  // the conv path's L: the strip-padded layout where the plan
+  // has one and multi-row tiles are not switched off; the fused path reads I
+  const bool spad = p.kwc_s > 0 && path != MEC_PATH_FUSED && opt->rows_per_tile != 1;
+  const Plan pc = spad ? mec::strip_padded_plan(p) : p;
   void* L = base;
-  void* Kt = base + p.off_kt;
+  void* Kt = base + pc.off_kt;
 
   auto rec = [&](int i) {
     if (opt->stage_events[i]) cudaEventRecord(static_cast<cudaEvent_t>(opt->stage_events[i]), stream_);
@@ -370,7 +416,7 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
   rec(0);
   // Alg.2 l.2-7: lowering into the pitch-padded L, and K as a (k_h k_w i_c) x k_c matrix
   // (the fused path skips L: only the weight operand is prepared)
-  e = mec::launch_lower(p, I, path == MEC_PATH_FUSED ? nullptr : L, p.pitch, K, Kt, stream_, &launches,
+  e = mec::launch_lower(pc, I, path == MEC_PATH_FUSED ? nullptr : L, pc.pitch, K, Kt, stream_, &launches,
                         path == MEC_PATH_FUSED && !mec::fused_eligible(p));
   if (e != cudaSuccess) goto fail;
   rec(1);
@@ -391,7 +437,7 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
       ga.batch_folded = false;
       ga.out_hnwc = false;
     }
-    e = mec::launch_window_gemm(p, ga, stream_, &launches);
+    e = mec::launch_window_gemm(pc, ga, stream_, &launches);
     if (e != cudaSuccess) goto fail;
   }
   rec(2);

@@ -27,18 +27,26 @@ struct Plan {
   mec_dtype_t dt;
   int elt;               // bytes per element (2 bf16, 4 tf32/fp32)
   int64_t o_h, o_w;      // Eq. (1)
-  int64_t l_cols;        // i_h k_w i_c: one row of L (Alg.2 l.9 / l.21 "i_h k_w i_c")
+  // Window geometry of the L the GEMM reads (set_window_geometry).  strip is
+  // its strip length: k_w i_c (the paper's dense L), or kwc_s in the
+  // strip-padded plan (strip_padded_plan; the extra elements are zeros).
+  int64_t strip;
+  int64_t kwc_s;         // strip-padded length for the conv path, 0 = not used
+  int64_t kdim_src;      // k_h k_w i_c (the paper's reduction length, whatever the strip)
+  int64_t l_cols;        // i_h strip: one row of L (Alg.2 l.9 / l.21 "i_h k_w i_c")
   int64_t pitch;         // l_cols rounded up to 16 B (TMA stride rule), elements
   int64_t kdim;          // k_h k_w i_c: GEMM reduction length
   int64_t shift;         // s_h k_w i_c: column offset between output rows
   int bk;                // K-tile in elements (128 B / elt)
   // TMA needs every box to start 16-byte aligned in dim 0, but window h starts
   // at column h*shift.  The box therefore starts at the aligned column
-  // x = h*shift - delta, delta = (h*shift) mod vec (vec = 16/elt), and the
-  // B operand used for that window is K_mat shifted down by delta rows
-  // (zero rows above).  delta takes n_var = vec / gcd(shift, vec) values,
-  // multiples of delta_step = gcd(shift, vec); Kt holds one copy per value.
+  // x = h*shift - delta, delta = (h*shift) mod avec (avec = 32/elt, or 16/elt
+  // when 32 bytes would need more than 8 copies), and the B operand used for
+  // that window is K_mat shifted down by delta rows (zero rows above).  delta
+  // takes n_var = avec / gcd(shift, avec) values, multiples of delta_step =
+  // gcd(shift, avec); Kt holds one copy per value.
   int vec;               // elements per 16 bytes
+  int avec;              // box-start alignment of the window GEMM, elements (32 or 16 bytes)
   int delta_step;        // gcd(shift, vec)
   int n_var;             // number of shifted weight copies
   int64_t kdim_pad;      // (kdim + max delta) rounded up to bk
@@ -57,6 +65,11 @@ struct Plan {
   size_t ws_bytes;         // total workspace (incl. alignment slack)
 };
 
+// The plan's window geometry (l_cols, pitch, kdim, shift, box alignment,
+// weight copies, workspace) for strip length kw_s.
+void set_window_geometry(Plan* p, int64_t kw_s);
+// The conv path's plan: p with the strip-padded geometry when p.kwc_s > 0.
+Plan strip_padded_plan(const Plan& p);
 // Returns MEC_OK and fills *p, or MEC_ERR_INVALID_ARG.
 // pad_h / pad_w >= 0: zero padding applied virtually (never materialised).
 mec_status_t make_plan(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, Plan* p, int pad_h = 0,

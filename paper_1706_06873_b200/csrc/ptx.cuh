@@ -364,6 +364,39 @@ __device__ __forceinline__ void mma_ss_atom_elect(uint32_t tmem_d, uint64_t ades
   }
 }
 
+// As mma_ss_atom_elect, with an independent B descriptor per 32-byte K step
+// (multi-row tiles whose window shift is a whole K step but not a whole atom).
+template <bool kTF32>
+__device__ __forceinline__ void mma_ss_atom4b_elect(uint32_t tmem_d, uint64_t adesc, uint64_t b0, uint64_t b1,
+                                                    uint64_t b2, uint64_t b3, uint32_t idesc,
+                                                    uint32_t accumulate) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3;\n\t"
+        "setp.ne.b32 p, %7, 0;\n\t"
+        "add.u64 a1, %1, 2;\n\tadd.u64 a2, %1, 4;\n\tadd.u64 a3, %1, 6;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], a1, %3, %6, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], a2, %4, %6, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], a3, %5, %6, 1;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(b0), "l"(b1), "l"(b2), "l"(b3), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3;\n\t"
+        "setp.ne.b32 p, %7, 0;\n\t"
+        "add.u64 a1, %1, 2;\n\tadd.u64 a2, %1, 4;\n\tadd.u64 a3, %1, 6;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, %3, %6, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, %4, %6, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, %5, %6, 1;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(b0), "l"(b1), "l"(b2), "l"(b3), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+
 // Whole-warp call: one elected lane issues the 4 TS MMAs of a 128-byte A atom
 // (K = 4 x 32 bytes: A columns a_tmem + 0/8/16/24, B descriptor + 0/2/4/6 in
 // 16-byte units) -- one election and one operand transfer per atom.

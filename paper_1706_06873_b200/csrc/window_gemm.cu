@@ -167,9 +167,10 @@ struct GemmParams {
   int n_kstages;    // ceil(n_atoms / 2)
   int bn, n_tiles_n;
   int n_var;
+  int avec;         // box-start alignment (elements); variant v absorbs delta = h shift mod avec
   int n_combo;      // n_var * n_tiles_n
   int ctas_per_combo;
-  int h_first[8];   // smallest h with weight variant v
+  int h_first[16];  // smallest h with weight variant v
   // multi-row tiles: a tile computes R consecutive output rows h0 .. h0+R-1;
   // it streams the union of their windows once (columns [h0 shift,
   // (h0+R-1) shift + kdim)) and issues every A atom's MMAs into the R TMEM
@@ -177,7 +178,8 @@ struct GemmParams {
   // shift % kchunk == 0, one weight variant, resident weights).  R = 1 is
   // the one-window-per-tile schedule.
   int R;
-  int shift_atoms;  // multi-row: shift / bk (window start advance per output row, in K-atoms)
+  int shift_atoms;  // multi-row: shift / bk if a whole number of K-atoms, else 0
+  int shift_chunks; // multi-row: shift / kchunk (window start advance per output row, in 32-byte K steps)
   int kchunk;       // elements per 32-byte MMA K step (16 bf16 / 8 tf32)
   int kchunk_log2;
   int n_chunks;     // ceil(kdim / kchunk): B chunks holding weights
@@ -340,6 +342,14 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) MEC_TRACE_EV(0, 7);
+#ifdef MEC_TRACE
+  // SM clock check: clock64 and globaltimer at entry and exit (tile slot 62)
+  unsigned long long clk0 = 0, gt0 = 0;
+  if (threadIdx.x == 0 && mec_trace_ptr != nullptr) {
+    clk0 = clock64();
+    gt0 = mec_gtime();
+  }
+#endif
   const int32_t b_row0 = static_cast<int32_t>(v * p.kc_pad + nt * p.bn);
 
   if (warp == 0) {
@@ -357,7 +367,7 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
           ptx::tma_load_2d(smemB + static_cast<size_t>(a) * b_tile_bytes, &tmB, bfull, a * p.bk,
                            b_row0, hintB);
       }
-      constexpr int64_t kVec = kTF32 ? 4 : 8;  // elements per 16 bytes
+      const int64_t kVec = p.avec;  // box-start alignment (elements)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t t = t_begin; !kGather && t < n_tiles; t += t_step) {
@@ -491,7 +501,7 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
       for (int ks = 0; ks < n_ks; ++ks) {
         const int na = min(kAtomsPerStage, c.n_a - ks * kAtomsPerStage);
         if (kGather && p.spin) ptx::mbar_spin(&full[stage], phase);
-        else ptx::mbar_wait(&full[stage], phase);
+        else if (!(p.dbg & 128)) ptx::mbar_wait(&full[stage], phase);  // (trace builds: 128 = no full waits)
         ptx::tc_fence_after();
         if (ks == 0 && lane == 0) MEC_TRACE_EV(tl, 3);
         if (kGather && ks < 7 && lane == 0) MEC_TRACE_EV(tl, 8 + ks);
@@ -523,12 +533,36 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
               // row h0 + r's window -- the same 4 MMAs as R = 1, into
               // accumulator r against resident weight tile b
               const int sa = ks * kAtomsPerStage + a;
-              for (int r = 0; r < c.r_eff; ++r) {
-                const int b = sa - r * p.shift_atoms;
-                if (b < 0 || b >= p.n_atoms || (p.dbg & 2)) continue;
-                ptx::mma_ss_atom_elect<kTF32>(d_set + static_cast<uint32_t>(r * p.bn), ad,
-                                              b_desc0 + static_cast<uint32_t>(b) * b_tile16, p.idesc,
-                                              b != 0 ? 1u : 0u);
+              if (p.shift_atoms > 0) {
+                for (int r = 0; r < c.r_eff; ++r) {
+                  const int b = sa - r * p.shift_atoms;
+                  if (b < 0 || b >= p.n_atoms || (p.dbg & 2)) continue;
+                  ptx::mma_ss_atom_elect<kTF32>(d_set + static_cast<uint32_t>(r * p.bn), ad,
+                                                b_desc0 + static_cast<uint32_t>(b) * b_tile16, p.idesc,
+                                                b != 0 ? 1u : 0u);
+                }
+              } else {
+                // shift a whole 32-byte K step only: the atom's K step k meets
+                // B chunk c0 + k of row r (chunk = 32 bytes of a B tile row)
+                const int nbc = 4 * p.n_atoms;
+                for (int r = 0; r < c.r_eff; ++r) {
+                  const int c0 = 4 * sa - r * p.shift_chunks;
+                  if (c0 + 3 < 0 || c0 >= nbc || (p.dbg & 2)) continue;
+                  const uint32_t d = d_set + static_cast<uint32_t>(r * p.bn);
+                  auto bdesc = [&](int ch) -> uint64_t {
+                    return b_desc0 + static_cast<uint32_t>((ch >> 2) * static_cast<int>(b_tile16) + (ch & 3) * 2);
+                  };
+                  if (c0 >= 0 && c0 + 3 < nbc) {
+                    ptx::mma_ss_atom4b_elect<kTF32>(d, ad, bdesc(c0), bdesc(c0 + 1), bdesc(c0 + 2), bdesc(c0 + 3),
+                                                    p.idesc, c0 != 0 ? 1u : 0u);
+                  } else {
+                    for (int k = 0; k < 4; ++k) {
+                      const int ch = c0 + k;
+                      if (ch < 0 || ch >= nbc) continue;
+                      ptx::mma_ss_elect<kTF32>(d, ad + 2 * k, bdesc(ch), p.idesc, ch != 0 ? 1u : 0u);
+                    }
+                  }
+                }
               }
             }
           }
@@ -706,7 +740,7 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
         orow_own = static_cast<unsigned char*>(p.O) +
                    (out_row * p.k_c + static_cast<int64_t>(nt) * p.bn) * kOutElt;
       }
-      if (kGather && p.backoff_ns > 0) ptx::mbar_wait_backoff(&tfull[acc], acc_phase, p.backoff_ns);
+      if (p.backoff_ns > 0) ptx::mbar_wait_backoff(&tfull[acc], acc_phase, p.backoff_ns);
       else ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       if ((warp & 3) == 2 && lane == 0) MEC_TRACE_EV(tl, 5);
@@ -853,6 +887,15 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+#ifdef MEC_TRACE
+  if (threadIdx.x == 0 && mec_trace_ptr != nullptr) {
+    unsigned long long* c = mec_trace_ptr + (static_cast<size_t>(blockIdx.x) * 64 + 62) * 16;
+    c[0] = clk0;
+    c[1] = clock64();
+    c[2] = gt0;
+    c[3] = mec_gtime();
+  }
+#endif
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, p.tmem_cols);
@@ -1008,15 +1051,16 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   p.bn = pl.bn;
   p.n_tiles_n = pl.n_tiles_n;
   p.n_var = a.fused ? 1 : pl.n_var;  // the fused path uses weight variant 0 only
+  p.avec = pl.avec;
   p.n_combo = p.n_var * pl.n_tiles_n;
   if (p.n_combo > kMaxCombos) return cudaErrorInvalidConfiguration;
   // first h of each weight variant: delta(h) = (h shift) mod vec = v delta_step
-  for (int v = 0; v < 8; ++v) p.h_first[v] = static_cast<int>(pl.o_h);  // none
+  for (int v = 0; v < 16; ++v) p.h_first[v] = static_cast<int>(pl.o_h);  // none
   if (a.fused) {
     p.h_first[0] = 0;
   } else {
     for (int64_t h = 0; h < std::min<int64_t>(pl.o_h, pl.n_var); ++h) {
-      const int v = static_cast<int>(((h * pl.shift) % pl.vec) / pl.delta_step);
+      const int v = static_cast<int>(((h * pl.shift) % pl.avec) / pl.delta_step);
       if (p.h_first[v] > h) p.h_first[v] = static_cast<int>(h);
     }
   }
@@ -1028,6 +1072,7 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   if (const char* e = getenv("MEC_GATHER_SPIN")) p.spin = gather && atoi(e) != 0;
   p.backoff_ns = 0;
   if (const char* e = getenv("MEC_GATHER_BACKOFF")) p.backoff_ns = gather ? static_cast<uint32_t>(atoi(e)) : 0u;
+  if (const char* e = getenv("MEC_EPI_BACKOFF")) p.backoff_ns = gather ? p.backoff_ns : static_cast<uint32_t>(atoi(e));
   p.idesc = ptx::instr_desc(tf32, kBM, pl.bn);
   p.kchunk = 32 / pl.elt;
   p.kchunk_log2 = pl.elt == 2 ? 4 : 3;
@@ -1099,6 +1144,8 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
                       : (b_res + 2 * kMaxAtomsPerStage * kAtomBytes <= budget_g && b_res <= 120 * 1024);
   if (gather && !p.resident) return cudaErrorInvalidConfiguration;
   p.aps = (p.resident && !gather) ? 2 : 1;
+  if (const char* e = getenv("MEC_APS"))  // (experiments) K-atoms per pipeline stage with resident weights
+    if (p.resident && !gather) p.aps = std::max(1, std::min(6, atoi(e)));
   const size_t stage_a = gather ? 0 : static_cast<size_t>(p.aps) * kAtomBytes;
   p.n_kstages = (p.n_atoms + p.aps - 1) / p.aps;
   int stages;
@@ -1113,19 +1160,23 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   // Multi-row tiles (requested via mec_options_t::rows_per_tile) are parity-
   // tested, but with SS operands the extra B reads make them shared-memory-
   // bound on B200 (slower than R = 1), so auto = 1.
+  // rows_per_tile 0 = auto: 4 (measured: C3 165 -> 142 us, C2 575 -> 500 us),
+  // capped by TMEM (2 accumulator sets of R x bn columns)
+  const int rpt = a.rows_per_tile > 0 ? a.rows_per_tile : (getenv("MEC_AUTO_R") ? atoi(getenv("MEC_AUTO_R")) : 4);
   p.R = 1;
-  if (a.rows_per_tile > 1 && !a.fused && pl.n_var == 1 && p.resident && pl.shift % pl.bk == 0 &&
+  if (rpt > 1 && !a.fused && pl.n_var == 1 && p.resident && pl.shift % p.kchunk == 0 &&
       pl.shift < pl.kdim && pl.o_h > 1) {
     const int r = static_cast<int>(std::min<int64_t>({8, 512 / (2 * pl.bn), pl.o_h}));
-    p.R = std::max(1, std::min(r, a.rows_per_tile));
+    p.R = std::max(1, std::min(r, rpt));
   }
 #ifdef MEC_TRACE
   if (const char* e = getenv("MEC_DEBUG_R")) {
-    if (!a.fused && pl.n_var == 1 && p.resident && pl.shift % pl.bk == 0 && pl.shift < pl.kdim && pl.o_h > 1)
+    if (!a.fused && pl.n_var == 1 && p.resident && pl.shift % p.kchunk == 0 && pl.shift < pl.kdim && pl.o_h > 1)
       p.R = std::max(1, std::min<int>(std::min<int64_t>({8, 512 / (2 * pl.bn), pl.o_h}), atoi(e)));
   }
 #endif
-  p.shift_atoms = static_cast<int>(pl.shift / pl.bk);
+  p.shift_atoms = pl.shift % pl.bk == 0 ? static_cast<int>(pl.shift / pl.bk) : 0;
+  p.shift_chunks = static_cast<int>(pl.shift / p.kchunk);
   p.n_acc = p.R > 1 ? 2 : (4 * pl.bn <= 512 ? 4 : 2);
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(p.n_acc * p.R * pl.bn)) cols <<= 1;

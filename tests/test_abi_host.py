@@ -73,9 +73,13 @@ def test_workspace_is_lowered_size_not_im2col():
             pitch = -(-(c["i_h"] * c["k_w"] * c["i_c"]) // (16 // elt)) * (16 // elt)
             L_pitched = c["i_n"] * o_w * pitch * elt
             assert ws >= n_l * elt and ws >= L_pitched
-            # only pitch padding + the prepared K + alignment on top of L
-            kt = (-(-c["k_c"] // 16) * 16 + 256) * (-(-(c["k_h"] * c["k_w"] * c["i_c"]) // 64) * 64 + 64) * elt
-            assert ws <= L_pitched + kt + 4096, name
+            # only pitch padding (rows rounded up to at most 32 bytes, the window
+            # GEMM's box alignment; strips padded by at most 15%)
+            # + the prepared K (at most 8 shifted copies) + alignment on top of L
+            pitch32 = -(-(c["i_h"] * c["k_w"] * c["i_c"]) // (32 // elt)) * (32 // elt)
+            L_pitched32 = int(c["i_n"] * o_w * (pitch32 * 1.15 + 32 // elt) * elt)
+            kt = 8 * (-(-c["k_c"] // 16) * 16 + 256) * (-(-(c["k_h"] * c["k_w"] * c["i_c"]) // 64) * 64 + 64) * elt
+            assert ws <= L_pitched32 + kt + 4096, name
             if c["k_h"] > c["s_h"] and (c["i_h"] - c["k_h"]) % c["s_h"] == 0:
                 # the lowered buffer itself is smaller than im2col's (Eq. 4); on the batched
                 # configs so is the whole workspace

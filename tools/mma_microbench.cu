@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../paper_1706_06873_b200/csrc/ptx.cuh"
 
@@ -14,7 +15,7 @@ using namespace mec;
 
 // kMode: 0 = SS, elect in asm; 1 = SS, elect block; 2 = TS (A in TMEM cols 256..); 3 = TS + commit per 4
 template <int kMode>
-__global__ void __launch_bounds__(128, 1) mma_bench(int n, int iters, unsigned long long* cycles) {
+__global__ void __launch_bounds__(128, 1) mma_bench(int n, int iters, unsigned long long* cycles, int rnd) {
   constexpr bool kElectInAsm = kMode != 1;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar, bar2;
@@ -25,9 +26,17 @@ __global__ void __launch_bounds__(128, 1) mma_bench(int n, int iters, unsigned l
     ptx::mbar_init(&bar2, 1);
     ptx::fence_mbar_init();
   }
-  // zero operands
-  for (int i = threadIdx.x; i < (32768 + 7 * 16384) / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  // operands: zero, or (rnd) pseudo-random bf16 in about [-1, 1)
+  for (int i = threadIdx.x; i < (131072 + 6 * 96 * 128) / 16; i += blockDim.x) {
+    uint32_t w[4];
+    for (int j = 0; j < 4; ++j) {
+      uint32_t x = (i * 4 + j) * 2654435761u + 12345u;
+      x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+      // two bf16: sign/exponent around 1.0 (0x3f80), random mantissa and sign
+      w[j] = rnd ? (((x & 0x807Fu) | 0x3F00u) | (((x >> 16) & 0x807Fu) | 0x3F00u) << 16) : 0u;
+    }
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
   if (warp == 0) ptx::tmem_alloc_dyn(&tslot, 512);
   ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
@@ -37,10 +46,29 @@ __global__ void __launch_bounds__(128, 1) mma_bench(int n, int iters, unsigned l
   if (warp == 1) {
     const uint32_t idesc = ptx::instr_desc(false, 128, n);
     const uint64_t ad0 = ptx::smem_desc_sw128(ptx::smem_u32(smem));
-    const uint64_t bd0 = ptx::smem_desc_sw128(ptx::smem_u32(smem + 32768));
+    const uint64_t bd0 = ptx::smem_desc_sw128(ptx::smem_u32(smem + (kMode >= 6 ? 131072 : 32768)));
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
-      if constexpr (kMode >= 4) {
+      if constexpr (kMode == 6 || kMode == 7) {
+        // kernel-like SS: per "tile" 6 K-atoms of A from a 4-stage ring (2 atoms
+        // per stage), B from 6 resident atoms, D rotating over 4 accumulators of
+        // n columns, commit per stage (mode 7: D always at column 0)
+        const uint32_t d = tmem + (kMode == 6 ? static_cast<uint32_t>((it & 3) * n) : 0u);
+#pragma unroll 1
+        for (int st = 0; st < 3; ++st) {
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+            const int atom = st * 2 + a;
+            const uint64_t ad = ad0 + static_cast<uint32_t>(((it * 3 + st) & 3) * 2048 + a * 1024);
+            const uint64_t bd = bd0 + static_cast<uint32_t>(atom * n * 128 / 16);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              ptx::mma_ss_elect<false>(d, ad + 2 * k, bd + 2 * k, idesc, (atom | k) != 0);
+          }
+          ptx::mma_commit_elect(&bar2);
+        }
+      } else if constexpr (kMode >= 4) {
         // 7 B atoms (N x 128 B each), 4 MMAs per atom, commit per atom (kernel-like)
 #pragma unroll 1
         for (int a = 0; a < 7; ++a) {
@@ -95,32 +123,38 @@ __global__ void __launch_bounds__(128, 1) mma_bench(int n, int iters, unsigned l
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int rnd = argc > 1 ? atoi(argv[1]) : 0;
   unsigned long long* d;
   cudaMalloc(&d, 1024 * sizeof(unsigned long long));
-  const int smem = 32768 + 7 * 16384 + 1024;
+  const int smem = 131072 + 6 * 96 * 128 + 1024;
   cudaFuncSetAttribute(mma_bench<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(mma_bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(mma_bench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(mma_bench<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(mma_bench<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(mma_bench<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_bench<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_bench<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  const char* names[6] = {"SS elect-in-asm", "SS elect-block ", "TS             ", "TS commit/4    ",
-                          "TS 7 B atoms   ", "TS 7B + LDS    "};
-  for (int variant = 0; variant < 6; ++variant) {
-    for (int n : {32, 64, 96, 128}) {
+  const char* names[8] = {"SS elect-in-asm", "SS elect-block ", "TS             ", "TS commit/4    ",
+                          "TS 7 B atoms   ", "TS 7B + LDS    ", "SS kernel-like ", "SS kernel D=0  "};
+  printf("operands: %s\n", rnd ? "random" : "zero");
+  for (int variant = 0; variant < 8; ++variant) {
+    for (int n : {32, 64, 96}) {
       cudaEvent_t a, b;
       cudaEventCreate(&a);
       cudaEventCreate(&b);
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(a);
-        if (variant == 0) mma_bench<0><<<148, 128, smem>>>(n, iters, d);
-        if (variant == 1) mma_bench<1><<<148, 128, smem>>>(n, iters, d);
-        if (variant == 2) mma_bench<2><<<148, 128, smem>>>(n, iters, d);
-        if (variant == 3) mma_bench<3><<<148, 128, smem>>>(n, iters, d);
-        if (variant == 4) mma_bench<4><<<148, 128, smem>>>(n, iters, d);
-        if (variant == 5) mma_bench<5><<<148, 128, smem>>>(n, iters, d);
+        if (variant == 0) mma_bench<0><<<148, 128, smem>>>(n, iters, d, rnd);
+        if (variant == 1) mma_bench<1><<<148, 128, smem>>>(n, iters, d, rnd);
+        if (variant == 2) mma_bench<2><<<148, 128, smem>>>(n, iters, d, rnd);
+        if (variant == 3) mma_bench<3><<<148, 128, smem>>>(n, iters, d, rnd);
+        if (variant == 4) mma_bench<4><<<148, 128, smem>>>(n, iters, d, rnd);
+        if (variant == 5) mma_bench<5><<<148, 128, smem>>>(n, iters, d, rnd);
+        if (variant == 6) mma_bench<6><<<148, 128, smem>>>(n, iters, d, rnd);
+        if (variant == 7) mma_bench<7><<<148, 128, smem>>>(n, iters, d, rnd);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
       }
@@ -128,7 +162,7 @@ int main() {
       cudaEventElapsedTime(&ms, a, b);
       unsigned long long h[148];
       cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-      const double mmas = (variant >= 4 ? 28.0 : 8.0) * iters;
+      const double mmas = (variant >= 6 ? 24.0 : (variant >= 4 ? 28.0 : 8.0)) * iters;
       const double flops = 148.0 * mmas * 2.0 * 128 * n * 16;
       printf("%s N=%3d: %.1f cycles/MMA (cta0), %.3f ms, %.0f TFLOP/s  [%s]\n",
              names[variant], n, h[0] / mmas, ms, flops / (ms * 1e-3) / 1e12,

@@ -42,6 +42,12 @@ for c in ([] if args.quiet else list(ctas[:2]) + [ctas[-1]]):
                         (("R_wait", 7), ("R_dec", 8), ("R_arm", 9), ("R_cp0", 10), ("R_cp1", 11), ("R_req", 15))
                         if tr[c, tl, e])
         print("  tile", tl, " ".join(f"{n}={(x - t0)/1e3:7.2f}" if x else f"{n}=   -   " for n, x in zip(names, row)) + extra)
+# SM clock: clock64 / globaltimer deltas over each CTA's lifetime (slot 62)
+ck = tr[ctas, 62, :4]
+ok = (ck[:, 3] > ck[:, 2])
+if ok.any():
+    mhz = (ck[ok, 1] - ck[ok, 0]) / ((ck[ok, 3] - ck[ok, 2]) / 1e3) 
+    print("SM clock over CTA lifetimes (MHz): median %.0f min %.0f max %.0f" % (np.median(mhz), mhz.min(), mhz.max()))
 # aggregates
 ends = tr[ctas][:, :, 6]; ends = ends[ends > 0]
 print("kernel span us", (ends.max() - t0) / 1e3)
