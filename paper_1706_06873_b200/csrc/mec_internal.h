@@ -117,6 +117,14 @@ cudaError_t launch_maxpool(const void* X, void* Y, int64_t i_n, int64_t h, int64
 bool gather_eligible(const Plan& p);
 cudaError_t launch_window_gemm(const Plan& p, const GemmArgs& a, cudaStream_t st, int* launches);
 
+// The same window GEMMs as a sweep along h with A staged in TMEM
+// (sweep_gemm.cu): each 128-row tile of L is streamed once per chunk of H
+// output rows instead of once per row.  Returns cudaErrorNotSupported (and
+// launches nothing) where it does not apply; the caller then runs
+// launch_window_gemm.
+bool sweep_config(const Plan& p, bool batch_folded, int* n_vres, int* n_acc, int* ns, int* stages);
+cudaError_t launch_sweep_gemm(const Plan& p, const GemmArgs& a, cudaStream_t st, int* launches);
+
 // Solution A format fix, paper-literal (Alg.2 l.13-19): "Copy L = O" and the
 // block transpose O[n,h,:] = L[h,n,:].
 cudaError_t launch_sola_copy(const Plan& p, const void* O, void* Laux, cudaStream_t st,

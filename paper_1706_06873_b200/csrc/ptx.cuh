@@ -433,6 +433,112 @@ __device__ __forceinline__ void mma_ts_atom_elect(uint32_t tmem_d, uint32_t a_tm
   }
 }
 
+// Whole-warp call: one elected lane issues the first n (1..4) of the 4 TS
+// MMAs of a 128-byte K group: A columns a_tmem + 0/8/16/24, B descriptor
+// + 0/2/4/6 (16-byte units, i.e. 32-byte K steps).  accumulate applies to the
+// first MMA; the others always accumulate.
+template <bool kTF32>
+__device__ __forceinline__ void mma_ts_grp_elect(uint32_t tmem_d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate, int n) {
+#define MEC_TS_GRP_BODY(KIND)                                                                 \
+  asm volatile(                                                                               \
+      "{\n\t.reg .pred p, e, e1, e2, e3;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"    \
+      "setp.ne.b32 p, %4, 0;\n\t"                                                             \
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"                    \
+      "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t"                      \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                       \
+      "setp.gt.and.s32 e1, %5, 1, e;\n\t"                                                     \
+      "setp.gt.and.s32 e2, %5, 2, e;\n\t"                                                     \
+      "setp.gt.and.s32 e3, %5, 3, e;\n\t"                                                     \
+      "@e tcgen05.mma.cta_group::1.kind::" KIND " [%0], [%1], %2, %3, p;\n\t"                   \
+      "@e1 tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a1], b1, %3, 1;\n\t"                  \
+      "@e2 tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a2], b2, %3, 1;\n\t"                  \
+      "@e3 tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a3], b3, %3, 1;\n\t}" ::"r"(tmem_d),  \
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(n)                             \
+      : "memory")
+  if constexpr (kTF32) {
+    MEC_TS_GRP_BODY("tf32");
+  } else {
+    MEC_TS_GRP_BODY("f16");
+  }
+#undef MEC_TS_GRP_BODY
+}
+
+// Whole-warp call: the 4 TS MMAs of a 128-byte K group (A columns a_tmem +
+// 0/8/16/24, B descriptor low word + 0/2/4/6; the high word is the constant
+// of smem_desc_sw128), issued by one elected lane behind a branch rather than
+// per-instruction predicates (fewer uniform-register moves per MMA).
+template <bool kTF32>
+__device__ __forceinline__ void mma_ts_atom_br(uint32_t tmem_d, uint32_t a_tmem, uint32_t bdesc_lo, uint32_t idesc,
+                                               uint32_t accumulate) {
+#define MEC_TS_BR_BODY(KIND)                                                                         \
+  asm volatile(                                                                                      \
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 a1, a2, a3, l1, l2, l3;\n\t.reg .b64 b0, b1, b2, b3;\n\t"       \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                              \
+      "@!e bra SKIP_%=;\n\t"                                                                         \
+      "setp.ne.b32 p, %4, 0;\n\t"                                                                    \
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"                           \
+      "add.u32 l1, %2, 2;\n\tadd.u32 l2, %2, 4;\n\tadd.u32 l3, %2, 6;\n\t"                             \
+      "mov.b64 b0, {%2, 0x40004040};\n\tmov.b64 b1, {l1, 0x40004040};\n\t"                             \
+      "mov.b64 b2, {l2, 0x40004040};\n\tmov.b64 b3, {l3, 0x40004040};\n\t"                             \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [%1], b0, %3, p;\n\t"                             \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a1], b1, %3, 1;\n\t"                             \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a2], b2, %3, 1;\n\t"                             \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a3], b3, %3, 1;\n\t"                             \
+      "SKIP_%=:\n\t}" ::"r"(tmem_d),                                                                  \
+      "r"(a_tmem), "r"(bdesc_lo), "r"(idesc), "r"(accumulate)                                        \
+      : "memory")
+  if constexpr (kTF32) {
+    MEC_TS_BR_BODY("tf32");
+  } else {
+    MEC_TS_BR_BODY("f16");
+  }
+#undef MEC_TS_BR_BODY
+}
+
+// Whole-warp call: one elected lane issues n_groups (>= 1) consecutive
+// 128-byte K groups of TS MMAs into one accumulator, in a PTX loop (no
+// per-group election or convergence code): group g reads A at TMEM column
+// a_tmem + 32 g (wrapping from ring_end back by ring_cols), steps + 0/8/16/24,
+// and B at descriptor low word b_lo + g b_step + 0/2/4/6 (high word: the
+// constant of smem_desc_sw128).  The first MMA accumulates iff accumulate.
+template <bool kTF32>
+__device__ __forceinline__ void mma_ts_groups_elect(uint32_t tmem_d, uint32_t a_tmem, uint32_t ring_end,
+                                                    uint32_t ring_cols, uint32_t b_lo, uint32_t b_step,
+                                                    uint32_t idesc, uint32_t accumulate, int n_groups) {
+#define MEC_TS_LOOP_BODY(KIND)                                                                         \
+  asm volatile(                                                                                        \
+      "{\n\t.reg .pred e, p, w, more;\n\t.reg .b32 c, b, g, a1, a2, a3, l1, l2, l3, hi;\n\t"             \
+      ".reg .b64 b0, b1, b2, b3;\n\t"                                                                  \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                                \
+      "@!e bra DONE_%=;\n\t"                                                                           \
+      "mov.b32 hi, 0x40004040;\n\t"                                                                    \
+      "mov.b32 c, %1;\n\tmov.b32 b, %4;\n\tmov.b32 g, 0;\n\t"                                           \
+      "setp.ne.b32 p, %7, 0;\n"                                                                        \
+      "LOOP_%=:\n\t"                                                                                   \
+      "add.u32 a1, c, 8;\n\tadd.u32 a2, c, 16;\n\tadd.u32 a3, c, 24;\n\t"                                \
+      "add.u32 l1, b, 2;\n\tadd.u32 l2, b, 4;\n\tadd.u32 l3, b, 6;\n\t"                                  \
+      "mov.b64 b0, {b, hi};\n\tmov.b64 b1, {l1, hi};\n\tmov.b64 b2, {l2, hi};\n\tmov.b64 b3, {l3, hi};\n\t" \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [c], b0, %6, p;\n\t"                                \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a1], b1, %6, 1;\n\t"                               \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a2], b2, %6, 1;\n\t"                               \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a3], b3, %6, 1;\n\t"                               \
+      "setp.ne.b32 p, 1, 0;\n\t"                                                                       \
+      "add.u32 c, c, 32;\n\tsetp.ge.u32 w, c, %2;\n\t@w sub.u32 c, c, %3;\n\t"                          \
+      "add.u32 b, b, %5;\n\tadd.u32 g, g, 1;\n\t"                                                      \
+      "setp.lt.s32 more, g, %8;\n\t@more bra LOOP_%=;\n"                                                \
+      "DONE_%=:\n\t}" ::"r"(tmem_d),                                                                   \
+      "r"(a_tmem), "r"(ring_end), "r"(ring_cols), "r"(b_lo), "r"(b_step), "r"(idesc), "r"(accumulate),    \
+      "r"(n_groups)                                                                                     \
+      : "memory")
+  if constexpr (kTF32) {
+    MEC_TS_LOOP_BODY("tf32");
+  } else {
+    MEC_TS_LOOP_BODY("f16");
+  }
+#undef MEC_TS_LOOP_BODY
+}
+
 // Whole-warp call: one elected lane commits (arrives on `bar` when done).
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
   asm volatile(
@@ -483,6 +589,13 @@ __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
+}
+
+__device__ __forceinline__ void tmem_st_32x32b_x4(uint32_t taddr, uint32_t r0, uint32_t r1, uint32_t r2,
+                                                  uint32_t r3) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(r0), "r"(r1),
+               "r"(r2), "r"(r3)
+               : "memory");
 }
 
 __device__ __forceinline__ void tmem_st_wait() {

@@ -1,0 +1,799 @@
+// sweep_gemm.cu -- MEC's window GEMMs as a sweep along h, A staged in TMEM
+// (sm_100a).
+//
+// Paper: output row h is O[:, h] = L[:, h s_h k_w i_c : + k_h k_w i_c] x K,
+// one GEMM per row over an overlapping window of L (Sec. 3.2, P:100-102;
+// Alg.2 l.10-12 Solution A, l.23-25 Solution B).  Consecutive windows overlap
+// by k_h k_w i_c - s_h k_w i_c columns: the paper's BLAS calls re-read that
+// overlap once per row (k_h / s_h times in all).  On B200 the re-reads come
+// from L2, whose bandwidth to the SMs is about the HBM bandwidth, so the
+// one-window-per-tile schedule (window_gemm.cu) is bounded by ~(k_h/s_h) #L
+// of L2 traffic, not by #L.
+//
+// This kernel streams each 128-row tile of L ONCE along its columns and
+// lets every output row h take its window out of the stream:
+//   * a work item is (row tile, a chunk of H consecutive output rows); its
+//     stream is the column range [x0, (h_end - 1) shift + kdim) of the tile's
+//     L rows, read as 128-byte K-atoms by TMA into a shared-memory ring;
+//   * 4 copier warps move each atom from shared memory into a TMEM ring
+//     (tcgen05.st, row m -> TMEM lane m), so the MMAs take A from TMEM (the
+//     "TS" form).  A TMEM operand can start at any 16-byte column step, so
+//     row h's window is addressed at its exact offset o = h shift - x0 up to
+//     d = o mod (16 B / elt) elements; d is absorbed by the weight copy
+//     shifted down by d rows (Kt variant d / delta_step, mec_internal.h).
+//     All the variants needed (at most 16 B / gcd(shift elt, 16 B)) stay
+//     resident in shared memory;
+//   * one thread issues, when atom i has landed, every 32-byte K step of every
+//     open row whose last element falls in atom i (a step that straddles two
+//     atoms reads a TMEM guard copy of the next atom's first 16 bytes when the
+//     ring wraps); rows use a ring of TMEM accumulators, opened at their first
+//     step and committed to the epilogue at their last;
+//   * 8 epilogue warps (two groups, alternate rows) drain the accumulators
+//     row by row: tcgen05.ld -> bf16/fp32 -> swizzled smem -> TMA store of
+//     O[n, h, w, :] (n-h-w-c; Solution A's permutation, Alg.2 l.17-19, applied
+//     at store time) or of O_hnwc[h, n, w, :] (the paper's intermediate).
+// L2 -> SM traffic per item: (H - 1) shift + kdim columns instead of
+// H kdim.  Per row the arithmetic is the same K steps, in the same order, for
+// Solution A and B (so A == B bitwise, reading Q10).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+
+#include "mec_internal.h"
+#include "ptx.cuh"
+#include "tma_host.h"
+
+#ifdef MEC_TRACE
+// Debug-only per-atom timestamps (tools/trace_sweep.py, -DMEC_TRACE build):
+// [cta < 160][atom seq < 256][event < 8]
+__device__ unsigned long long* g_sweep_trace = nullptr;
+extern "C" int mec_sweep_trace_enable(void** dev_buf_out, size_t* bytes_out) {
+  const size_t bytes = static_cast<size_t>(160) * 256 * 8 * 8;
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, bytes) != cudaSuccess) return 1;
+  cudaMemset(buf, 0, bytes);
+  if (cudaMemcpyToSymbol(g_sweep_trace, &buf, sizeof(buf)) != cudaSuccess) return 2;
+  *dev_buf_out = buf;
+  *bytes_out = bytes;
+  return 0;
+}
+#define SW_TRACE(seq, ev)                                                                      \
+  do {                                                                                         \
+    if (sw_tr != nullptr && blockIdx.x < 160 && (seq) < 256) {                                 \
+      unsigned long long t_;                                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+      sw_tr[(static_cast<size_t>(blockIdx.x) * 256 + (seq)) * 8 + (ev)] = t_;                  \
+    }                                                                                          \
+  } while (0)
+#else
+#define SW_TRACE(seq, ev) \
+  do {                    \
+  } while (0)
+#endif
+
+namespace mec {
+namespace {
+
+constexpr int kSwCopyWarps = 4;
+constexpr int kSwEpiWarps = 8;
+constexpr int kSwFirstCopyWarp = 2;
+constexpr int kSwFirstEpiWarp = kSwFirstCopyWarp + kSwCopyWarps;
+// MMA issuer warps (rows dealt round-robin): 1, or 2 with the second at warp
+// kSwMma2Warp.  Two issuers only pay when the TMEM ring holds both issuers'
+// windows (span + shift atoms); measured deadlock-free but not faster with 11
+// slots, so one.
+constexpr int kSwIssuers = 1;
+constexpr int kSwMma2Warp = kSwFirstEpiWarp + kSwEpiWarps;
+constexpr int kSwThreads = 32 * (kSwMma2Warp + (kSwIssuers - 1));  // 448
+constexpr int kSwAtomBytes = kBM * kTileKBytes;                   // 16 KB: 128 rows x 128 B
+constexpr int kSwMaxRing = 16;
+constexpr int kSwMaxAcc = 8;
+constexpr int kSwGuardCols = 32;  // TMEM guard after the A ring: a copy of slot 0's atom
+
+struct SweepParams {
+  void* O;
+  int64_t o_h, o_w, i_n, k_c;
+  // row tiling, as in window_gemm.cu: flat (Solution A, o_w < 32: 128 folded
+  // rows n o_w + w per tile), packed (ipt images per tile in `slot`-row
+  // slots) or one image per tile (ipt = 1)
+  bool flat;
+  int ipt, slot;
+  int64_t rows, groups, n_mt;
+  int shift;       // s_h k_w i_c (elements)
+  int kdim;        // k_h k_w i_c
+  int bk;          // K-atom (elements per 128 B)
+  int bk_log2;
+  int kchunk_log2; // elements per 32-byte MMA K step: 16 bf16 / 8 tf32
+  int mvec;        // elements per 16 bytes (TMEM A operand column step)
+  int avec;        // TMA box-start alignment of x0 (elements)
+  int ds_log2;     // log2(delta_step): variant v = d / delta_step
+  int nb_atoms;    // B atoms per weight variant (kdim_pad / bk)
+  int n_vres;      // resident weight variants
+  int64_t kc_pad;
+  int bn;
+  int H;           // output rows per work item
+  int64_t n_hc, n_items;
+  int stages;      // shared-memory A stages (one atom each)
+  int ns;          // TMEM A ring slots (32 columns each)
+  int n_acc;       // TMEM accumulators (bn columns each)
+  uint32_t a_col0, guard_col;
+  uint32_t idesc;
+  int col_shift;   // TMEM column of element e within an atom: (e mod bk) >> col_shift... (bf16: 1, tf32: 0)
+  bool out_hnwc;
+  bool tma_store;
+  int pw, n_pass;
+  uint32_t stage_out_bytes;
+  uint32_t backoff_ns;  // copier / epilogue waits: nanosleep between probes (0: spin)
+  int dbg;  // (experiments, MEC_SWEEP_DBG) 1: no O stores, 2: no MMAs, 4: no TMEM stores of A
+};
+
+struct SwItem {
+  int64_t h0, mt, g;
+  int nrows;
+  int n_a;     // atoms streamed
+  int x0;      // stream start column (multiple of avec)
+  int off0;    // h0 shift - x0 (< avec)
+};
+
+__device__ __forceinline__ SwItem sw_decode(const SweepParams& p, int64_t t) {
+  SwItem it;
+  const int64_t hc = t % p.n_hc;
+  t /= p.n_hc;
+  it.mt = t % p.n_mt;
+  it.g = t / p.n_mt;
+  it.h0 = hc * p.H;
+  it.nrows = static_cast<int>(min(static_cast<int64_t>(p.H), p.o_h - it.h0));
+  const int64_t xs = it.h0 * p.shift;
+  it.x0 = static_cast<int>(xs - xs % p.avec);
+  it.off0 = static_cast<int>(xs - it.x0);
+  // the last row's last K step bounds the stream
+  const int o_last = it.off0 + (it.nrows - 1) * p.shift;
+  const int d_last = o_last & (p.mvec - 1);
+  const int kc = 1 << p.kchunk_log2;
+  const int nk_last = (p.kdim + d_last + kc - 1) >> p.kchunk_log2;
+  it.n_a = (o_last - d_last + nk_last * kc + p.bk - 1) / p.bk;
+  return it;
+}
+
+__device__ __forceinline__ uint32_t sw_pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Epilogue of one output row h of tile (mt, g): this warp's 32 TMEM lanes
+// (quarter) of accumulator columns taddr .. taddr + bn.  Same stores as the
+// one-window-per-tile kernel.
+template <bool kTF32>
+__device__ __forceinline__ void sw_store_row(const SweepParams& p, const CUtensorMap* tmO, int64_t h, int64_t mt,
+                                             int64_t g, int quarter, int lane, uint32_t taddr, uint32_t stg,
+                                             unsigned char* stg_gen) {
+  constexpr int kOutElt = kTF32 ? 4 : 2;
+  const int row_bytes = p.pw * kOutElt;
+  const int swz_shift = row_bytes == 128 ? 0 : (row_bytes == 64 ? 1 : 2);
+  const int swz_mask = row_bytes == 128 ? 7 : (row_bytes == 64 ? 3 : 1);
+  const uint32_t my_x = static_cast<uint32_t>((lane >> swz_shift) & swz_mask);
+  int64_t gr0, nvalid, n_img = 0, w0 = 0;
+  if (p.flat) {
+    const int64_t r0 = mt * kBM + quarter * 32;
+    nvalid = min(static_cast<int64_t>(32), p.rows - r0);
+    gr0 = r0;
+  } else {
+    const int j = (quarter * 32) / p.slot;
+    n_img = g * p.ipt + j;
+    w0 = mt * kBM + quarter * 32 - j * p.slot;
+    nvalid = (j < p.ipt && n_img < p.i_n) ? min(static_cast<int64_t>(32), p.o_w - w0) : 0;
+    gr0 = n_img * p.o_w + w0;
+  }
+  unsigned char* orow_own;
+  {
+    const int64_t gr = gr0 + lane;
+    int64_t out_row;
+    if (p.out_hnwc) {
+      out_row = h * (p.i_n * p.o_w) + gr;
+    } else {
+      const int64_t n = gr / p.o_w, w = gr - n * p.o_w;
+      out_row = (n * p.o_h + h) * p.o_w + w;
+    }
+    orow_own = static_cast<unsigned char*>(p.O) + out_row * p.k_c * kOutElt;
+  }
+  for (int pass = 0; pass < p.n_pass; ++pass) {
+    const int c0 = pass * p.pw;
+    uint32_t v16[4][16];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j * 16 < p.pw) ptx::tmem_ld_32x32b_x16(taddr + c0 + 16 * j, v16[j]);
+    ptx::tmem_ld_wait();
+    if (nvalid <= 0 || c0 >= p.k_c || (p.dbg & 1)) continue;  // warp-uniform
+    if (p.tma_store) {
+      const uint32_t my_row = stg + static_cast<uint32_t>(lane * row_bytes);
+      if (lane == 0) ptx::bulk_wait_group_read<0>();  // the previous store finished reading the box
+      __syncwarp();
+      const int nchunk = row_bytes / 16;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        if (ch >= nchunk) break;
+        uint32_t q0, q1, q2, q3;
+        if constexpr (kTF32) {
+          const int j = ch >> 2, e = (ch & 3) * 4;
+          q0 = v16[j][e];
+          q1 = v16[j][e + 1];
+          q2 = v16[j][e + 2];
+          q3 = v16[j][e + 3];
+        } else {
+          const int j = ch >> 1, e = (ch & 1) * 8;
+          q0 = sw_pack_bf16x2(__uint_as_float(v16[j][e]), __uint_as_float(v16[j][e + 1]));
+          q1 = sw_pack_bf16x2(__uint_as_float(v16[j][e + 2]), __uint_as_float(v16[j][e + 3]));
+          q2 = sw_pack_bf16x2(__uint_as_float(v16[j][e + 4]), __uint_as_float(v16[j][e + 5]));
+          q3 = sw_pack_bf16x2(__uint_as_float(v16[j][e + 6]), __uint_as_float(v16[j][e + 7]));
+        }
+        ptx::st_shared_v4(my_row + ((static_cast<uint32_t>(ch) ^ my_x) << 4), q0, q1, q2, q3);
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      const int32_t col = c0;
+      if (!p.flat) {
+        if (lane == 0) {
+          if (p.out_hnwc)  // O_hnwc as {k_c, o_w, i_n, o_h}
+            ptx::tma_store_4d(tmO, stg_gen, col, static_cast<int32_t>(w0), static_cast<int32_t>(n_img),
+                              static_cast<int32_t>(h));
+          else  // O as {k_c, o_w, o_h, i_n}
+            ptx::tma_store_4d(tmO, stg_gen, col, static_cast<int32_t>(w0), static_cast<int32_t>(h),
+                              static_cast<int32_t>(n_img));
+          ptx::bulk_commit_group();
+        }
+      } else if (p.out_hnwc) {
+        if (lane == 0) {
+          ptx::tma_store_3d(tmO, stg_gen, col, static_cast<int32_t>(gr0), static_cast<int32_t>(h));
+          ptx::bulk_commit_group();
+        }
+      } else {
+        // rows of the first image: one TMA store; rows of a later image in the
+        // 32-row block (TMA stores reject negative coordinates) by the warp
+        const int64_t n_first = gr0 / p.o_w;
+        const int k_first = static_cast<int>(min(nvalid, (n_first + 1) * p.o_w - gr0));
+        if (lane == 0) {
+          ptx::tma_store_4d(tmO, stg_gen, col, static_cast<int32_t>(gr0 - n_first * p.o_w),
+                            static_cast<int32_t>(h), static_cast<int32_t>(n_first));
+          ptx::bulk_commit_group();
+        }
+        if (k_first < nvalid) {
+          const int lg = nchunk == 8 ? 3 : (nchunk == 4 ? 2 : 1);
+          const int nrest = static_cast<int>(nvalid) - k_first;
+          const int total = nrest * nchunk;
+          for (int ci0 = 0; ci0 < total; ci0 += 32) {
+            const int ci = min(ci0 + lane, total - 1);
+            const int row = k_first + (ci >> lg), ch = ci & (nchunk - 1);
+            const unsigned long long base =
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(orow_own), row);
+            const uint32_t x = static_cast<uint32_t>((row >> swz_shift) & swz_mask);
+            const uint4 val =
+                ptx::ld_shared_v4(stg + static_cast<uint32_t>(row * row_bytes) + ((static_cast<uint32_t>(ch) ^ x) << 4));
+            if (ci0 + lane < total)
+              *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(base) + c0 * kOutElt + ch * 16) = val;
+          }
+        }
+      }
+    } else if (lane < nvalid) {
+      // k_c elt not a multiple of 16 (or of the pass width): element stores
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int col = c0 + j * 16 + e;
+          if (j * 16 + e < p.pw && col < p.k_c) {
+            if constexpr (kTF32) {
+              reinterpret_cast<uint32_t*>(orow_own)[col] = v16[j][e];
+            } else {
+              const uint32_t pkd = sw_pack_bf16x2(__uint_as_float(v16[j][e]), 0.0f);
+              reinterpret_cast<uint16_t*>(orow_own)[col] = static_cast<uint16_t>(pkd & 0xFFFFu);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <bool kTF32>
+__global__ void __launch_bounds__(kSwThreads, 1)
+    sweep_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmO, const SweepParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + kSmemAlign - 1) & ~uintptr_t(kSmemAlign - 1));
+  const int S = p.stages;
+  const uint32_t b_tile_bytes = static_cast<uint32_t>(p.bn) * kTileKBytes;
+  const int n_btiles = p.n_vres * p.nb_atoms;
+  unsigned char* smemA = smem;
+  unsigned char* smemB = smem + static_cast<size_t>(S) * kSwAtomBytes;
+  unsigned char* smemE = smemB + static_cast<size_t>(n_btiles) * b_tile_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smemE + static_cast<size_t>(kSwEpiWarps) * p.stage_out_bytes);
+  uint64_t* full = bars;                    // [S]  TMA -> copiers
+  uint64_t* empty = bars + 8;               // [S]  copiers -> TMA
+  uint64_t* afull = bars + 16;              // [ns] copiers -> MMA
+  uint64_t* aempty = bars + 32;             // [ns] MMA -> copiers
+  uint64_t* tfull = bars + 48;              // [n_acc] MMA -> epilogue
+  uint64_t* tempty = bars + 56;             // [n_acc] epilogue -> MMA
+  uint64_t* bfull = bars + 64;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 65);
+
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const int64_t t_begin = blockIdx.x, t_step = gridDim.x;
+#ifdef MEC_TRACE
+  unsigned long long* const sw_tr = g_sweep_trace;
+#endif
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmA);
+    ptx::tma_prefetch_desc(&tmB);
+    ptx::tma_prefetch_desc(&tmO);
+    for (int i = 0; i < S; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], kSwCopyWarps);
+    }
+    for (int i = 0; i < p.ns; ++i) {
+      ptx::mbar_init(&afull[i], kSwCopyWarps);
+      ptx::mbar_init(&aempty[i], kSwIssuers);  // every MMA issuer releases each atom
+    }
+    for (int i = 0; i < p.n_acc; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 4);  // the 4 warps of one epilogue group
+    }
+    ptx::mbar_init(bfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc_dyn(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  // broadcast from lane 0: provably warp-uniform, so the MMA warp keeps its
+  // operand addresses in uniform registers (no per-MMA R2UR loops)
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const uint64_t hintA = ptx::policy_evict_normal();
+      const uint64_t hintB = ptx::policy_evict_last();
+      ptx::griddep_wait();  // L and Kt come from the preceding (lowering) kernel
+      if (t_begin < p.n_items) {
+        ptx::mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(n_btiles) * b_tile_bytes);
+        for (int v = 0; v < p.n_vres; ++v)
+          for (int a = 0; a < p.nb_atoms; ++a)
+            ptx::tma_load_2d(smemB + static_cast<size_t>(v * p.nb_atoms + a) * b_tile_bytes, &tmB, bfull, a * p.bk,
+                             static_cast<int32_t>(v * p.kc_pad), hintB);
+      }
+      uint32_t pseq = 0;
+      for (int64_t t = t_begin; t < p.n_items; t += t_step) {
+        const SwItem it = sw_decode(p, t);
+        const int32_t y0 = static_cast<int32_t>(it.mt * kBM);
+        const int32_t z0 = static_cast<int32_t>(it.g);
+        for (int i = 0; i < it.n_a; ++i, ++pseq) {
+          const int stage = static_cast<int>(pseq % static_cast<uint32_t>(S));
+          ptx::mbar_wait(&empty[stage], ((pseq / S) & 1u) ^ 1u);
+          ptx::mbar_arrive_expect_tx(&full[stage], kSwAtomBytes);
+          unsigned char* dstA = smemA + static_cast<size_t>(stage) * kSwAtomBytes;
+          const int32_t x = it.x0 + i * p.bk;
+          if (p.ipt <= 1) {
+            ptx::tma_load_3d(dstA, &tmA, &full[stage], x, y0, z0, hintA);
+          } else {  // one box of `slot` rows per image of the tile (images >= i_n: zero fill)
+            for (int j = 0; j < p.ipt; ++j)
+              ptx::tma_load_3d(dstA + j * p.slot * kTileKBytes, &tmA, &full[stage], x, 0, z0 * p.ipt + j, hintA);
+          }
+          SW_TRACE(pseq, 0);
+        }
+      }
+    }
+  } else if (warp == 1 || (kSwIssuers > 1 && warp == kSwMma2Warp)) {
+    // ===================== MMA issuer(s) =====================
+    // Issuer mi takes the rows with global sequence number g = mi (mod
+    // kSwIssuers); row g accumulates into accumulator g mod 2.  A row's K
+    // steps (kdim + d elements in 32-byte steps) are issued back to back, 4
+    // per election, waiting for each atom as its steps need it; atoms before
+    // the row's first are released first (an atom's slot is refilled once
+    // every issuer released it).  Single-warp control code is latency-bound
+    // (DESIGN.md section 7), so per group of 4 steps the loop does two adds:
+    // consecutive groups are 32 TMEM columns apart (the ring wraps; a group
+    // across the wrap reads the guard) and one B atom apart.
+    const int mi = warp == 1 ? 0 : 1;
+    const uint64_t b_desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smemB));
+    const uint32_t b_tile16 = b_tile_bytes >> 4;
+    const uint32_t bvar16 = b_tile16 * static_cast<uint32_t>(p.nb_atoms);  // descriptor step per weight variant
+    const int kcl = p.kchunk_log2, cs = p.col_shift, bkl = p.bk_log2;
+    const int ns = p.ns, shift = p.shift, mmask = p.mvec - 1;
+    const int kdim_r = p.kdim + (1 << kcl) - 1;
+    const uint32_t ring0 = tmem_base + p.a_col0, ring_cols = static_cast<uint32_t>(32 * ns);
+    const bool no_mma = (p.dbg & 2) != 0;
+    if (t_begin < p.n_items) ptx::mbar_wait(bfull, 0);
+    int wslot = 0;          // ring slot of the next atom to wait for
+    uint32_t wphase = 0;
+    int rslot = 0;          // ring slot of the next atom to release
+    uint32_t q = 0;         // global sequence number of the item's row 0
+    uint32_t aseq = 0;      // atoms waited (traces only)
+    (void)aseq;
+    for (int64_t t = t_begin; t < p.n_items; t += t_step) {
+      const SwItem it = sw_decode(p, t);
+      const int slot0 = wslot;  // ring slot of the item's atom 0
+      int avail = 0;            // atoms of the item landed in TMEM
+      int released = 0;         // atoms of the item released by this issuer
+      auto wait_atom = [&]() {
+        ptx::mbar_wait(&afull[wslot], wphase);
+        if (lane == 0 && mi == 0) SW_TRACE(aseq, 4);
+        ++aseq;
+        if (++wslot == ns) {
+          wslot = 0;
+          wphase ^= 1u;
+        }
+        ++avail;
+      };
+      // release every atom before `upto` (an atom is waited for first, so a
+      // release never runs ahead of the fill it frees)
+      auto release_upto = [&](int upto) {
+        while (released < upto) {
+          if (released >= avail) {
+            wait_atom();
+            ptx::tc_fence_after();
+          }
+          ptx::mma_commit_elect(&aempty[rslot]);
+          if (++rslot == ns) rslot = 0;
+          ++released;
+        }
+      };
+      // first row of this issuer: g = q + r = mi (mod kSwIssuers)
+      int r = static_cast<int>((static_cast<uint32_t>(mi + kSwIssuers) - q % kSwIssuers) % kSwIssuers);
+      int o = it.off0 + r * shift;
+      for (; r < it.nrows; r += kSwIssuers, o += kSwIssuers * shift) {
+        const int d = o & mmask;
+        const int a = o - d;  // stream element of the row's first step
+        const int nk = (kdim_r + d) >> kcl;
+        release_upto(a >> bkl);  // atoms before this row's first: no later row of this issuer needs them
+        const uint32_t g = q + static_cast<uint32_t>(r);
+        const int acc = static_cast<int>(g & 1u);
+        ptx::mbar_wait(&tempty[acc], ((g >> 1) & 1u) ^ 1u);
+        ptx::tc_fence_after();
+        if (lane == 0 && mi == 0) SW_TRACE(static_cast<uint32_t>(r), 6);
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * p.bn);
+        // TMEM column of step 0: slot of atom a / bk, then the offset inside it
+        int s0 = slot0 + (a >> bkl);
+        while (s0 >= ns) s0 -= ns;
+        uint32_t col = ring0 + static_cast<uint32_t>(s0 * 32) + (static_cast<uint32_t>(a & ((1 << bkl) - 1)) >> cs);
+        const uint64_t bvar = b_desc0 + static_cast<uint32_t>(d >> p.ds_log2) * bvar16;
+        // issue the row's full groups in runs: every group whose atoms have
+        // landed goes in one call (a PTX loop, no per-group election); then
+        // wait for the next atom.  A group that runs past the ring end reads
+        // the guard (a copy of slot 0's atom).
+        const int n_full = nk >> 2;
+        const uint32_t b_lo0 = static_cast<uint32_t>(bvar);
+        int k4 = 0;  // groups issued
+        while (k4 < n_full) {
+          // groups whose last element lies in a landed atom
+          int ready = ((avail << bkl) - a) >> (kcl + 2);
+          if (ready > n_full) ready = n_full;
+          if (ready <= k4) {
+            wait_atom();
+            ptx::tc_fence_after();
+            continue;
+          }
+          const int ng = ready - k4;
+          if (!no_mma)
+            ptx::mma_ts_groups_elect<kTF32>(d_tmem, col, ring0 + ring_cols, ring_cols,
+                                            b_lo0 + static_cast<uint32_t>(k4) * b_tile16, b_tile16, p.idesc,
+                                            k4 != 0 ? 1u : 0u, ng);
+          col += static_cast<uint32_t>(ng * 32);
+          while (col >= ring0 + ring_cols) col -= ring_cols;
+          k4 = ready;
+        }
+        if (nk & 3) {  // tail group of nk mod 4 steps
+          const int need = (a + (nk << kcl) - 1) >> bkl;
+          if (avail <= need) {
+            do {
+              wait_atom();
+            } while (avail <= need);
+            ptx::tc_fence_after();
+          }
+          if (!no_mma)
+            ptx::mma_ts_grp_elect<kTF32>(d_tmem, col, bvar + static_cast<uint32_t>(n_full) * b_tile16, p.idesc,
+                                         n_full != 0 ? 1u : 0u, nk & 3);
+        }
+        ptx::mma_commit_elect(&tfull[acc]);
+
+        if (lane == 0 && mi == 0) SW_TRACE(static_cast<uint32_t>(r), 7);
+        __syncwarp();
+      }
+      release_upto(it.n_a);  // the item's remaining atoms
+      // every atom of the item was waited for by this issuer (release_upto)
+      q += static_cast<uint32_t>(it.nrows);
+    }
+  } else if (warp < kSwFirstEpiWarp) {
+    // ===================== copiers: smem atom -> TMEM ring =====================
+    const int quarter = warp & 3;
+    const int m = 32 * quarter + lane;  // tile row = TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>(32 * quarter) << 16;
+    const uint32_t a_smem = ptx::smem_u32(smemA) + static_cast<uint32_t>(m * kTileKBytes);
+    const uint32_t sw = static_cast<uint32_t>(m & 7);
+    uint32_t cseq = 0;
+    for (int64_t t = t_begin; t < p.n_items; t += t_step) {
+      const SwItem it = sw_decode(p, t);
+      for (int i = 0; i < it.n_a; ++i, ++cseq) {
+        const int stage = static_cast<int>(cseq % static_cast<uint32_t>(S));
+        const int slot = static_cast<int>(cseq % static_cast<uint32_t>(p.ns));
+        if (p.backoff_ns) ptx::mbar_wait_backoff(&full[stage], (cseq / S) & 1u, p.backoff_ns);
+        else ptx::mbar_wait(&full[stage], (cseq / S) & 1u);
+        if (warp == kSwFirstCopyWarp && lane == 0) SW_TRACE(cseq, 1);
+        uint32_t r[32];
+        const uint32_t src = a_smem + static_cast<uint32_t>(stage * kSwAtomBytes);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // 128-byte swizzle: 16-byte chunk c of row m at c ^ (m mod 8)
+          const uint4 x = ptx::ld_shared_v4(src + ((static_cast<uint32_t>(c) ^ sw) << 4));
+          r[4 * c] = x.x;
+          r[4 * c + 1] = x.y;
+          r[4 * c + 2] = x.z;
+          r[4 * c + 3] = x.w;
+        }
+        if (p.backoff_ns) ptx::mbar_wait_backoff(&aempty[slot], ((cseq / p.ns) & 1u) ^ 1u, p.backoff_ns);
+        else ptx::mbar_wait(&aempty[slot], ((cseq / p.ns) & 1u) ^ 1u);
+        ptx::tc_fence_after();
+        if (warp == kSwFirstCopyWarp && lane == 0) SW_TRACE(cseq, 2);
+        if (!(p.dbg & 4)) ptx::tmem_st_32x32b_x32(tmem_base + lane_base + p.a_col0 + static_cast<uint32_t>(slot * 32), r);
+        if (slot == 0 && !(p.dbg & 4))  // guard: a K group running past the ring end reads it
+          ptx::tmem_st_32x32b_x32(tmem_base + lane_base + p.guard_col, r);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&empty[stage]);
+          ptx::mbar_arrive(&afull[slot]);
+        }
+        if (warp == kSwFirstCopyWarp && lane == 0) SW_TRACE(cseq, 3);
+      }
+    }
+  } else {
+    // ===================== epilogue (two groups of 4 warps, alternate rows) =====================
+    const int quarter = warp & 3;
+    const int group = (warp - kSwFirstEpiWarp) >> 2;
+    unsigned char* const stg_gen = smemE + static_cast<size_t>(warp - kSwFirstEpiWarp) * p.stage_out_bytes;
+    const uint32_t stg = ptx::smem_u32(stg_gen);
+    const uint32_t lane_base = static_cast<uint32_t>(32 * quarter) << 16;
+    uint32_t q = 0;
+    for (int64_t t = t_begin; t < p.n_items; t += t_step) {
+      const SwItem it = sw_decode(p, t);
+      for (int r = 0; r < it.nrows; ++r) {
+        const uint32_t qr = q + static_cast<uint32_t>(r);
+        if (static_cast<int>(qr & 1u) != group) continue;
+        const int acc = static_cast<int>(qr % static_cast<uint32_t>(p.n_acc));
+        if (p.backoff_ns) ptx::mbar_wait_backoff(&tfull[acc], (qr / p.n_acc) & 1u, p.backoff_ns);
+        else ptx::mbar_wait(&tfull[acc], (qr / p.n_acc) & 1u);
+        ptx::tc_fence_after();
+        sw_store_row<kTF32>(p, &tmO, it.h0 + r, it.mt, it.g, quarter, lane,
+                            tmem_base + lane_base + static_cast<uint32_t>(acc * p.bn), stg, stg_gen);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      }
+      q += static_cast<uint32_t>(it.nrows);
+    }
+    if (lane == 0) ptx::bulk_wait_group<0>();
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, 512);
+  }
+}
+
+constexpr size_t kSwSmemBudget = 222 * 1024;
+
+int ilog2(int x) {
+  int l = 0;
+  while ((1 << l) < x) ++l;
+  return l;
+}
+
+}  // namespace
+
+// The sweep's resources for plan pl, or false when it does not apply (then
+// the one-window-per-tile kernel runs).
+bool sweep_config(const Plan& pl, bool batch_folded, int* n_vres_out, int* n_acc_out, int* ns_out,
+                  int* stages_out) {
+  if (getenv("MEC_SWEEP") && atoi(getenv("MEC_SWEEP")) == 0) return false;
+  if (pl.n_tiles_n != 1 || pl.o_h < 2 || pl.shift >= pl.kdim) return false;  // no window overlap: nothing to share
+  if (pl.l_cols > (1LL << 30) || pl.o_h * pl.shift > (1LL << 30)) return false;
+  const int mvec = 16 / pl.elt;
+  int64_t g = pl.shift % mvec, b = mvec;
+  while (g) { const int64_t t = b % g; b = g; g = t; }
+  const int n_vres = static_cast<int>(mvec / b);  // variants d = (h shift) mod mvec, multiples of gcd(shift, mvec)
+  if (n_vres > pl.n_var) return false;
+  if (n_vres > 1 && pl.delta_step != b) return false;
+  const int kc = 32 / pl.elt;
+  // TMEM: n_acc accumulators (rows in flight between MMA and epilogue) and a
+  // ring of ns atoms that holds one row's whole window (span atoms) plus
+  // look-ahead, and the guard
+  // (worst case over the window's start inside an atom and over d)
+  int span = 0;
+  for (int phi = 0; phi < pl.bk; phi += mvec)
+    for (int d = 0; d < mvec; d += static_cast<int>(b)) {
+      const int64_t nk = (pl.kdim + d + kc - 1) / kc;
+      span = std::max<int>(span, static_cast<int>((phi + nk * kc - 1) / pl.bk) + 1);
+    }
+  // one accumulator per MMA issuer
+  const int n_acc = 2;
+  const int ns = std::min(kSwMaxRing, (512 - kSwGuardCols - ((2 * pl.bn + 31) / 32) * 32) / 32);
+  if (ns < span) return false;
+  int row_bytes = 128;
+  while (row_bytes > 32 && (pl.bn * pl.elt) % row_bytes != 0) row_bytes /= 2;
+  const size_t epi = static_cast<size_t>(kSwEpiWarps) * 32 * row_bytes;
+  const size_t b_res = static_cast<size_t>(n_vres) * (pl.kdim_pad / pl.bk) * pl.bn * kTileKBytes;
+  const size_t fixed = b_res + epi + 66 * 8 + 64;
+  if (fixed + 2 * kSwAtomBytes > kSwSmemBudget) return false;
+  const int stages = static_cast<int>(std::min<size_t>(8, (kSwSmemBudget - fixed) / kSwAtomBytes));
+  (void)batch_folded;
+  *n_vres_out = n_vres;
+  *n_acc_out = n_acc;
+  *ns_out = ns;
+  *stages_out = stages;
+  return true;
+}
+
+cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st, int* launches) {
+  int n_vres, n_acc, ns, stages;
+  if (a.fused || !sweep_config(pl, a.batch_folded, &n_vres, &n_acc, &ns, &stages)) return cudaErrorNotSupported;
+  const bool tf32 = pl.dt == MEC_DTYPE_TF32;
+  const int out_elt = pl.elt;
+  CUtensorMap tmA, tmB, tmO;
+  // row tiling: as window_gemm.cu
+  const bool flat = a.batch_folded && pl.o_w < 32;
+  int slot = 128, ipt = 1;
+  if (!flat && pl.o_w <= 128) {
+    slot = static_cast<int>((pl.o_w + 31) / 32 * 32);
+    if (a.batch_folded) ipt = std::max(1, 128 / slot);
+    if (ipt == 1) slot = 128;
+  }
+  const int64_t rows = flat ? pl.s.i_n * pl.o_w : pl.o_w;
+  const int64_t groups = flat ? 1 : (pl.s.i_n + ipt - 1) / ipt;
+  const int64_t n_mt = flat ? (rows + kBM - 1) / kBM : (ipt > 1 ? 1 : (pl.o_w + kBM - 1) / kBM);
+  {  // A: L as {columns, rows, groups} (flat: one group of i_n o_w rows)
+    const uint64_t dims[3] = {static_cast<uint64_t>(pl.l_cols), static_cast<uint64_t>(rows),
+                              static_cast<uint64_t>(flat ? 1 : pl.s.i_n)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(pl.pitch) * pl.elt,
+                                 static_cast<uint64_t>(pl.pitch) * pl.elt * rows};
+    const uint32_t box[3] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(ipt > 1 ? slot : kBM), 1};
+    cudaError_t e = encode_tiled(&tmA, tf32, 3, a.L, dims, strides, box);
+    if (e != cudaSuccess) return e;
+  }
+  {  // B: Kt, n_var x kc_pad rows of kdim_pad (K-major)
+    const uint64_t dims[2] = {static_cast<uint64_t>(pl.kdim_pad), static_cast<uint64_t>(pl.n_var * pl.kc_pad)};
+    const uint64_t strides[1] = {static_cast<uint64_t>(pl.kdim_pad) * pl.elt};
+    const uint32_t box[2] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(pl.bn)};
+    cudaError_t e = encode_tiled(&tmB, tf32, 2, a.Kt, dims, strides, box);
+    if (e != cudaSuccess) return e;
+  }
+  SweepParams p{};
+  p.O = a.O;
+  p.o_h = pl.o_h;
+  p.o_w = pl.o_w;
+  p.i_n = pl.s.i_n;
+  p.k_c = pl.s.k_c;
+  p.flat = flat;
+  p.ipt = ipt;
+  p.slot = slot;
+  p.rows = rows;
+  p.groups = groups;
+  p.n_mt = n_mt;
+  p.shift = static_cast<int>(pl.shift);
+  p.kdim = static_cast<int>(pl.kdim);
+  p.bk = pl.bk;
+  p.bk_log2 = ilog2(pl.bk);
+  p.kchunk_log2 = pl.elt == 2 ? 4 : 3;
+  p.mvec = 16 / pl.elt;
+  p.avec = pl.avec;
+  p.ds_log2 = ilog2(pl.delta_step);
+  p.nb_atoms = static_cast<int>(pl.kdim_pad / pl.bk);
+  p.n_vres = n_vres;
+  p.kc_pad = pl.kc_pad;
+  p.bn = pl.bn;
+  p.stages = stages;
+  p.ns = ns;
+  p.n_acc = n_acc;
+  p.a_col0 = static_cast<uint32_t>(((n_acc * pl.bn + 31) / 32) * 32);
+  p.guard_col = p.a_col0 + static_cast<uint32_t>(32 * ns);
+  p.idesc = ptx::instr_desc(tf32, kBM, pl.bn);
+  p.col_shift = pl.elt == 2 ? 1 : 0;
+  p.out_hnwc = a.out_hnwc;
+  p.dbg = getenv("MEC_SWEEP_DBG") ? atoi(getenv("MEC_SWEEP_DBG")) : 0;
+  p.backoff_ns = getenv("MEC_SWEEP_BACKOFF") ? static_cast<uint32_t>(atoi(getenv("MEC_SWEEP_BACKOFF"))) : 0u;
+  // epilogue: pass width = 128 / 64 / 32 bytes per row, dividing bn
+  int row_bytes = 128;
+  while (row_bytes > 32 && (pl.bn * out_elt) % row_bytes != 0) row_bytes /= 2;
+  p.pw = row_bytes / out_elt;
+  p.n_pass = pl.bn / p.pw;
+  p.tma_store = ((pl.s.k_c * out_elt) % 16 == 0) && (reinterpret_cast<uintptr_t>(a.O) % 16 == 0) &&
+                pl.s.k_c % p.pw == 0;
+  p.stage_out_bytes = static_cast<uint32_t>(32 * row_bytes);
+  if (p.tma_store) {
+    cudaError_t e;
+    if (a.out_hnwc && flat) {  // O_hnwc as {k_c, i_n o_w, o_h}
+      const uint64_t dims[3] = {static_cast<uint64_t>(pl.s.k_c), static_cast<uint64_t>(pl.s.i_n * pl.o_w),
+                                static_cast<uint64_t>(pl.o_h)};
+      const uint64_t strides[2] = {static_cast<uint64_t>(pl.s.k_c) * out_elt,
+                                   static_cast<uint64_t>(pl.s.i_n * pl.o_w * pl.s.k_c) * out_elt};
+      const uint32_t box[3] = {static_cast<uint32_t>(p.pw), 32, 1};
+      e = encode_tiled_swz(&tmO, tf32, 3, a.O, dims, strides, box, row_bytes);
+    } else if (a.out_hnwc) {  // O_hnwc as {k_c, o_w, i_n, o_h}
+      const uint64_t dims[4] = {static_cast<uint64_t>(pl.s.k_c), static_cast<uint64_t>(pl.o_w),
+                                static_cast<uint64_t>(pl.s.i_n), static_cast<uint64_t>(pl.o_h)};
+      const uint64_t strides[3] = {static_cast<uint64_t>(pl.s.k_c) * out_elt,
+                                   static_cast<uint64_t>(pl.o_w * pl.s.k_c) * out_elt,
+                                   static_cast<uint64_t>(pl.s.i_n * pl.o_w * pl.s.k_c) * out_elt};
+      const uint32_t box[4] = {static_cast<uint32_t>(p.pw), 32, 1, 1};
+      e = encode_tiled_swz(&tmO, tf32, 4, a.O, dims, strides, box, row_bytes);
+    } else {  // O as {k_c, o_w, o_h, i_n}
+      const uint64_t dims[4] = {static_cast<uint64_t>(pl.s.k_c), static_cast<uint64_t>(pl.o_w),
+                                static_cast<uint64_t>(pl.o_h), static_cast<uint64_t>(pl.s.i_n)};
+      const uint64_t strides[3] = {static_cast<uint64_t>(pl.s.k_c) * out_elt,
+                                   static_cast<uint64_t>(pl.o_w * pl.s.k_c) * out_elt,
+                                   static_cast<uint64_t>(pl.o_h * pl.o_w * pl.s.k_c) * out_elt};
+      const uint32_t box[4] = {static_cast<uint32_t>(p.pw), 32, 1, 1};
+      e = encode_tiled_swz(&tmO, tf32, 4, a.O, dims, strides, box, row_bytes);
+    }
+    if (e != cudaSuccess) return e;
+  } else {
+    std::memset(&tmO, 0, sizeof(tmO));
+  }
+
+  // h-chunk size H: minimise (waves) x (bytes one item moves: its stream of
+  // atoms, its O rows and a fixed pipeline fill), ties to fewer items
+  const int64_t tiles = n_mt * groups;
+  const int sms = num_sms();
+  const double o_row_bytes = static_cast<double>(kBM) * pl.bn * out_elt;
+  double best = 1e300;
+  int64_t best_H = pl.o_h;
+  for (int64_t n_hc = 1; n_hc <= pl.o_h; ++n_hc) {
+    const int64_t H = (pl.o_h + n_hc - 1) / n_hc;
+    if (n_hc > 1 && (pl.o_h + H - 1) / H != n_hc) continue;
+    const int64_t items = n_hc * tiles;
+    const int64_t waves = (items + sms - 1) / sms;
+    const double atoms = static_cast<double>((H - 1) * pl.shift + pl.kdim + pl.avec) / pl.bk + 1.0;
+    const double cost = static_cast<double>(waves) * (atoms * kSwAtomBytes + H * o_row_bytes + 4.0 * kSwAtomBytes);
+    if (cost < best * 0.999) {
+      best = cost;
+      best_H = H;
+    }
+  }
+  if (const char* e = getenv("MEC_SWEEP_H")) best_H = std::max<int64_t>(1, std::min<int64_t>(pl.o_h, atoi(e)));
+  p.H = static_cast<int>(best_H);
+  p.n_hc = (pl.o_h + best_H - 1) / best_H;
+  p.n_items = p.n_hc * tiles;
+
+  const size_t b_res = static_cast<size_t>(n_vres) * p.nb_atoms * pl.bn * kTileKBytes;
+  const size_t smem = kSmemAlign + static_cast<size_t>(stages) * kSwAtomBytes + b_res +
+                      static_cast<size_t>(kSwEpiWarps) * p.stage_out_bytes + 66 * 8 + 16;
+  if (smem > kSwSmemBudget + kSmemAlign + 2048) return cudaErrorInvalidConfiguration;
+  const int64_t grid = std::min<int64_t>(p.n_items, sms);
+  auto kern = tf32 ? sweep_gemm_kernel<true> : sweep_gemm_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kSwThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = getenv("MEC_NO_PDL") ? 0 : 1;
+  e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmO, p);
+  if (e != cudaSuccess) return e;
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace mec
