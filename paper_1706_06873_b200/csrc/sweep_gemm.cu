@@ -53,7 +53,7 @@
 // [cta < 160][atom seq < 256][event < 8]
 __device__ unsigned long long* g_sweep_trace = nullptr;
 extern "C" int mec_sweep_trace_enable(void** dev_buf_out, size_t* bytes_out) {
-  const size_t bytes = static_cast<size_t>(160) * 256 * 8 * 8;
+  const size_t bytes = static_cast<size_t>(160) * 512 * 8 * 8;
   void* buf = nullptr;
   if (cudaMalloc(&buf, bytes) != cudaSuccess) return 1;
   cudaMemset(buf, 0, bytes);
@@ -67,7 +67,7 @@ extern "C" int mec_sweep_trace_enable(void** dev_buf_out, size_t* bytes_out) {
     if (sw_tr != nullptr && blockIdx.x < 160 && (seq) < 256) {                                 \
       unsigned long long t_;                                                                   \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
-      sw_tr[(static_cast<size_t>(blockIdx.x) * 256 + (seq)) * 8 + (ev)] = t_;                  \
+      sw_tr[(static_cast<size_t>(blockIdx.x) * 512 + (seq)) * 8 + (ev)] = t_;                  \
     }                                                                                          \
   } while (0)
 #else
@@ -316,7 +316,11 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   uint64_t* full = bars;                    // [S]  TMA -> copiers
   uint64_t* empty = bars + 8;               // [S]  copiers -> TMA
   uint64_t* afull = bars + 16;              // [ns] copiers -> MMA
-  uint64_t* aempty = bars + 32;             // [ns] MMA -> copiers
+  // rows completed, per epilogue group (even / odd global row numbers):
+  // epilogue -> copiers.  A slot is refilled once the last row that reads its
+  // atom has completed; monotonic counters instead of per-slot barriers keep
+  // the MMA warp at one tcgen05.commit per row (a commit costs ~500 cycles)
+  uint32_t* rows_done = reinterpret_cast<uint32_t*>(bars + 32);
   uint64_t* tfull = bars + 48;              // [n_acc] MMA -> epilogue
   uint64_t* tempty = bars + 56;             // [n_acc] epilogue -> MMA
   uint64_t* bfull = bars + 64;
@@ -337,10 +341,9 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], kSwCopyWarps);
     }
-    for (int i = 0; i < p.ns; ++i) {
-      ptx::mbar_init(&afull[i], kSwCopyWarps);
-      ptx::mbar_init(&aempty[i], kSwIssuers);  // every MMA issuer releases each atom
-    }
+    for (int i = 0; i < p.ns; ++i) ptx::mbar_init(&afull[i], kSwCopyWarps);
+    rows_done[0] = 0;
+    rows_done[1] = 0;
     for (int i = 0; i < p.n_acc; ++i) {
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], 4);  // the 4 warps of one epilogue group
@@ -413,37 +416,32 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     if (t_begin < p.n_items) ptx::mbar_wait(bfull, 0);
     int wslot = 0;          // ring slot of the next atom to wait for
     uint32_t wphase = 0;
-    int rslot = 0;          // ring slot of the next atom to release
     uint32_t q = 0;         // global sequence number of the item's row 0
     uint32_t aseq = 0;      // atoms waited (traces only)
     (void)aseq;
+#ifdef MEC_TRACE
+    long long cyc_wait = 0, cyc_issue = 0, cyc_tempty = 0, cyc_row0 = 0;
+#endif
     for (int64_t t = t_begin; t < p.n_items; t += t_step) {
       const SwItem it = sw_decode(p, t);
       const int slot0 = wslot;  // ring slot of the item's atom 0
       int avail = 0;            // atoms of the item landed in TMEM
       int released = 0;         // atoms of the item released by this issuer
       auto wait_atom = [&]() {
+#ifdef MEC_TRACE
+        const long long cw0 = clock64();
+#endif
         ptx::mbar_wait(&afull[wslot], wphase);
-        if (lane == 0 && mi == 0) SW_TRACE(aseq, 4);
+#ifdef MEC_TRACE
+        cyc_wait += clock64() - cw0;
+#endif
+        if (lane == 0 && mi == 0 && !(p.dbg & 16)) SW_TRACE(aseq, 4);
         ++aseq;
         if (++wslot == ns) {
           wslot = 0;
           wphase ^= 1u;
         }
         ++avail;
-      };
-      // release every atom before `upto` (an atom is waited for first, so a
-      // release never runs ahead of the fill it frees)
-      auto release_upto = [&](int upto) {
-        while (released < upto) {
-          if (released >= avail) {
-            wait_atom();
-            ptx::tc_fence_after();
-          }
-          ptx::mma_commit_elect(&aempty[rslot]);
-          if (++rslot == ns) rslot = 0;
-          ++released;
-        }
       };
       // first row of this issuer: g = q + r = mi (mod kSwIssuers)
       int r = static_cast<int>((static_cast<uint32_t>(mi + kSwIssuers) - q % kSwIssuers) % kSwIssuers);
@@ -452,12 +450,19 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         const int d = o & mmask;
         const int a = o - d;  // stream element of the row's first step
         const int nk = (kdim_r + d) >> kcl;
-        release_upto(a >> bkl);  // atoms before this row's first: no later row of this issuer needs them
         const uint32_t g = q + static_cast<uint32_t>(r);
         const int acc = static_cast<int>(g & 1u);
+#ifdef MEC_TRACE
+        cyc_wait = 0;
+        cyc_issue = 0;
+        cyc_row0 = clock64();
+#endif
         ptx::mbar_wait(&tempty[acc], ((g >> 1) & 1u) ^ 1u);
+#ifdef MEC_TRACE
+        cyc_tempty = clock64() - cyc_row0;
+#endif
         ptx::tc_fence_after();
-        if (lane == 0 && mi == 0) SW_TRACE(static_cast<uint32_t>(r), 6);
+        if (lane == 0 && mi == 0 && !(p.dbg & 16)) SW_TRACE(static_cast<uint32_t>(r), 6);
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * p.bn);
         // TMEM column of step 0: slot of atom a / bk, then the offset inside it
         int s0 = slot0 + (a >> bkl);
@@ -471,20 +476,38 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         const int n_full = nk >> 2;
         const uint32_t b_lo0 = static_cast<uint32_t>(bvar);
         int k4 = 0;  // groups issued
+#ifdef MEC_TRACE
+        int n_runs = 0;
+        long long cyc_fence = 0;
+        const long long cyc_setup = clock64() - cyc_row0 - cyc_tempty;
+#endif
         while (k4 < n_full) {
           // groups whose last element lies in a landed atom
           int ready = ((avail << bkl) - a) >> (kcl + 2);
           if (ready > n_full) ready = n_full;
           if (ready <= k4) {
             wait_atom();
+#ifdef MEC_TRACE
+            const long long cf0 = clock64();
+#endif
             ptx::tc_fence_after();
+#ifdef MEC_TRACE
+            cyc_fence += clock64() - cf0;
+#endif
             continue;
           }
           const int ng = ready - k4;
+#ifdef MEC_TRACE
+          const long long ci0 = clock64();
+          ++n_runs;
+#endif
           if (!no_mma)
             ptx::mma_ts_groups_elect<kTF32>(d_tmem, col, ring0 + ring_cols, ring_cols,
                                             b_lo0 + static_cast<uint32_t>(k4) * b_tile16, b_tile16, p.idesc,
                                             k4 != 0 ? 1u : 0u, ng);
+#ifdef MEC_TRACE
+          cyc_issue += clock64() - ci0;
+#endif
           col += static_cast<uint32_t>(ng * 32);
           while (col >= ring0 + ring_cols) col -= ring_cols;
           k4 = ready;
@@ -501,13 +524,30 @@ __global__ void __launch_bounds__(kSwThreads, 1)
             ptx::mma_ts_grp_elect<kTF32>(d_tmem, col, bvar + static_cast<uint32_t>(n_full) * b_tile16, p.idesc,
                                          n_full != 0 ? 1u : 0u, nk & 3);
         }
+#ifdef MEC_TRACE
+        const long long cc0 = clock64();
+#endif
         ptx::mma_commit_elect(&tfull[acc]);
-
-        if (lane == 0 && mi == 0) SW_TRACE(static_cast<uint32_t>(r), 7);
+#ifdef MEC_TRACE
+        const long long cyc_commit = clock64() - cc0;
+#endif
+        if (lane == 0 && mi == 0 && !(p.dbg & 16)) SW_TRACE(static_cast<uint32_t>(r), 7);
+#ifdef MEC_TRACE
+        if (lane == 0 && sw_tr != nullptr && blockIdx.x < 160 && r < 256) {
+          unsigned long long* e = sw_tr + (static_cast<size_t>(blockIdx.x) * 512 + 256 + r) * 8;
+          e[0] = static_cast<unsigned long long>(cyc_tempty) + 1;
+          e[1] = static_cast<unsigned long long>(cyc_wait) + 1;
+          e[2] = static_cast<unsigned long long>(cyc_issue) + 1;
+          e[3] = static_cast<unsigned long long>(clock64() - cyc_row0) + 1;
+          e[4] = static_cast<unsigned long long>(cyc_commit) + 1;
+          e[5] = static_cast<unsigned long long>(n_runs) + 1;
+          e[6] = static_cast<unsigned long long>(cyc_setup) + 1;
+          e[7] = static_cast<unsigned long long>(cyc_fence) + 1;
+        }
+#endif
         __syncwarp();
       }
-      release_upto(it.n_a);  // the item's remaining atoms
-      // every atom of the item was waited for by this issuer (release_upto)
+      while (avail < it.n_a) wait_atom();  // (atoms no row of this issuer needed)
       q += static_cast<uint32_t>(it.nrows);
     }
   } else if (warp < kSwFirstEpiWarp) {
@@ -518,8 +558,10 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     const uint32_t a_smem = ptx::smem_u32(smemA) + static_cast<uint32_t>(m * kTileKBytes);
     const uint32_t sw = static_cast<uint32_t>(m & 7);
     uint32_t cseq = 0;
+    uint32_t q = 0;  // global number of the item's row 0
     for (int64_t t = t_begin; t < p.n_items; t += t_step) {
       const SwItem it = sw_decode(p, t);
+      const uint32_t jstart = cseq;  // the item's atom 0
       for (int i = 0; i < it.n_a; ++i, ++cseq) {
         const int stage = static_cast<int>(cseq % static_cast<uint32_t>(S));
         const int slot = static_cast<int>(cseq % static_cast<uint32_t>(p.ns));
@@ -536,8 +578,25 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           r[4 * c + 2] = x.z;
           r[4 * c + 3] = x.w;
         }
-        if (p.backoff_ns) ptx::mbar_wait_backoff(&aempty[slot], ((cseq / p.ns) & 1u) ^ 1u, p.backoff_ns);
-        else ptx::mbar_wait(&aempty[slot], ((cseq / p.ns) & 1u) ^ 1u);
+        if (cseq >= static_cast<uint32_t>(p.ns)) {
+          // the slot's previous atom J = cseq - ns is free once the last row
+          // reading it completed: in this item row r_max = the last row whose
+          // window starts at or before atom J; an atom of an earlier item is
+          // free once that item's last row completed
+          const uint32_t J = cseq - static_cast<uint32_t>(p.ns);
+          uint32_t g_free;
+          if (J >= jstart) {
+            const int jj = static_cast<int>(J - jstart);
+            const int rm = min(it.nrows - 1, (((jj + 1) << p.bk_log2) - 1 - it.off0) / p.shift);
+            g_free = q + static_cast<uint32_t>(rm);
+          } else {
+            g_free = q - 1u;
+          }
+          const uint32_t want = (g_free >> 1) + 1u;
+          while (ptx::ld_acquire_shared_u32(ptx::smem_u32(&rows_done[g_free & 1u])) < want) {
+            if (p.backoff_ns) __nanosleep(p.backoff_ns);
+          }
+        }
         ptx::tc_fence_after();
         if (warp == kSwFirstCopyWarp && lane == 0) SW_TRACE(cseq, 2);
         if (!(p.dbg & 4)) ptx::tmem_st_32x32b_x32(tmem_base + lane_base + p.a_col0 + static_cast<uint32_t>(slot * 32), r);
@@ -552,6 +611,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         }
         if (warp == kSwFirstCopyWarp && lane == 0) SW_TRACE(cseq, 3);
       }
+      q += static_cast<uint32_t>(it.nrows);
     }
   } else {
     // ===================== epilogue (two groups of 4 warps, alternate rows) =====================
@@ -570,6 +630,9 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         if (p.backoff_ns) ptx::mbar_wait_backoff(&tfull[acc], (qr / p.n_acc) & 1u, p.backoff_ns);
         else ptx::mbar_wait(&tfull[acc], (qr / p.n_acc) & 1u);
         ptx::tc_fence_after();
+        // row qr's MMAs are complete: its A atoms may be overwritten
+        if (lane == 0 && ((warp - kSwFirstEpiWarp) & 3) == 0)
+          ptx::st_release_shared_u32(ptx::smem_u32(&rows_done[group]), (qr >> 1) + 1u);
         sw_store_row<kTF32>(p, &tmO, it.h0 + r, it.mt, it.g, quarter, lane,
                             tmem_base + lane_base + static_cast<uint32_t>(acc * p.bn), stg, stg_gen);
         ptx::tc_fence_before();

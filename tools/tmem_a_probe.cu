@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(128, 1) probe(float* out_mma, uint32_t* out_cp
   __syncthreads();
   ptx::tc_fence_after();
   // timing: 2048 TS MMAs N=96 at A column 256 + 8k (aligned) vs 256 + 2 + 8k
-  for (int t = 0; t < 2 && mode >= 2; ++t) {
+  for (int t = 0; t < 2 && (mode == 2 || mode == 3); ++t) {
     if (mode == 2 && t == 1) break;
     if (mode == 3 && t == 0) continue;
     if (warp == 0) {
@@ -146,6 +146,28 @@ __global__ void __launch_bounds__(128, 1) probe(float* out_mma, uint32_t* out_cp
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+  }
+  // sweep-like pattern: rows of 36 TS MMAs (9 groups of 4) alternating two
+  // accumulators of N = the_off columns, A at 8-column steps in cols 256..
+  if (mode == 5 || mode == 6) {
+    if (warp == 0) {
+      const uint32_t n = static_cast<uint32_t>(the_off);
+      const uint32_t idesc = ptx::instr_desc(false, 128, n);
+      const long long t0 = clock64();
+      for (int r = 0; r < 64; ++r) {
+        const uint32_t d = tmem + static_cast<uint32_t>((r & 1) * n);
+        for (int g = 0; g < 9; ++g) {
+          const uint32_t col = tmem + 256 + static_cast<uint32_t>(((r * 3 + g) % 7) * 32 + (mode == 6 ? 8 : 0));
+          ptx::mma_ts_atom_elect<false>(d, col, bdesc, idesc, g != 0 ? 1u : 0u);
+        }
+      }
+      ptx::mma_commit_elect(&bar);
+      ptx::mbar_wait(&bar, ph);
+      if (lane == 0) cyc[0] = clock64() - t0;
+    } else {
+      ptx::mbar_wait(&bar, ph);
+    }
+    ph ^= 1;
   }
   // tcgen05.cp throughput: 1024 copies of 128x256b (4 KB each)
   if (mode == 4 && warp == 0) {
@@ -237,6 +259,7 @@ int main(int argc, char** argv) {
   printf("MMA on cp'd A at column offset 2: %s (%d wrong)\n", bad ? "MISMATCH" : "exact", bad);
   }
 timing:
+  if (mode == 5 || mode == 6) printf("sweep-like TS rows N=%d (%s): %.1f cyc/MMA\n", the_off, mode == 5 ? "aligned" : "col+8", cyc[0] / (64.0 * 36));
   if (mode == 2 || mode == 3) printf("TS MMA N=96 (%s): %.1f cyc/MMA\n", mode == 2 ? "aligned" : "col+2", cyc[mode - 2] / 2048.0);
   if (mode == 4)
   printf("tcgen05.cp 128x256b: %.1f cyc each (4 KB)\n", cyc[2] / 1024.0);

@@ -28,12 +28,14 @@ mec.conv_forward(I, K, cfg["s_h"], cfg["s_w"], path=path); torch.cuda.synchroniz
 host = np.zeros(nbytes.value // 8, dtype=np.uint64)
 L.mec_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
 assert L.mec_trace_read(host.ctypes.data, buf, nbytes) == 0
-tr = host.reshape(160, 256, 8).astype(np.int64)
+tr = host.reshape(160, 512, 8).astype(np.int64)
+tr_rows = tr[:, 256:, :]
 if os.environ.get("SW_CYCLES"):
-    c = np.where(tr[:, 0, 6] > 0)[0]
-    rows = tr[c][:, 1:40, :4] - 1
+    c = np.where(tr[:, 257, 3] > 0)[0]
+    rows = tr[c][:, 257:296, :8] - 1
+    print("raw", tr[c[0], 256:259, :4].tolist(), "ctas", len(c))
     rows = rows[(rows >= 0).all(axis=2)]
-    print("per-row cycles (median): afull waits %d  MMA asm %d  tfull commit %d  row body %d" % tuple(np.median(rows, axis=0)))
+    print("per-row cycles (median): tempty wait %d  afull waits %d  MMA issue calls %d  row total %d  commit %d  runs %d  setup %d  fences %d" % tuple(np.median(rows, axis=0)))
     sys.exit(0)
 ctas = np.where(tr[:, 0, 0] > 0)[0]
 t0 = tr[ctas, 0, 0].min()
