@@ -83,13 +83,12 @@ constexpr int kSwCopyWarps = 4;
 constexpr int kSwEpiWarps = 8;
 constexpr int kSwFirstCopyWarp = 2;
 constexpr int kSwFirstEpiWarp = kSwFirstCopyWarp + kSwCopyWarps;
-// MMA issuer warps (rows dealt round-robin): 1, or 2 with the second at warp
-// kSwMma2Warp.  Two issuers only pay when the TMEM ring holds both issuers'
-// windows (span + shift atoms); measured deadlock-free but not faster with 11
-// slots, so one.
-constexpr int kSwIssuers = 1;
+// MMA issuer warps (rows dealt round-robin, p.n_iss = 1 or 2; the second is
+// warp kSwMma2Warp): a second issuer overlaps one row's per-row control code
+// with the other's MMAs (single-warp issue is latency-bound).
+constexpr int kSwMaxIssuers = 2;
 constexpr int kSwMma2Warp = kSwFirstEpiWarp + kSwEpiWarps;
-constexpr int kSwThreads = 32 * (kSwMma2Warp + (kSwIssuers - 1));  // 448
+constexpr int kSwThreads = 32 * (kSwMma2Warp + 1);  // 480
 constexpr int kSwAtomBytes = kBM * kTileKBytes;                   // 16 KB: 128 rows x 128 B
 constexpr int kSwMaxRing = 16;
 constexpr int kSwMaxAcc = 8;
@@ -129,6 +128,7 @@ struct SweepParams {
   int pw, n_pass;
   uint32_t stage_out_bytes;
   uint32_t backoff_ns;  // copier / epilogue waits: nanosleep between probes (0: spin)
+  int n_iss;  // MMA issuer warps (1 or 2)
   int dbg;  // (experiments, MEC_SWEEP_DBG) 1: no O stores, 2: no MMAs, 4: no TMEM stores of A
 };
 
@@ -393,10 +393,10 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         }
       }
     }
-  } else if (warp == 1 || (kSwIssuers > 1 && warp == kSwMma2Warp)) {
+  } else if (warp == 1 || (warp == kSwMma2Warp && p.n_iss > 1)) {
     // ===================== MMA issuer(s) =====================
     // Issuer mi takes the rows with global sequence number g = mi (mod
-    // kSwIssuers); row g accumulates into accumulator g mod 2.  A row's K
+    // p.n_iss); row g accumulates into accumulator g mod 2.  A row's K
     // steps (kdim + d elements in 32-byte steps) are issued back to back, 4
     // per election, waiting for each atom as its steps need it; atoms before
     // the row's first are released first (an atom's slot is refilled once
@@ -443,13 +443,27 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         }
         ++avail;
       };
-      // first row of this issuer: g = q + r = mi (mod kSwIssuers)
-      int r = static_cast<int>((static_cast<uint32_t>(mi + kSwIssuers) - q % kSwIssuers) % kSwIssuers);
+      // advance the ring position over atoms this issuer does not read,
+      // without waiting for them (a wait could see their slot refilled twice)
+      auto skip_to = [&](int upto) {
+        while (avail < upto) {
+          if (++wslot == ns) {
+            wslot = 0;
+            wphase ^= 1u;
+          }
+          ++avail;
+          ++aseq;
+        }
+      };
+      // first row of this issuer: g = q + r = mi (mod n_iss)
+      const int n_iss = p.n_iss;
+      int r = static_cast<int>((static_cast<uint32_t>(mi + n_iss) - q % n_iss) % n_iss);
       int o = it.off0 + r * shift;
-      for (; r < it.nrows; r += kSwIssuers, o += kSwIssuers * shift) {
+      for (; r < it.nrows; r += n_iss, o += n_iss * shift) {
         const int d = o & mmask;
         const int a = o - d;  // stream element of the row's first step
         const int nk = (kdim_r + d) >> kcl;
+        skip_to(a >> bkl);  // atoms before this row's window
         const uint32_t g = q + static_cast<uint32_t>(r);
         const int acc = static_cast<int>(g & 1u);
 #ifdef MEC_TRACE
@@ -547,9 +561,11 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 #endif
         __syncwarp();
       }
-      while (avail < it.n_a) wait_atom();  // (atoms no row of this issuer needed)
+      skip_to(it.n_a);  // atoms no row of this issuer needs: never waited for
       q += static_cast<uint32_t>(it.nrows);
     }
+  } else if (warp == kSwMma2Warp) {
+    // (second issuer not used for this problem)
   } else if (warp < kSwFirstEpiWarp) {
     // ===================== copiers: smem atom -> TMEM ring =====================
     const int quarter = warp & 3;
@@ -592,9 +608,18 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           } else {
             g_free = q - 1u;
           }
+          // rows of one parity complete in order (one accumulator, one
+          // issuer per parity when two issue): rows g_free and g_free - 1
+          // cover every earlier row of both parities
           const uint32_t want = (g_free >> 1) + 1u;
           while (ptx::ld_acquire_shared_u32(ptx::smem_u32(&rows_done[g_free & 1u])) < want) {
             if (p.backoff_ns) __nanosleep(p.backoff_ns);
+          }
+          if (g_free > 0) {
+            const uint32_t g2 = g_free - 1u, want2 = (g2 >> 1) + 1u;
+            while (ptx::ld_acquire_shared_u32(ptx::smem_u32(&rows_done[g2 & 1u])) < want2) {
+              if (p.backoff_ns) __nanosleep(p.backoff_ns);
+            }
           }
         }
         ptx::tc_fence_after();
@@ -771,6 +796,12 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   p.col_shift = pl.elt == 2 ? 1 : 0;
   p.out_hnwc = a.out_hnwc;
   p.dbg = getenv("MEC_SWEEP_DBG") ? atoi(getenv("MEC_SWEEP_DBG")) : 0;
+  // two issuers need every atom read by both issuers' rows (windows of rows
+  // h and h + 2 overlap), else an issuer could lag a slot by two fills
+  // (measured: 2 issuers win with one weight variant -- C2 434->397 us, C3
+  // 127->117 us -- and lose ~8% on the shifted-variant layers, C1 / cv1 / cv3)
+  p.n_iss = (2 * pl.shift < pl.kdim && n_vres == 1) ? 2 : 1;
+  if (const char* e = getenv("MEC_SWEEP_ISSUERS")) p.n_iss = std::max(1, std::min(p.n_iss, atoi(e)));
   p.backoff_ns = getenv("MEC_SWEEP_BACKOFF") ? static_cast<uint32_t>(atoi(getenv("MEC_SWEEP_BACKOFF"))) : 0u;
   // epilogue: pass width = 128 / 64 / 32 bytes per row, dividing bn
   int row_bytes = 128;
