@@ -87,8 +87,12 @@ typedef struct {
   int path;       /* mec_path_t; MEC_PATH_AUTO by default */
   int T;          /* threshold of Alg.2 l.8; <= 0 means MEC_DEFAULT_T */
   int sola_fix;   /* mec_sola_fix_t; used only when Solution A runs */
-  int rows_per_tile; /* output rows h per GEMM tile (multi-row schedule: the union of
-                        their overlapping windows of L is streamed once); 0 = auto (1) */
+  int rows_per_tile; /* 0 = auto: the h-sweep window GEMM where it applies (each
+                        128-row tile of L streamed once per chunk of output rows,
+                        DESIGN.md 6.2b), else the one-window-per-tile kernel with its
+                        automatic rows per tile.  >= 1: force the one-window-per-tile
+                        kernel with this many output rows h per tile (the union of
+                        their overlapping windows of L is streamed once). */
   void* workspace;        /* device buffer >= mec_workspace_bytes(); NULL = stream-ordered pool */
   size_t workspace_bytes;
   /* Optional cudaEvent_t handles recorded on `stream` at stage boundaries

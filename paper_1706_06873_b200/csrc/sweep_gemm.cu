@@ -64,7 +64,7 @@ extern "C" int mec_sweep_trace_enable(void** dev_buf_out, size_t* bytes_out) {
 }
 #define SW_TRACE(seq, ev)                                                                      \
   do {                                                                                         \
-    if (sw_tr != nullptr && blockIdx.x < 160 && (seq) < 256) {                                 \
+    if (sw_tr != nullptr && blockIdx.x < 160 && (seq) < 512) {                                 \
       unsigned long long t_;                                                                   \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
       sw_tr[(static_cast<size_t>(blockIdx.x) * 512 + (seq)) * 8 + (ev)] = t_;                  \
@@ -115,7 +115,7 @@ struct SweepParams {
   int n_vres;      // resident weight variants
   int64_t kc_pad;
   int bn;
-  int H;           // output rows per work item
+  int H;           // output rows of the largest work item (chunks differ by <= 1 row)
   int64_t n_hc, n_items;
   int stages;      // shared-memory A stages (one atom each)
   int ns;          // TMEM A ring slots (32 columns each)
@@ -146,8 +146,9 @@ __device__ __forceinline__ SwItem sw_decode(const SweepParams& p, int64_t t) {
   t /= p.n_hc;
   it.mt = t % p.n_mt;
   it.g = t / p.n_mt;
-  it.h0 = hc * p.H;
-  it.nrows = static_cast<int>(min(static_cast<int64_t>(p.H), p.o_h - it.h0));
+  // chunk hc: rows [hc o_h / n_hc, (hc + 1) o_h / n_hc) (sizes differ by <= 1)
+  it.h0 = hc * p.o_h / p.n_hc;
+  it.nrows = static_cast<int>((hc + 1) * p.o_h / p.n_hc - it.h0);
   const int64_t xs = it.h0 * p.shift;
   it.x0 = static_cast<int>(xs - xs % p.avec);
   it.off0 = static_cast<int>(xs - it.x0);
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   unsigned long long* const sw_tr = g_sweep_trace;
 #endif
 
+  if (threadIdx.x == 0) SW_TRACE(511u, 0);
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
@@ -358,6 +360,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   // broadcast from lane 0: provably warp-uniform, so the MMA warp keeps its
   // operand addresses in uniform registers (no per-MMA R2UR loops)
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  if (threadIdx.x == 0) SW_TRACE(511u, 1);
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -372,6 +375,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
             ptx::tma_load_2d(smemB + static_cast<size_t>(v * p.nb_atoms + a) * b_tile_bytes, &tmB, bfull, a * p.bk,
                              static_cast<int32_t>(v * p.kc_pad), hintB);
       }
+      SW_TRACE(511u, 2);
       uint32_t pseq = 0;
       for (int64_t t = t_begin; t < p.n_items; t += t_step) {
         const SwItem it = sw_decode(p, t);
@@ -414,6 +418,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     const uint32_t ring0 = tmem_base + p.a_col0, ring_cols = static_cast<uint32_t>(32 * ns);
     const bool no_mma = (p.dbg & 2) != 0;
     if (t_begin < p.n_items) ptx::mbar_wait(bfull, 0);
+    if (lane == 0 && mi == 0) SW_TRACE(511u, 3);
     int wslot = 0;          // ring slot of the next atom to wait for
     uint32_t wphase = 0;
     uint32_t q = 0;         // global sequence number of the item's row 0
@@ -667,10 +672,12 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       q += static_cast<uint32_t>(it.nrows);
     }
     if (lane == 0) ptx::bulk_wait_group<0>();
+    if (lane == 0 && warp == kSwFirstEpiWarp) SW_TRACE(511u, 4);
   }
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) SW_TRACE(511u, 5);
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, 512);
@@ -849,9 +856,9 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   const double o_row_bytes = static_cast<double>(kBM) * pl.bn * out_elt;
   double best = 1e300;
   int64_t best_H = pl.o_h;
+  int64_t best_n = 1;
   for (int64_t n_hc = 1; n_hc <= pl.o_h; ++n_hc) {
-    const int64_t H = (pl.o_h + n_hc - 1) / n_hc;
-    if (n_hc > 1 && (pl.o_h + H - 1) / H != n_hc) continue;
+    const int64_t H = (pl.o_h + n_hc - 1) / n_hc;  // the largest chunk
     const int64_t items = n_hc * tiles;
     const int64_t waves = (items + sms - 1) / sms;
     const double atoms = static_cast<double>((H - 1) * pl.shift + pl.kdim + pl.avec) / pl.bk + 1.0;
@@ -859,11 +866,15 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
     if (cost < best * 0.999) {
       best = cost;
       best_H = H;
+      best_n = n_hc;
     }
   }
-  if (const char* e = getenv("MEC_SWEEP_H")) best_H = std::max<int64_t>(1, std::min<int64_t>(pl.o_h, atoi(e)));
+  if (const char* e = getenv("MEC_SWEEP_H")) {
+    best_H = std::max<int64_t>(1, std::min<int64_t>(pl.o_h, atoi(e)));
+    best_n = (pl.o_h + best_H - 1) / best_H;
+  }
   p.H = static_cast<int>(best_H);
-  p.n_hc = (pl.o_h + best_H - 1) / best_H;
+  p.n_hc = best_n;
   p.n_items = p.n_hc * tiles;
 
   const size_t b_res = static_cast<size_t>(n_vres) * p.nb_atoms * pl.bn * kTileKBytes;

@@ -1,13 +1,17 @@
 #!/bin/bash
-# Round evidence: GPU parity tests, the default bench line, the reference arm,
-# the ncu launch list of the same command and one full capture of the
-# dominant kernels.
+# Round evidence: GPU parity tests, smoke, the default bench line, the
+# reference arm, other configs, the ncu launch list of the default command and
+# one full capture of the dominant kernels.  Every step under its own timeout.
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv > gpurun_out/smi.csv
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
-timeout 400 python bench.py > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
-timeout 400 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 400 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 200 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+timeout 300 python bench.py > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
+timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+B="timeout 120 python bench.py --no-cpu-baseline --no-e2e --steps 20"
+: > gpurun_out/bench_cfgs.json
+for c in C2 C2_tf32 C3; do $B --config $c >> gpurun_out/bench_cfgs.json 2>> gpurun_out/bench_cfgs.err; done
+for c in cv1 cv2 cv3 cv4 cv5 cv6 cv7 cv8 cv9 cv10 cv11 cv12; do $B --config C4_$c --batch 128 --no-fused-alt >> gpurun_out/bench_cfgs.json 2>> gpurun_out/bench_cfgs.err; done
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c1.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"window_gemm|lower_kernel" -s 6 -c 3 -o gpurun_out/prof_c1 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-fused-alt > gpurun_out/ncu_full.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"sweep_gemm|window_gemm|lower_kernel" -s 6 -c 3 -o gpurun_out/prof_c1 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-fused-alt > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out

@@ -32,10 +32,11 @@ KEYS = [
 
 
 def short(name):
-    for k in ("lower_kernel", "window_gemm_kernel", "copy16_kernel", "block_permute_kernel", "flush_kernel",
+    for k in ("lower_kernel", "window_gemm_kernel", "sweep_gemm_kernel", "copy16_kernel", "block_permute_kernel", "flush_kernel",
               "synth_kernel", "fused"):
         if k in name:
             return {"lower_kernel": "mec_lower", "window_gemm_kernel": "window_gemm",
+                    "sweep_gemm_kernel": "window_gemm",  # the window GEMM stage (h-sweep kernel)
                     "copy16_kernel": "sola_copy", "block_permute_kernel": "sola_transpose"}.get(k, k)
     return name[:40]
 

@@ -39,6 +39,13 @@ if os.environ.get("SW_CYCLES"):
     sys.exit(0)
 ctas = np.where(tr[:, 0, 0] > 0)[0]
 t0 = tr[ctas, 0, 0].min()
+life = tr[ctas, 511, :6]
+ent = life[:, 0].min()
+print("CTA lifetime (us after the first CTA entry), pct 0/50/100:")
+for k, n in enumerate(["entry", "prologue done", "weights issued", "weights landed", "epilogue drained", "exit"]):
+    v = (life[:, k] - ent) / 1e3
+    print("  %-17s %7.2f %7.2f %7.2f" % (n, np.percentile(v, 0), np.percentile(v, 50), np.percentile(v, 100)))
+print("  first A TMA issue %7.2f" % ((t0 - ent) / 1e3))
 names = ["P_issued", "C_full", "C_aempty", "C_arrived", "M_afull", "M_released"]
 print("ctas", len(ctas))
 def med(e1, e2):
