@@ -170,9 +170,12 @@ __device__ __forceinline__ uint32_t sw_pack_bf16x2(float lo, float hi) {
 // (quarter) of accumulator columns taddr .. taddr + bn.  Same stores as the
 // one-window-per-tile kernel.
 template <bool kTF32>
+// The accumulator is released (tempty arrive) as soon as the last pass's
+// tcgen05.ld has completed, before the conversion and the stores, so the
+// next row that uses it can start accumulating while this one is stored.
 __device__ __forceinline__ void sw_store_row(const SweepParams& p, const CUtensorMap* tmO, int64_t h, int64_t mt,
                                              int64_t g, int quarter, int lane, uint32_t taddr, uint32_t stg,
-                                             unsigned char* stg_gen) {
+                                             unsigned char* stg_gen, uint64_t* tempty_bar) {
   constexpr int kOutElt = kTF32 ? 4 : 2;
   const int row_bytes = p.pw * kOutElt;
   const int swz_shift = row_bytes == 128 ? 0 : (row_bytes == 64 ? 1 : 2);
@@ -209,6 +212,11 @@ __device__ __forceinline__ void sw_store_row(const SweepParams& p, const CUtenso
     for (int j = 0; j < 4; ++j)
       if (j * 16 < p.pw) ptx::tmem_ld_32x32b_x16(taddr + c0 + 16 * j, v16[j]);
     ptx::tmem_ld_wait();
+    if (pass == p.n_pass - 1) {
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(tempty_bar);
+    }
     if (nvalid <= 0 || c0 >= p.k_c || (p.dbg & 1)) continue;  // warp-uniform
     if (p.tma_store) {
       const uint32_t my_row = stg + static_cast<uint32_t>(lane * row_bytes);
@@ -664,10 +672,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         if (lane == 0 && ((warp - kSwFirstEpiWarp) & 3) == 0)
           ptx::st_release_shared_u32(ptx::smem_u32(&rows_done[group]), (qr >> 1) + 1u);
         sw_store_row<kTF32>(p, &tmO, it.h0 + r, it.mt, it.g, quarter, lane,
-                            tmem_base + lane_base + static_cast<uint32_t>(acc * p.bn), stg, stg_gen);
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                            tmem_base + lane_base + static_cast<uint32_t>(acc * p.bn), stg, stg_gen, &tempty[acc]);
       }
       q += static_cast<uint32_t>(it.nrows);
     }
