@@ -509,20 +509,17 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         const long long cyc_setup = clock64() - cyc_row0 - cyc_tempty;
 #endif
         while (k4 < n_full) {
-          // groups whose last element lies in a landed atom
+          // wait for every atom up to the one holding group k4's last element
+          // (a tight wait loop), then issue every group whose atoms landed
+          const int need = (a + ((k4 + 1) << (kcl + 2)) - 1) >> bkl;
+          if (avail <= need) {
+            do {
+              wait_atom();
+            } while (avail <= need);
+            ptx::tc_fence_after();
+          }
           int ready = ((avail << bkl) - a) >> (kcl + 2);
           if (ready > n_full) ready = n_full;
-          if (ready <= k4) {
-            wait_atom();
-#ifdef MEC_TRACE
-            const long long cf0 = clock64();
-#endif
-            ptx::tc_fence_after();
-#ifdef MEC_TRACE
-            cyc_fence += clock64() - cf0;
-#endif
-            continue;
-          }
           const int ng = ready - k4;
 #ifdef MEC_TRACE
           const long long ci0 = clock64();
@@ -536,7 +533,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           cyc_issue += clock64() - ci0;
 #endif
           col += static_cast<uint32_t>(ng * 32);
-          while (col >= ring0 + ring_cols) col -= ring_cols;
+          if (col >= ring0 + ring_cols) col -= ring_cols;  // ng * 32 < ring_cols: one wrap at most
           k4 = ready;
         }
         if (nk & 3) {  // tail group of nk mod 4 steps
