@@ -109,7 +109,8 @@ typedef struct {
    * the padded extents; O is i_n x o_h x o_w x k_c of the padded problem.
    * Not supported by the fused gather variant (MEC_ERR_UNSUPPORTED). */
   int pad_h, pad_w;
-  int reserved1;
+  int selected_gemm; /* OUT: the window-GEMM kernel that ran: 1 = one window per tile
+                        (DESIGN.md 6.2), 2 = h-sweep with A in TMEM (6.2b), 0 = none */
 } mec_options_t;
 
 /* Fills *opt with defaults (AUTO path, T = 100, epilogue fix, pool workspace). */

@@ -65,7 +65,7 @@ class MecOptions(ctypes.Structure):
         ("selected_path", ctypes.c_int),
         ("pad_h", ctypes.c_int),
         ("pad_w", ctypes.c_int),
-        ("reserved1", ctypes.c_int),
+        ("selected_gemm", ctypes.c_int),
     ]
 
 

@@ -440,8 +440,12 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
     // rows_per_tile 0 (auto): the h-sweep where it applies; 1 or more: the
     // one-window-per-tile kernel (R output rows per tile)
     e = cudaErrorNotSupported;
+    opt->selected_gemm = 2;
     if (opt->rows_per_tile == 0 && !ga.fused) e = mec::launch_sweep_gemm(pc, ga, stream_, &launches);
-    if (e == cudaErrorNotSupported) e = mec::launch_window_gemm(pc, ga, stream_, &launches);
+    if (e == cudaErrorNotSupported) {
+      opt->selected_gemm = 1;
+      e = mec::launch_window_gemm(pc, ga, stream_, &launches);
+    }
     if (e != cudaSuccess) goto fail;
   }
   rec(2);

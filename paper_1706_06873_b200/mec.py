@@ -123,10 +123,12 @@ def lower_pitched(I: torch.Tensor, k_h: int, k_w: int, s_h: int, s_w: int, pitch
 def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torch.Tensor | None = None,
                  path: int = MEC_PATH_AUTO, T: int = MEC_DEFAULT_T, sola_fix: int = MEC_SOLA_FIX_EPILOGUE,
                  workspace: torch.Tensor | None = None, stage_events=None, return_path: bool = False,
-                 rows_per_tile: int = 0, pad_h: int = 0, pad_w: int = 0):
+                 rows_per_tile: int = 0, pad_h: int = 0, pad_w: int = 0, return_gemm: bool = False):
     """mec_conv_forward_ex: O = MEC(I, K, s) (Algorithm 2), O in n-h-w-c
     (or h-n-w-c with sola_fix=MEC_SOLA_FIX_NONE when Solution A runs).  pad_h / pad_w:
-    zero padding applied virtually inside the lowering (never materialised)."""
+    zero padding applied virtually inside the lowering (never materialised).
+    return_path / return_gemm: also return the path that ran (1 = A, 2 = B, 3 = fused)
+    / the window-GEMM kernel that ran (1 = one window per tile, 2 = h-sweep)."""
     _cuda(I, "I")
     _cuda(K, "K")
     if K.dtype != I.dtype:
@@ -156,7 +158,8 @@ def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torc
                                         ctypes.byref(_shape(i_n, i_h, i_w, i_c, k_h, k_w, k_c)),
                                         s_h, s_w, dtype_code(I.dtype), _stream(I), ctypes.byref(opt))
     _lib.check(st, "mec_conv_forward")
-    return (out, opt.selected_path) if return_path else out
+    extra = ([opt.selected_path] if return_path else []) + ([opt.selected_gemm] if return_gemm else [])
+    return (out, *extra) if extra else out
 
 
 def maxpool(X: torch.Tensor, p_h: int, p_w: int, s_h: int, s_w: int, hnwc: bool = False,

@@ -544,3 +544,54 @@ def test_maxpool_consumes_hnwc(cuda_ok, case, dtype):
                                   _maxpool_ref(O_nhwc.float().cpu().numpy(), pk, pk, ps, ps))
     ref = _maxpool_ref(oracle.direct_conv(I, K, s, s, n_threads=8), pk, pk, ps, ps)
     check_O(Y_n, ref, dtype, i_c * k_h * k_w)
+
+
+# The h-sweep window GEMM against the oracle and against the
+# one-window-per-tile kernel: shapes with 1, 2, 4 and 8 shifted weight variants,
+# one and two MMA issuers, packed / flat (o_w < 32) Solution A tiles and
+# Solution B with two M tiles per image (o_w > 128).
+SWEEP_CASES = [
+    ((2, 227, 227, 3, 11, 11, 96), 4),   # AlexNet conv1: 2 variants, 1 issuer
+    ((2, 224, 224, 3, 7, 7, 64), 2),     # cv3: 4 variants
+    ((2, 64, 64, 3, 3, 3, 64), 1),       # cv7-like: 8 variants, many rows per atom
+    ((3, 56, 56, 64, 3, 3, 64), 1),      # cv9: 1 variant, 2 issuers
+    ((4, 20, 20, 64, 3, 3, 64), 1),      # o_w = 18: flat Solution A tiles
+    ((2, 140, 140, 64, 3, 3, 64), 1),    # o_w = 138: two M tiles per image
+    ((2, 30, 30, 32, 5, 5, 48), 2),      # k_c = 48, stride 2
+]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("case", range(len(SWEEP_CASES)))
+def test_sweep_gemm_vs_oracle_and_one_window(cuda_ok, case, dtype):
+    shape, s = SWEEP_CASES[case]
+    I, K = make_inputs(shape, dtype, seed=6100 + case)
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    kdim = shape[4] * shape[5] * shape[3]
+    outs = {}
+    for path in (MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B):
+        try:
+            O, g = mec.conv_forward(Id, Kd, s, s, path=path, return_gemm=True)
+        except MecError:  # (Solution A infeasible when #O > #L)
+            continue
+        O1, g1 = mec.conv_forward(Id, Kd, s, s, path=path, rows_per_tile=1, return_gemm=True)
+        torch.cuda.synchronize()
+        assert g1 == 1
+        check_O(O, ref, dtype, kdim)
+        check_O(O1, ref, dtype, kdim)
+        outs[path] = (O, g)
+    assert outs, "no path ran"
+    gs = {g for _, g in outs.values()}
+    assert len(gs) == 1
+    if len(outs) == 2:  # Solutions A and B: the same K steps per row -> bitwise equal (reading Q10)
+        assert torch.equal(outs[MEC_PATH_SOLUTION_A][0], outs[MEC_PATH_SOLUTION_B][0])
+
+
+def test_sweep_gemm_selected_for_C1_C2_C3(cuda_ok):
+    """The configs the bench times run the h-sweep kernel (bf16)."""
+    for shape, s in [((1, 227, 227, 3, 11, 11, 96), 4), ((1, 224, 224, 64, 3, 3, 64), 1),
+                     ((2, 56, 56, 64, 3, 3, 64), 1)]:
+        I, K = make_inputs(shape, "bf16", seed=6200)
+        _, g = mec.conv_forward(to_dev(I, "bf16"), to_dev(K, "bf16"), s, s, return_gemm=True)
+        assert g == 2, shape
