@@ -807,10 +807,12 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   p.dbg = getenv("MEC_SWEEP_DBG") ? atoi(getenv("MEC_SWEEP_DBG")) : 0;
   // two issuers need every atom read by both issuers' rows (windows of rows
   // h and h + 2 overlap), else an issuer could lag a slot by two fills
-  // (measured: 2 issuers win with one weight variant -- C2 434->397 us, C3
-  // 127->117 us -- and lose ~8% on the shifted-variant layers, C1 / cv1 / cv3)
-  p.n_iss = (2 * pl.shift < pl.kdim && n_vres == 1) ? 2 : 1;
-  if (const char* e = getenv("MEC_SWEEP_ISSUERS")) p.n_iss = std::max(1, std::min(p.n_iss, atoi(e)));
+  // (measured: 2 issuers win where the accumulators are 64 columns -- C2
+  // 434->397 us, C3 127->117 us, cv3 106->95 us, cv7 255->250 us -- and lose
+  // ~4-7% at k_c = 96, C1 / cv1, whose TMEM ring has 2 slots fewer)
+  p.n_iss = (2 * pl.shift < pl.kdim && pl.bn <= 64) ? 2 : 1;
+  if (const char* e = getenv("MEC_SWEEP_ISSUERS"))  // (experiments; 2 needs 2 shift < kdim)
+    p.n_iss = (atoi(e) >= 2 && 2 * pl.shift < pl.kdim) ? 2 : 1;
   p.backoff_ns = getenv("MEC_SWEEP_BACKOFF") ? static_cast<uint32_t>(atoi(getenv("MEC_SWEEP_BACKOFF"))) : 0u;
   // epilogue: pass width = 128 / 64 / 32 bytes per row, dividing bn
   int row_bytes = 128;
