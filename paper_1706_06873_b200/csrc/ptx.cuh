@@ -550,6 +550,69 @@ __device__ __forceinline__ void mma_ts_groups_elect(uint32_t tmem_d, uint32_t a_
 #undef MEC_TS_LOOP_BODY
 }
 
+// Whole-warp call: one elected lane issues a whole row of n_groups (>= 1)
+// 128-byte K groups of TS MMAs (as mma_ts_groups_elect), waiting inside the
+// same PTX loop for every A atom a group needs: group g ends at stream element
+// a + ((g + 1) << grp_log2) - 1, held by atom >> bkl; atoms are waited in
+// ring order on the mbarriers afull_base + 8 slot (phase parity wphase),
+// starting from ring slot wslot with `avail` atoms already landed.  The
+// caller advances its own copy of (wslot, wphase, avail) past the last atom
+// the row needs (the elected lane's counters are not returned).  One call per
+// row: no per-group or per-run control code in the warp (latency-bound).
+template <bool kTF32>
+__device__ __forceinline__ void mma_ts_row_elect(uint32_t tmem_d, uint32_t a_tmem, uint32_t ring_end,
+                                                 uint32_t ring_cols, uint32_t b_lo, uint32_t b_step,
+                                                 uint32_t idesc, int n_groups, int a, int grp_log2, int bkl,
+                                                 uint32_t afull_base, int wslot, uint32_t wphase, int avail,
+                                                 int ns) {
+#define MEC_TS_ROW_BODY(KIND)                                                                          \
+  asm volatile(                                                                                        \
+      "{\n\t.reg .pred e, p, w, more, ok, fin;\n\t"                                                    \
+      ".reg .b32 c, b, g, a1, a2, a3, l1, l2, l3, hi, need, t, ws, wp, av, bar;\n\t"                    \
+      ".reg .b64 b0, b1, b2, b3;\n\t"                                                                  \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                                \
+      "@!e bra DONE_%=;\n\t"                                                                           \
+      "mov.b32 hi, 0x40004040;\n\t"                                                                    \
+      "mov.b32 c, %1;\n\tmov.b32 b, %4;\n\tmov.b32 g, 0;\n\t"                                           \
+      "mov.b32 ws, %12;\n\tmov.b32 wp, %13;\n\tmov.b32 av, %14;\n\t"                                     \
+      "setp.ne.b32 p, 0, 0;\n"                                                                         \
+      "LOOP_%=:\n\t"                                                                                   \
+      "add.u32 t, g, 1;\n\tshl.b32 t, t, %10;\n\tadd.u32 t, t, %9;\n\tsub.u32 t, t, 1;\n\t"               \
+      "shr.s32 need, t, %11;\n"                                                                        \
+      "WAIT_%=:\n\t"                                                                                   \
+      "setp.gt.s32 ok, av, need;\n\t@ok bra READY_%=;\n\t"                                              \
+      "mad.lo.u32 bar, ws, 8, %15;\n"                                                                  \
+      "SPIN_%=:\n\t"                                                                                   \
+      "mbarrier.try_wait.parity.shared::cta.b64 w, [bar], wp;\n\t"                                     \
+      "@!w bra SPIN_%=;\n\t"                                                                           \
+      "add.u32 ws, ws, 1;\n\tsetp.eq.u32 fin, ws, %16;\n\t@fin mov.b32 ws, 0;\n\t@fin xor.b32 wp, wp, 1;\n\t" \
+      "add.u32 av, av, 1;\n\tbra WAIT_%=;\n"                                                            \
+      "READY_%=:\n\t"                                                                                  \
+      "tcgen05.fence::after_thread_sync;\n\t"                                                          \
+      "add.u32 a1, c, 8;\n\tadd.u32 a2, c, 16;\n\tadd.u32 a3, c, 24;\n\t"                                \
+      "add.u32 l1, b, 2;\n\tadd.u32 l2, b, 4;\n\tadd.u32 l3, b, 6;\n\t"                                  \
+      "mov.b64 b0, {b, hi};\n\tmov.b64 b1, {l1, hi};\n\tmov.b64 b2, {l2, hi};\n\tmov.b64 b3, {l3, hi};\n\t" \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [c], b0, %6, p;\n\t"                                \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a1], b1, %6, 1;\n\t"                               \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a2], b2, %6, 1;\n\t"                               \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a3], b3, %6, 1;\n\t"                               \
+      "setp.ne.b32 p, 1, 0;\n\t"                                                                       \
+      "add.u32 c, c, 32;\n\tsetp.ge.u32 w, c, %2;\n\t@w sub.u32 c, c, %3;\n\t"                          \
+      "add.u32 b, b, %5;\n\tadd.u32 g, g, 1;\n\t"                                                      \
+      "setp.lt.s32 more, g, %7;\n\t@more bra LOOP_%=;\n"                                                \
+      "DONE_%=:\n\t}" ::"r"(tmem_d),                                                                   \
+      "r"(a_tmem), "r"(ring_end), "r"(ring_cols), "r"(b_lo), "r"(b_step), "r"(idesc), "r"(n_groups),      \
+      "r"(0), "r"(a), "r"(grp_log2), "r"(bkl), "r"(wslot), "r"(wphase), "r"(avail), "r"(afull_base),   \
+      "r"(ns)                                                                                          \
+      : "memory")
+  if constexpr (kTF32) {
+    MEC_TS_ROW_BODY("tf32");
+  } else {
+    MEC_TS_ROW_BODY("f16");
+  }
+#undef MEC_TS_ROW_BODY
+}
+
 // Whole-warp call: one elected lane commits (arrives on `bar` when done).
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
   asm volatile(

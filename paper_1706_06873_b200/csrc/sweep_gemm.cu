@@ -502,40 +502,36 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         // the guard (a copy of slot 0's atom).
         const int n_full = nk >> 2;
         const uint32_t b_lo0 = static_cast<uint32_t>(bvar);
-        int k4 = 0;  // groups issued
 #ifdef MEC_TRACE
         int n_runs = 0;
         long long cyc_fence = 0;
         const long long cyc_setup = clock64() - cyc_row0 - cyc_tempty;
 #endif
-        while (k4 < n_full) {
-          // wait for every atom up to the one holding group k4's last element
-          // (a tight wait loop), then issue every group whose atoms landed
-          const int need = (a + ((k4 + 1) << (kcl + 2)) - 1) >> bkl;
-          if (avail <= need) {
-            do {
-              wait_atom();
-            } while (avail <= need);
-            ptx::tc_fence_after();
-          }
-          int ready = ((avail << bkl) - a) >> (kcl + 2);
-          if (ready > n_full) ready = n_full;
-          const int ng = ready - k4;
-#ifdef MEC_TRACE
-          const long long ci0 = clock64();
-          ++n_runs;
-#endif
+        if (n_full > 0) {
+          // the whole row in one call: the elected lane waits for each atom
+          // inside the PTX loop; this warp's ring counters then skip past the
+          // last atom the row's full groups need
           if (!no_mma)
-            ptx::mma_ts_groups_elect<kTF32>(d_tmem, col, ring0 + ring_cols, ring_cols,
-                                            b_lo0 + static_cast<uint32_t>(k4) * b_tile16, b_tile16, p.idesc,
-                                            k4 != 0 ? 1u : 0u, ng);
-#ifdef MEC_TRACE
-          cyc_issue += clock64() - ci0;
-#endif
-          col += static_cast<uint32_t>(ng * 32);
-          if (col >= ring0 + ring_cols) col -= ring_cols;  // ng * 32 < ring_cols: one wrap at most
-          k4 = ready;
+            ptx::mma_ts_row_elect<kTF32>(d_tmem, col, ring0 + ring_cols, ring_cols, b_lo0, b_tile16, p.idesc,
+                                         n_full, a, kcl + 2, bkl, ptx::smem_u32(afull), wslot, wphase, avail,
+                                         ns);
+          const int last = (a + (n_full << (kcl + 2)) - 1) >> bkl;
+          while (avail <= last) {
+            if (no_mma) ptx::mbar_wait(&afull[wslot], wphase);
+            if (++wslot == ns) {
+              wslot = 0;
+              wphase ^= 1u;
+            }
+            ++avail;
+            ++aseq;
+          }
+          col += static_cast<uint32_t>(n_full * 32);
+          while (col >= ring0 + ring_cols) col -= ring_cols;
+          if (no_mma) ptx::tc_fence_after();
         }
+#ifdef MEC_TRACE
+        const long long c_loop_end = clock64();
+#endif
         if (nk & 3) {  // tail group of nk mod 4 steps
           const int need = (a + (nk << kcl) - 1) >> bkl;
           if (avail <= need) {
@@ -566,7 +562,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           e[4] = static_cast<unsigned long long>(cyc_commit) + 1;
           e[5] = static_cast<unsigned long long>(n_runs) + 1;
           e[6] = static_cast<unsigned long long>(cyc_setup) + 1;
-          e[7] = static_cast<unsigned long long>(cyc_fence) + 1;
+          e[7] = static_cast<unsigned long long>(cc0 - c_loop_end) + 1;  // tail
+          e[5] = static_cast<unsigned long long>(c_loop_end - cyc_row0 - cyc_tempty - cyc_setup) + 1;  // run loop
         }
 #endif
         __syncwarp();

@@ -35,7 +35,7 @@ if os.environ.get("SW_CYCLES"):
     rows = tr[c][:, 257:296, :8] - 1
     print("raw", tr[c[0], 256:259, :4].tolist(), "ctas", len(c))
     rows = rows[(rows >= 0).all(axis=2)]
-    print("per-row cycles (median): tempty wait %d  afull waits %d  MMA issue calls %d  row total %d  commit %d  runs %d  setup %d  fences %d" % tuple(np.median(rows, axis=0)))
+    print("per-row cycles (median): tempty wait %d  afull waits %d  MMA issue calls %d  row total %d  commit %d  run-loop total %d  setup %d  tail %d" % tuple(np.median(rows, axis=0)))
     sys.exit(0)
 ctas = np.where(tr[:, 0, 0] > 0)[0]
 t0 = tr[ctas, 0, 0].min()
