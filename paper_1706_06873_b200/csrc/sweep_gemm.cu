@@ -156,7 +156,9 @@ __device__ __forceinline__ SwItem sw_decode(const SweepParams& p, int64_t t) {
   const int o_last = it.off0 + (it.nrows - 1) * p.shift;
   const int d_last = o_last & (p.mvec - 1);
   const int kc = 1 << p.kchunk_log2;
-  const int nk_last = (p.kdim + d_last + kc - 1) >> p.kchunk_log2;
+  // (a row's K steps are rounded up to whole 4-step groups: the extra steps
+  // meet zero weight rows, see the MMA issuer)
+  const int nk_last = (((p.kdim + d_last + kc - 1) >> p.kchunk_log2) + 3) & ~3;
   it.n_a = (o_last - d_last + nk_last * kc + p.bk - 1) / p.bk;
   return it;
 }
@@ -500,7 +502,10 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         // landed goes in one call (a PTX loop, no per-group election); then
         // wait for the next atom.  A group that runs past the ring end reads
         // the guard (a copy of slot 0's atom).
-        const int n_full = nk >> 2;
+        // whole 4-step groups: the steps past kdim + d meet zero rows of the
+        // weight operand (kdim_pad is a whole number of 4-step groups), so the
+        // row needs no separately issued tail group
+        const int n_full = (nk + 3) >> 2;
         const uint32_t b_lo0 = static_cast<uint32_t>(bvar);
 #ifdef MEC_TRACE
         int n_runs = 0;
@@ -532,18 +537,6 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 #ifdef MEC_TRACE
         const long long c_loop_end = clock64();
 #endif
-        if (nk & 3) {  // tail group of nk mod 4 steps
-          const int need = (a + (nk << kcl) - 1) >> bkl;
-          if (avail <= need) {
-            do {
-              wait_atom();
-            } while (avail <= need);
-            ptx::tc_fence_after();
-          }
-          if (!no_mma)
-            ptx::mma_ts_grp_elect<kTF32>(d_tmem, col, bvar + static_cast<uint32_t>(n_full) * b_tile16, p.idesc,
-                                         n_full != 0 ? 1u : 0u, nk & 3);
-        }
 #ifdef MEC_TRACE
         const long long cc0 = clock64();
 #endif
@@ -714,7 +707,7 @@ bool sweep_config(const Plan& pl, bool batch_folded, int* n_vres_out, int* n_acc
   int span = 0;
   for (int phi = 0; phi < pl.bk; phi += mvec)
     for (int d = 0; d < mvec; d += static_cast<int>(b)) {
-      const int64_t nk = (pl.kdim + d + kc - 1) / kc;
+      const int64_t nk = ((pl.kdim + d + kc - 1) / kc + 3) / 4 * 4;
       span = std::max<int>(span, static_cast<int>((phi + nk * kc - 1) / pl.bk) + 1);
     }
   // one accumulator per MMA issuer
