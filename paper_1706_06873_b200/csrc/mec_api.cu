@@ -441,7 +441,7 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
     // one-window-per-tile kernel (R output rows per tile)
     e = cudaErrorNotSupported;
     opt->selected_gemm = 2;
-    if (opt->rows_per_tile == 0 && !ga.fused) e = mec::launch_sweep_gemm(pc, ga, stream_, &launches);
+    if (opt->rows_per_tile == 0) e = mec::launch_sweep_gemm(pc, ga, stream_, &launches);
     if (e == cudaErrorNotSupported) {
       opt->selected_gemm = 1;
       e = mec::launch_window_gemm(pc, ga, stream_, &launches);

@@ -129,6 +129,11 @@ struct SweepParams {
   uint32_t stage_out_bytes;
   uint32_t backoff_ns;  // copier / epilogue waits: nanosleep between probes (0: spin)
   int n_iss;  // MMA issuer warps (1 or 2)
+  // fused (MEC_PATH_FUSED, i_c elt a multiple of 128 B): stream atoms are TMA
+  // boxes of I -- column c = hh kwc + b i_c + ci of L row (n, w) is pixel
+  // s_w w + b of input row hh, channels ci (Alg.2 l.4-6), so L is never written
+  bool fused;
+  int kwc, i_c, s_w, pad_h, pad_w;
   int dbg;  // (experiments, MEC_SWEEP_DBG) 1: no O stores, 2: no MMAs, 4: no TMEM stores of A
 };
 
@@ -397,7 +402,19 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           ptx::mbar_arrive_expect_tx(&full[stage], kSwAtomBytes);
           unsigned char* dstA = smemA + static_cast<size_t>(stage) * kSwAtomBytes;
           const int32_t x = it.x0 + i * p.bk;
-          if (p.ipt <= 1) {
+          if (p.fused) {
+            // L column x -> input row hh, kernel column b, channel block cb
+            const int hh = x / p.kwc, rem = x - hh * p.kwc;
+            const int b = rem / p.i_c, cb = rem - b * p.i_c;
+            const int32_t zy = hh - p.pad_h;  // (padding: TMA zero-fills out-of-bounds pixels and rows)
+            if (p.ipt <= 1) {
+              ptx::tma_load_4d(dstA, &tmA, &full[stage], cb, y0 * p.s_w + b - p.pad_w, zy, z0, hintA);
+            } else {
+              for (int j = 0; j < p.ipt; ++j)
+                ptx::tma_load_4d(dstA + j * p.slot * kTileKBytes, &tmA, &full[stage], cb, b - p.pad_w, zy,
+                                 z0 * p.ipt + j, hintA);
+            }
+          } else if (p.ipt <= 1) {
             ptx::tma_load_3d(dstA, &tmA, &full[stage], x, y0, z0, hintA);
           } else {  // one box of `slot` rows per image of the tile (images >= i_n: zero fill)
             for (int j = 0; j < p.ipt; ++j)
@@ -731,12 +748,13 @@ bool sweep_config(const Plan& pl, bool batch_folded, int* n_vres_out, int* n_acc
 
 cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st, int* launches) {
   int n_vres, n_acc, ns, stages;
-  if (a.fused || !sweep_config(pl, a.batch_folded, &n_vres, &n_acc, &ns, &stages)) return cudaErrorNotSupported;
+  if (a.fused && !fused_eligible(pl)) return cudaErrorNotSupported;
+  if (!sweep_config(pl, a.batch_folded, &n_vres, &n_acc, &ns, &stages)) return cudaErrorNotSupported;
   const bool tf32 = pl.dt == MEC_DTYPE_TF32;
   const int out_elt = pl.elt;
   CUtensorMap tmA, tmB, tmO;
   // row tiling: as window_gemm.cu
-  const bool flat = a.batch_folded && pl.o_w < 32;
+  const bool flat = !a.fused && a.batch_folded && pl.o_w < 32;
   int slot = 128, ipt = 1;
   if (!flat && pl.o_w <= 128) {
     slot = static_cast<int>((pl.o_w + 31) / 32 * 32);
@@ -746,7 +764,20 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   const int64_t rows = flat ? pl.s.i_n * pl.o_w : pl.o_w;
   const int64_t groups = flat ? 1 : (pl.s.i_n + ipt - 1) / ipt;
   const int64_t n_mt = flat ? (rows + kBM - 1) / kBM : (ipt > 1 ? 1 : (pl.o_w + kBM - 1) / kBM);
-  {  // A: L as {columns, rows, groups} (flat: one group of i_n o_w rows)
+  if (a.fused) {
+    // A: the NHWC input as {i_c, i_w, i_h, i_n}; a box is bk channels x `rows`
+    // pixels taken every s_w pixels (elementStrides): one K-atom of the stream
+    const uint64_t dims[4] = {static_cast<uint64_t>(pl.s.i_c), static_cast<uint64_t>(pl.src_w),
+                              static_cast<uint64_t>(pl.src_h), static_cast<uint64_t>(pl.s.i_n)};
+    const uint64_t strides[3] = {static_cast<uint64_t>(pl.s.i_c) * pl.elt,
+                                 static_cast<uint64_t>(pl.src_w * pl.s.i_c) * pl.elt,
+                                 static_cast<uint64_t>(pl.src_h * pl.src_w * pl.s.i_c) * pl.elt};
+    const uint32_t rows_box = static_cast<uint32_t>(ipt > 1 ? slot : kBM);
+    const uint32_t box[4] = {static_cast<uint32_t>(pl.bk), rows_box * static_cast<uint32_t>(pl.s_w), 1, 1};
+    const uint32_t es[4] = {1, static_cast<uint32_t>(pl.s_w), 1, 1};
+    cudaError_t e = encode_tiled_strided(&tmA, tf32, 4, a.L, dims, strides, box, es);
+    if (e != cudaSuccess) return e;
+  } else {  // A: L as {columns, rows, groups} (flat: one group of i_n o_w rows)
     const uint64_t dims[3] = {static_cast<uint64_t>(pl.l_cols), static_cast<uint64_t>(rows),
                               static_cast<uint64_t>(flat ? 1 : pl.s.i_n)};
     const uint64_t strides[2] = {static_cast<uint64_t>(pl.pitch) * pl.elt,
@@ -764,6 +795,12 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   }
   SweepParams p{};
   p.O = a.O;
+  p.fused = a.fused;
+  p.kwc = static_cast<int>(pl.s.k_w * pl.s.i_c);
+  p.i_c = static_cast<int>(pl.s.i_c);
+  p.s_w = pl.s_w;
+  p.pad_h = pl.pad_h;
+  p.pad_w = pl.pad_w;
   p.o_h = pl.o_h;
   p.o_w = pl.o_w;
   p.i_n = pl.s.i_n;
