@@ -398,7 +398,9 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         const int32_t z0 = static_cast<int32_t>(it.g);
         for (int i = 0; i < it.n_a; ++i, ++pseq) {
           const int stage = static_cast<int>(pseq % static_cast<uint32_t>(S));
+          if (pseq < 100) SW_TRACE(300u + pseq, 0);
           ptx::mbar_wait(&empty[stage], ((pseq / S) & 1u) ^ 1u);
+          if (pseq < 100) SW_TRACE(300u + pseq, 1);
           ptx::mbar_arrive_expect_tx(&full[stage], kSwAtomBytes);
           unsigned char* dstA = smemA + static_cast<size_t>(stage) * kSwAtomBytes;
           const int32_t x = it.x0 + i * p.bk;
@@ -421,6 +423,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
               ptx::tma_load_3d(dstA + j * p.slot * kTileKBytes, &tmA, &full[stage], x, 0, z0 * p.ipt + j, hintA);
           }
           SW_TRACE(pseq, 0);
+          if (pseq < 100) SW_TRACE(300u + pseq, 2);
         }
       }
     }

@@ -91,6 +91,17 @@ extern "C" mec_status_t mec_l2_flush(void* scratch, size_t bytes, void* stream) 
   const int64_t grid = std::min<int64_t>((half16 + 255) / 256, 8LL * mec::num_sms());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint4* base = static_cast<uint4*>(scratch);
+  // the same all-shared carveout as the MEC kernels, so the timed step after a
+  // flush does not include an SM shared-memory reconfiguration the flush caused
+  static bool carveout = false;
+  if (!carveout) {
+    cudaFuncSetAttribute(mec::flush_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(mec::flush_read_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaGetLastError();
+    carveout = true;
+  }
   mec::flush_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(base, half16, salt);
   mec::flush_read_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
       base + half16, half16, salt, reinterpret_cast<uint32_t*>(base));

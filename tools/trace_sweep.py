@@ -46,6 +46,10 @@ for k, n in enumerate(["entry", "prologue done", "weights issued", "weights land
     v = (life[:, k] - ent) / 1e3
     print("  %-17s %7.2f %7.2f %7.2f" % (n, np.percentile(v, 0), np.percentile(v, 50), np.percentile(v, 100)))
 print("  first A TMA issue %7.2f" % ((t0 - ent) / 1e3))
+pr = tr[ctas[0], 300:320, :3]
+print("producer (cta %d): before-wait / after-wait / after-issue (us from t0):" % ctas[0])
+for k in range(20):
+    if pr[k, 0]: print("  atom %2d  %7.3f %7.3f %7.3f" % (k, (pr[k,0]-t0)/1e3, (pr[k,1]-t0)/1e3, (pr[k,2]-t0)/1e3))
 names = ["P_issued", "C_full", "C_aempty", "C_arrived", "M_afull", "M_released"]
 print("ctas", len(ctas))
 def med(e1, e2):
