@@ -123,6 +123,8 @@ struct LowerParams {
   int wcls;           // column-class period 16 / gcd(wstep_b, 16)
   uint32_t raw_bytes;   // smem bytes per raw band buffer (two, double-buffered)
   int64_t total_bands;  // i_n bands (the persistent CTAs loop over them)
+  bool direct;          // aligned-copies path without the copies: every output granule is
+                        // extracted from the raw band (two aligned LDS.128 per part)
 };
 
 template <typename T>
@@ -164,6 +166,17 @@ __device__ __forceinline__ uint4 extract16(uint4 x, uint4 y, uint32_t sh_b) {
   const uint32_t a[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
   return make_uint4(__funnelshift_r(a[KK], a[KK + 1], sh_b), __funnelshift_r(a[KK + 1], a[KK + 2], sh_b),
                     __funnelshift_r(a[KK + 2], a[KK + 3], sh_b), __funnelshift_r(a[KK + 3], a[KK + 4], sh_b));
+}
+
+// 16 bytes at byte offset o (0..15; k = o / 4, sh_b = 8 (o mod 4)) of the
+// 32-byte little-endian string x:y, k and sh_b loop-invariant for the caller.
+__device__ __forceinline__ uint4 extract16_rt(uint4 x, uint4 y, uint32_t k, uint32_t sh_b) {
+  const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+  uint32_t z[5];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) z[j] = k == 0 ? w[j] : (k == 1 ? w[j + 1] : (k == 2 ? w[j + 2] : w[j + 3]));
+  return make_uint4(__funnelshift_r(z[0], z[1], sh_b), __funnelshift_r(z[1], z[2], sh_b),
+                    __funnelshift_r(z[2], z[3], sh_b), __funnelshift_r(z[3], z[4], sh_b));
 }
 
 // Build one copy from the raw staged band: smem granule m (dst + 16 m) =
@@ -249,6 +262,7 @@ __device__ __forceinline__ void lower_copies(const LowerParams& p, unsigned char
   // per-thread granule setup, cached per band height
   uint32_t set_rows = 0, wpar = 0, x0 = 0, off1 = 0, off2 = 0, m0 = 0, m1 = 0, m2 = 0, m3 = 0, n_it = 0;
   uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+  uint32_t yb1 = 0, yb2 = 0;  // band bytes of granule byte 0 of parts 1 and 2 (direct mode)
   uint32_t wi = 0;
   bool idle = true;
   const uint32_t gsh = static_cast<uint32_t>(p.gcls_log2);
@@ -294,6 +308,8 @@ __device__ __forceinline__ void lower_copies(const LowerParams& p, unsigned char
       const uint32_t v1 = (hh * p.delta16 + wi * wstep_b) & 15u;
       off1 = (v1 >> gsh) * p.copy_bytes + 16u + ((16u - v1) & 15u) + y1;
       off2 = off1;  // part 2 (strip hh + 1), = part 1 if unused
+      yb1 = y1;
+      yb2 = cut2 < 16 ? y1 + iwc_b - kwcs_b : y1;
       if (cut2 < 16) {
         const uint32_t y2 = y1 + iwc_b - kwcs_b;
         const uint32_t v2 = (v1 + p.delta16) & 15u;
@@ -308,6 +324,36 @@ __device__ __forceinline__ void lower_copies(const LowerParams& p, unsigned char
     const uint32_t n16 = (band_b + 31) / 16 + 2;
     const uint32_t g15 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(G) & 15);
     const uint32_t rawb = raw0 + static_cast<uint32_t>(buf) * p.raw_bytes;  // band byte y at rawb + g15 + y
+    if (p.direct) {
+      // ---- output straight from the raw band: granule part 1 (and 2) are the
+      // 16 bytes at raw address a (a mod 16 fixed along the w loop: da is a
+      // multiple of 16), taken out of the two aligned 16-byte words around it ----
+      uint32_t a1 = rawb + g15 + yb1, a2 = rawb + g15 + yb2;
+      const uint32_t k1 = (a1 >> 2) & 3u, s1 = (a1 & 3u) * 8u, k2 = (a2 >> 2) & 3u, s2 = (a2 & 3u) * 8u;
+      a1 &= ~15u;
+      a2 &= ~15u;
+      const uint32_t da = wpar * wstep_b;
+      const size_t pitch_b = static_cast<size_t>(p.pitch) * sizeof(T);
+      unsigned char* dst = p.L + ((n * p.o_w + wi) * p.pitch + h0 * p.kwcs) * sizeof(T) + x0;
+      const size_t dstep = pitch_b * wpar;
+#pragma unroll 2
+      for (uint32_t i = 0; i < n_it; ++i) {
+        const uint4 x = extract16_rt(ptx::ld_shared_v4(a1), ptx::ld_shared_v4(a1 + 16), k1, s1);
+        const uint4 y = extract16_rt(ptx::ld_shared_v4(a2), ptx::ld_shared_v4(a2 + 16), k2, s2);
+        uint4 o;
+        o.x = (x.x & m0) | (y.x & n0);
+        o.y = (x.y & m1) | (y.y & n1);
+        o.z = (x.z & m2) | (y.z & n2);
+        o.w = (x.w & m3) | (y.w & n3);
+        *reinterpret_cast<uint4*>(dst) = o;
+        a1 += da;
+        a2 += da;
+        dst += dstep;
+      }
+      __syncthreads();  // this raw buffer is rewritten next
+      LOWER_TRACE(2);
+      continue;
+    }
     for (int k = 0; k < p.ncls; ++k) {
       const uint32_t o_k = (16u - (static_cast<uint32_t>(k) << gsh)) & 15u;
       const uint32_t r = rawb + g15 - 16u - o_k;  // raw address of copy granule 0 (>= raw0 - 32)
@@ -817,7 +863,11 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
       }
       threads = static_cast<int>(std::max<uint32_t>(best_t, 64));
       p.raw_bytes = static_cast<uint32_t>(raw_b);
-      smem = 128 + 2 * static_cast<size_t>(p.raw_bytes) + csmem;
+      // direct extraction without the copies: opt-in (MEC_LOWER_DIRECT=1),
+      // measured slower on B200 -- AlexNet conv1 22.4 vs 16.5 us, cv3 b128
+      // 114 vs 63 us: the output loop is instruction-bound, not store-bound
+      p.direct = getenv("MEC_LOWER_DIRECT") && atoi(getenv("MEC_LOWER_DIRECT")) != 0;
+      smem = 128 + 2 * static_cast<size_t>(p.raw_bytes) + (p.direct ? 0 : csmem);
       p.total_bands = p.n_lower_blocks;
       // persistent CTAs: as many as are co-resident (each loops over bands,
       // prefetching the next band's rows while it writes the current one)
