@@ -392,14 +392,15 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       }
       SW_TRACE(511u, 2);
       uint32_t pseq = 0;
+      int stage = 0;
+      uint32_t pphase = 0;
       for (int64_t t = t_begin; t < p.n_items; t += t_step) {
         const SwItem it = sw_decode(p, t);
         const int32_t y0 = static_cast<int32_t>(it.mt * kBM);
         const int32_t z0 = static_cast<int32_t>(it.g);
         for (int i = 0; i < it.n_a; ++i, ++pseq) {
-          const int stage = static_cast<int>(pseq % static_cast<uint32_t>(S));
           if (pseq < 100) SW_TRACE(300u + pseq, 0);
-          ptx::mbar_wait(&empty[stage], ((pseq / S) & 1u) ^ 1u);
+          ptx::mbar_wait(&empty[stage], pphase ^ 1u);
           if (pseq < 100) SW_TRACE(300u + pseq, 1);
           ptx::mbar_arrive_expect_tx(&full[stage], kSwAtomBytes);
           unsigned char* dstA = smemA + static_cast<size_t>(stage) * kSwAtomBytes;
@@ -424,6 +425,10 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           }
           SW_TRACE(pseq, 0);
           if (pseq < 100) SW_TRACE(300u + pseq, 2);
+          if (++stage == S) {
+            stage = 0;
+            pphase ^= 1u;
+          }
         }
       }
     }
@@ -500,13 +505,15 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         const int nk = (kdim_r + d) >> kcl;
         skip_to(a >> bkl);  // atoms before this row's window
         const uint32_t g = q + static_cast<uint32_t>(r);
-        const int acc = static_cast<int>(g & 1u);
+        // accumulator of row g: g mod n_acc (n_acc = 1 or 2); phase (g / n_acc) mod 2
+        const int acc = p.n_acc == 2 ? static_cast<int>(g & 1u) : 0;
+        const uint32_t acc_use = p.n_acc == 2 ? (g >> 1) : g;
 #ifdef MEC_TRACE
         cyc_wait = 0;
         cyc_issue = 0;
         cyc_row0 = clock64();
 #endif
-        ptx::mbar_wait(&tempty[acc], ((g >> 1) & 1u) ^ 1u);
+        ptx::mbar_wait(&tempty[acc], (acc_use & 1u) ^ 1u);
 #ifdef MEC_TRACE
         cyc_tempty = clock64() - cyc_row0;
 #endif
@@ -595,14 +602,18 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     const uint32_t sw = static_cast<uint32_t>(m & 7);
     uint32_t cseq = 0;
     uint32_t q = 0;  // global number of the item's row 0
+    // running ring positions (no divisions on this latency-critical path)
+    int stage = 0, slot = 0;
+    uint32_t sphase = 0;
     for (int64_t t = t_begin; t < p.n_items; t += t_step) {
       const SwItem it = sw_decode(p, t);
       const uint32_t jstart = cseq;  // the item's atom 0
+      // last row whose window starts at or before atom jj (jj increasing):
+      // fr, and fo = the first element of row fr + 1
+      int fr = 0, fo = it.off0 + p.shift;
       for (int i = 0; i < it.n_a; ++i, ++cseq) {
-        const int stage = static_cast<int>(cseq % static_cast<uint32_t>(S));
-        const int slot = static_cast<int>(cseq % static_cast<uint32_t>(p.ns));
-        if (p.backoff_ns) ptx::mbar_wait_backoff(&full[stage], (cseq / S) & 1u, p.backoff_ns);
-        else ptx::mbar_wait(&full[stage], (cseq / S) & 1u);
+        if (p.backoff_ns) ptx::mbar_wait_backoff(&full[stage], sphase, p.backoff_ns);
+        else ptx::mbar_wait(&full[stage], sphase);
         if (warp == kSwFirstCopyWarp && lane == 0) SW_TRACE(cseq, 1);
         uint32_t r[32];
         const uint32_t src = a_smem + static_cast<uint32_t>(stage * kSwAtomBytes);
@@ -622,20 +633,25 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           const uint32_t J = cseq - static_cast<uint32_t>(p.ns);
           uint32_t g_free;
           if (J >= jstart) {
-            const int jj = static_cast<int>(J - jstart);
-            const int rm = min(it.nrows - 1, (((jj + 1) << p.bk_log2) - 1 - it.off0) / p.shift);
-            g_free = q + static_cast<uint32_t>(rm);
+            const int jend = ((static_cast<int>(J - jstart) + 1) << p.bk_log2) - 1;  // last element of atom J
+            while (fr + 1 < it.nrows && fo <= jend) {
+              ++fr;
+              fo += p.shift;
+            }
+            g_free = q + static_cast<uint32_t>(fr);
           } else {
             g_free = q - 1u;
           }
           // rows of one parity complete in order (one accumulator, one
           // issuer per parity when two issue): rows g_free and g_free - 1
           // cover every earlier row of both parities
-          const uint32_t want = (g_free >> 1) + 1u;
-          while (ptx::ld_acquire_shared_u32(ptx::smem_u32(&rows_done[g_free & 1u])) < want) {
+          // (one epilogue group when n_acc = 1: its counter covers every row)
+          const uint32_t ngl = static_cast<uint32_t>(p.n_acc - 1);  // log2(n_acc), n_acc = 1 or 2
+          const uint32_t want = (g_free >> ngl) + 1u;
+          while (ptx::ld_acquire_shared_u32(ptx::smem_u32(&rows_done[g_free & ngl])) < want) {
             if (p.backoff_ns) __nanosleep(p.backoff_ns);
           }
-          if (g_free > 0) {
+          if (g_free > 0 && ngl == 1) {
             const uint32_t g2 = g_free - 1u, want2 = (g2 >> 1) + 1u;
             while (ptx::ld_acquire_shared_u32(ptx::smem_u32(&rows_done[g2 & 1u])) < want2) {
               if (p.backoff_ns) __nanosleep(p.backoff_ns);
@@ -655,6 +671,11 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           ptx::mbar_arrive(&afull[slot]);
         }
         if (warp == kSwFirstCopyWarp && lane == 0) SW_TRACE(cseq, 3);
+        if (++stage == S) {
+          stage = 0;
+          sphase ^= 1u;
+        }
+        if (++slot == p.ns) slot = 0;
       }
       q += static_cast<uint32_t>(it.nrows);
     }
@@ -670,14 +691,15 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       const SwItem it = sw_decode(p, t);
       for (int r = 0; r < it.nrows; ++r) {
         const uint32_t qr = q + static_cast<uint32_t>(r);
-        if (static_cast<int>(qr & 1u) != group) continue;
-        const int acc = static_cast<int>(qr % static_cast<uint32_t>(p.n_acc));
-        if (p.backoff_ns) ptx::mbar_wait_backoff(&tfull[acc], (qr / p.n_acc) & 1u, p.backoff_ns);
-        else ptx::mbar_wait(&tfull[acc], (qr / p.n_acc) & 1u);
+        const uint32_t al = static_cast<uint32_t>(p.n_acc - 1);  // log2(n_acc), n_acc = 1 or 2
+        const int acc = static_cast<int>(qr & al);
+        if (acc != group) continue;  // (n_acc = 1: group 0 takes every row)
+        if (p.backoff_ns) ptx::mbar_wait_backoff(&tfull[acc], (qr >> al) & 1u, p.backoff_ns);
+        else ptx::mbar_wait(&tfull[acc], (qr >> al) & 1u);
         ptx::tc_fence_after();
         // row qr's MMAs are complete: its A atoms may be overwritten
         if (lane == 0 && ((warp - kSwFirstEpiWarp) & 3) == 0)
-          ptx::st_release_shared_u32(ptx::smem_u32(&rows_done[group]), (qr >> 1) + 1u);
+          ptx::st_release_shared_u32(ptx::smem_u32(&rows_done[group]), (qr >> al) + 1u);
         sw_store_row<kTF32>(p, &tmO, it.h0 + r, it.mt, it.g, quarter, lane,
                             tmem_base + lane_base + static_cast<uint32_t>(acc * p.bn), stg, stg_gen, &tempty[acc]);
       }
@@ -730,9 +752,14 @@ bool sweep_config(const Plan& pl, bool batch_folded, int* n_vres_out, int* n_acc
       const int64_t nk = ((pl.kdim + d + kc - 1) / kc + 3) / 4 * 4;
       span = std::max<int>(span, static_cast<int>((phi + nk * kc - 1) / pl.bk) + 1);
     }
-  // one accumulator per MMA issuer
-  const int n_acc = 2;
-  const int ns = std::min(kSwMaxRing, (512 - kSwGuardCols - ((2 * pl.bn + 31) / 32) * 32) / 32);
+  // two accumulators (one per MMA issuer, or double-buffered), else one
+  // (k_c = 128: the ring then holds a 10-atom window; rows serialise on it)
+  int n_acc = 2;
+  int ns = std::min(kSwMaxRing, (512 - kSwGuardCols - ((2 * pl.bn + 31) / 32) * 32) / 32);
+  if (ns < span) {
+    n_acc = 1;
+    ns = std::min(kSwMaxRing, (512 - kSwGuardCols - ((pl.bn + 31) / 32) * 32) / 32);
+  }
   if (ns < span) return false;
   int row_bytes = 128;
   while (row_bytes > 32 && (pl.bn * pl.elt) % row_bytes != 0) row_bytes /= 2;
@@ -840,9 +867,9 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   // (measured: 2 issuers win where the accumulators are 64 columns -- C2
   // 434->397 us, C3 127->117 us, cv3 106->95 us, cv7 255->250 us -- and lose
   // ~4-7% at k_c = 96, C1 / cv1, whose TMEM ring has 2 slots fewer)
-  p.n_iss = (2 * pl.shift < pl.kdim && pl.bn <= 64) ? 2 : 1;
-  if (const char* e = getenv("MEC_SWEEP_ISSUERS"))  // (experiments; 2 needs 2 shift < kdim)
-    p.n_iss = (atoi(e) >= 2 && 2 * pl.shift < pl.kdim) ? 2 : 1;
+  p.n_iss = (2 * pl.shift < pl.kdim && pl.bn <= 64 && n_acc == 2) ? 2 : 1;
+  if (const char* e = getenv("MEC_SWEEP_ISSUERS"))  // (experiments; 2 needs 2 shift < kdim, 2 accumulators)
+    p.n_iss = (atoi(e) >= 2 && 2 * pl.shift < pl.kdim && n_acc == 2) ? 2 : 1;
   p.backoff_ns = getenv("MEC_SWEEP_BACKOFF") ? static_cast<uint32_t>(atoi(getenv("MEC_SWEEP_BACKOFF"))) : 0u;
   // epilogue: pass width = 128 / 64 / 32 bytes per row, dividing bn
   int row_bytes = 128;

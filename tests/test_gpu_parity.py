@@ -558,6 +558,7 @@ SWEEP_CASES = [
     ((4, 20, 20, 64, 3, 3, 64), 1),      # o_w = 18: flat Solution A tiles
     ((2, 140, 140, 64, 3, 3, 64), 1),    # o_w = 138: two M tiles per image
     ((2, 30, 30, 32, 5, 5, 48), 2),      # k_c = 48, stride 2
+    ((2, 30, 30, 64, 3, 3, 128), 1),     # k_c = 128: one TMEM accumulator
 ]
 
 
