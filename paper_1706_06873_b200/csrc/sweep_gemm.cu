@@ -625,6 +625,10 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           r[4 * c + 2] = x.z;
           r[4 * c + 3] = x.w;
         }
+        // the atom is in registers: its shared-memory stage can be refilled now
+        // (the arrive's release orders the loads before the next TMA write)
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[stage]);
         if (cseq >= static_cast<uint32_t>(p.ns)) {
           // the slot's previous atom J = cseq - ns is free once the last row
           // reading it completed: in this item row r_max = the last row whose
@@ -666,10 +670,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          ptx::mbar_arrive(&empty[stage]);
-          ptx::mbar_arrive(&afull[slot]);
-        }
+        if (lane == 0) ptx::mbar_arrive(&afull[slot]);
         if (warp == kSwFirstCopyWarp && lane == 0) SW_TRACE(cseq, 3);
         if (++stage == S) {
           stage = 0;
