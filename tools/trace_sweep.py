@@ -46,6 +46,8 @@ for k, n in enumerate(["entry", "prologue done", "weights issued", "weights land
     v = (life[:, k] - ent) / 1e3
     print("  %-17s %7.2f %7.2f %7.2f" % (n, np.percentile(v, 0), np.percentile(v, 50), np.percentile(v, 100)))
 print("  first A TMA issue %7.2f" % ((t0 - ent) / 1e3))
+for c in ctas[:3]:
+    print("  cta %d raw lifetime (us):" % c, " ".join("%.2f" % ((v - ent) / 1e3) for v in tr[c, 511, :6]))
 pr = tr[ctas[0], 300:320, :3]
 print("producer (cta %d): before-wait / after-wait / after-issue (us from t0):" % ctas[0])
 for k in range(20):
