@@ -757,7 +757,7 @@ bool sweep_config(const Plan& pl, bool batch_folded, int* n_vres_out, int* n_acc
   // (k_c = 128: the ring then holds a 10-atom window; rows serialise on it)
   int n_acc = 2;
   int ns = std::min(kSwMaxRing, (512 - kSwGuardCols - ((2 * pl.bn + 31) / 32) * 32) / 32);
-  if (ns < span) {
+  if (ns < span || (getenv("MEC_SWEEP_NACC") && atoi(getenv("MEC_SWEEP_NACC")) == 1)) {  // (env: experiments)
     n_acc = 1;
     ns = std::min(kSwMaxRing, (512 - kSwGuardCols - ((pl.bn + 31) / 32) * 32) / 32);
   }
