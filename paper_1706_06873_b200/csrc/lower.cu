@@ -855,7 +855,11 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
       // (<= 256 threads: every thread then loops over several columns, which
       // amortises its per-granule setup -- measured: 480-thread blocks with 4
       // columns per thread spent most instructions in setup)
-      for (uint32_t wp = wcls; nch * wp <= 256 || wp == wcls; wp += wcls) {
+      // (measured: 256 for AlexNet conv1, o_w = 55 -- 16.0 us vs 18.0 at 384;
+      // 512 for cv3 b128, o_w = 111 -- 54.9 vs 63.1 us)
+      const uint32_t max_t = getenv("MEC_LOWER_MAXT") ? static_cast<uint32_t>(atoi(getenv("MEC_LOWER_MAXT")))
+                                                      : (pl.o_w >= 100 ? 512u : 256u);
+      for (uint32_t wp = wcls; nch * wp <= max_t || wp == wcls; wp += wcls) {
         const uint32_t t = (nch * wp + 31) / 32 * 32;
         const double eff = static_cast<double>(nch * wp) / t;
         if (eff >= best_eff - 1e-9) { best_eff = eff; best_t = t; }
