@@ -789,6 +789,8 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   // exact while hb*kwc*kwc < 2^32
   while (hb > 1 && static_cast<uint64_t>(hb) * p.kwc * p.kwc >= (1ull << 32)) hb = (hb + 1) / 2;
   hb = std::max<int64_t>(1, hb);
+  if (const char* e = getenv("MEC_LOWER_HB"))  // (experiments: rows per band, a multiple of the period)
+    hb = std::max<int64_t>(period, std::min<int64_t>(s.i_h, atoi(e) / period * period));
   p.hb = static_cast<int>(hb);
   p.bands = static_cast<int>((s.i_h + hb - 1) / hb);
   p.n_lower_blocks = s.i_n * p.bands;
