@@ -53,6 +53,8 @@ def parse():
                     help="window GEMM output rows per tile (multi-row schedule; 0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=4,
+                    help="image chunks of the e2e host-buffer call (copies pipelined with the kernels)")
     ap.add_argument("--no-flush", action="store_true", help="(diagnostic) do not flush L2")
     ap.add_argument("--no-fused-alt", action="store_true",
                     help="with --path auto, skip measuring the fused path alongside (north_star (3))")
@@ -357,38 +359,43 @@ def main():
     except Exception as e:  # noqa: BLE001
         graph_ms = f"unavailable: {e}"
 
-    # ---- end to end through the public API with host buffers (pinned), copies timed
+    # ---- end to end through the public API with host buffers (pinned), copies timed:
+    # mec_conv_forward_host copies I and K in and O out inside the call, pipelined over
+    # image chunks on three streams (the copies of neighbouring chunks overlap the kernels)
     e2e = None
     if not args.no_e2e:
         I_h = I.cpu().pin_memory()
         K_h = K.cpu().pin_memory()
         O_h = torch.empty(O.shape, dtype=O.dtype).pin_memory()
-        I2 = torch.empty_like(I)
-        K2 = torch.empty_like(K)
+        nch = max(1, min(args.e2e_chunks, I.shape[0]))
+        scratch = torch.empty(mec.host_scratch_bytes(*I.shape, *K.shape[:2], K.shape[3], s_h, s_w, I.dtype, nch),
+                              dtype=torch.uint8, device=dev)
         eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(K_steps)]
+
+        def e2e_call():
+            mec.conv_forward_host(I_h, K_h, s_h, s_w, out=O_h, n_chunks=nch, path=path, T=args.T,
+                                  sola_fix=fix, scratch=scratch)
+
         for _ in range(2):
-            I2.copy_(I_h, non_blocking=True)
-            K2.copy_(K_h, non_blocking=True)
-            mec.conv_forward(I2, K2, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, workspace=workspace, rows_per_tile=args.rows_per_tile)
-            O_h.copy_(O, non_blocking=True)
+            e2e_call()
         dist.barrier()
         torch.cuda.synchronize()
+        e2e_launches = 0
         for a, b in eev:
             if not args.no_flush:
                 mec.l2_flush(flush)
             a.record()
-            I2.copy_(I_h, non_blocking=True)
-            K2.copy_(K_h, non_blocking=True)
-            mec.conv_forward(I2, K2, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, workspace=workspace, rows_per_tile=args.rows_per_tile)
-            O_h.copy_(O, non_blocking=True)
+            e2e_call()
+            e2e_launches += mec.last_launch_count()
             b.record()
         torch.cuda.synchronize()
         dist.barrier()
         e2e_ms = dist.max_over_ranks(sum(a.elapsed_time(b) for a, b in eev), dev)
         e2e = {"value": w["flops"] * ws * K_steps / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": (w["nI"] + w["nK"]) * elt, "d2h_bytes_per_step": w["nO"] * elt,
-               "ms_per_step": e2e_ms / K_steps}
+               "ms_per_step": e2e_ms / K_steps, "api": "mec_conv_forward_host",
+               "chunks": nch, "kernels_per_step": e2e_launches / K_steps}
 
     # ---- roofline of the dominant kernel
     peaks, peak_src = load_peaks()

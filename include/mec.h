@@ -12,7 +12,8 @@
  *   L  i_n x o_w x i_h x k_w x i_c  (MEC's compact lowered tensor, Alg.2 l.2-6)
  *
  * Conventions for every entry point:
- *  - All tensor pointers are DEVICE pointers owned by the caller.  The library
+ *  - All tensor pointers are DEVICE pointers owned by the caller (except the
+ *    HOST buffers of mec_conv_forward_host).  The library
  *    never frees or retains them past the call; work is enqueued
  *    asynchronously on `stream` (a cudaStream_t; NULL = legacy default
  *    stream), so buffers must stay alive until the stream reaches the work.
@@ -37,7 +38,7 @@
 extern "C" {
 #endif
 
-#define MEC_ABI_VERSION 3
+#define MEC_ABI_VERSION 4
 
 typedef enum {
   MEC_OK = 0,
@@ -185,6 +186,39 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O,
                                  const mec_shape_t* s, int s_h, int s_w,
                                  mec_dtype_t dt, void* stream,
                                  mec_options_t* opt);
+
+/* End to end on HOST buffers (ABI 4): O_host = MEC(I_host, K_host, s), the
+ * same Algorithm 2 call as mec_conv_forward_ex with the
+ * host<->device copies inside.  The i_n images are cut into n_chunks chunks of
+ * ceil(i_n / n_chunks) images (each chunk is an independent convolution of a
+ * sub-batch: Alg.2 never mixes images); chunk c's copy in, its MEC call and
+ * its copy out run on three library streams so the copy in of chunk c + 1 and
+ * the copy out of chunk c - 1 overlap chunk c's kernels (the PCIe link is
+ * full duplex).  The path is resolved ONCE on the full shape (Alg.2 l.8 with
+ * opt->T) and forced for every chunk, so each image takes the path the
+ * one-shot call would take.
+ *   I_host  i_n x i_h x i_w x i_c, K_host k_h x k_w x i_c x k_c, O_host
+ *           i_n x o_h x o_w x k_c, all n-h-w-c, caller-owned host memory.
+ *           Page-locked (cudaHostAlloc / torch pin_memory) for the copies to
+ *           be asynchronous; pageable memory works but serialises them.
+ *   stream  the caller's stream: work already on it is ordered before the
+ *           first copy, and it waits for the last copy out, so O_host is
+ *           complete once `stream` is synchronised.
+ *   opt     as mec_conv_forward_ex (NULL = defaults); opt->workspace is
+ *           ignored (the scratch holds it); MEC_SOLA_FIX_NONE is
+ *           MEC_ERR_UNSUPPORTED (h-n-w-c is not contiguous per chunk).
+ *   dev_scratch  device buffer of >= mec_host_scratch_bytes(...) bytes,
+ *           16-byte aligned, caller-owned, not touched after `stream`
+ *           completes; NULL = taken from the library's stream-ordered pool.
+ * n_chunks < 1 or > i_n: clamped to [1, i_n].  Errors as mec_conv_forward_ex;
+ * a copy failure is MEC_ERR_CUDA.  mec_last_launch_count() afterwards is the
+ * number of KERNELS enqueued over all chunks (copies are not counted). */
+size_t mec_host_scratch_bytes(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt,
+                              const mec_options_t* opt, int n_chunks);
+mec_status_t mec_conv_forward_host(const void* I_host, const void* K_host, void* O_host,
+                                   const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt,
+                                   void* stream, mec_options_t* opt, int n_chunks,
+                                   void* dev_scratch, size_t dev_scratch_bytes);
 
 /* Layout of a convolution output consumed by mec_maxpool. */
 typedef enum {

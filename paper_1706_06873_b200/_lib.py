@@ -43,6 +43,7 @@ EXPORTED = (
     "mec_conv_forward_ex", "mec_last_launch_count", "mec_status_string",
     "mec_last_error_message", "mec_abi_version", "mec_synth_fill", "mec_l2_flush",
     "mec_workspace_bytes_ex", "mec_lower_padded", "mec_maxpool", "mec_lower_pitched",
+    "mec_host_scratch_bytes", "mec_conv_forward_host",
 )
 # mec_layout_t
 MEC_LAYOUT_NHWC = 0
@@ -118,6 +119,11 @@ def lib():
         L.mec_conv_forward.restype = ci
         L.mec_conv_forward_ex.argtypes = [vp, vp, vp, sp, ci, ci, ci, vp, P(MecOptions)]
         L.mec_conv_forward_ex.restype = ci
+        L.mec_host_scratch_bytes.argtypes = [sp, ci, ci, ci, P(MecOptions), ci]
+        L.mec_host_scratch_bytes.restype = ctypes.c_size_t
+        L.mec_conv_forward_host.argtypes = [vp, vp, vp, sp, ci, ci, ci, vp, P(MecOptions), ci, vp,
+                                            ctypes.c_size_t]
+        L.mec_conv_forward_host.restype = ci
         L.mec_last_launch_count.argtypes = []
         L.mec_last_launch_count.restype = ci
         L.mec_status_string.argtypes = [ci]

@@ -493,3 +493,191 @@ mec_status_t mec_maxpool(const void* X, void* Y, int64_t i_n, int64_t h, int64_t
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// mec_conv_forward_host: the end-to-end call on host buffers (include/mec.h).
+// Chunk c of the images: copy in on the H2D stream, Algorithm 2 on the compute
+// stream, copy out on the D2H stream, with a ring of kSlots device buffers so
+// the copies of neighbouring chunks overlap chunk c's kernels in both PCIe
+// directions.
+namespace mec {
+namespace {
+
+constexpr int kSlots = 3;
+
+struct HostPipe {
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  cudaEvent_t start = nullptr, k_in = nullptr;
+  cudaEvent_t in[kSlots] = {}, done[kSlots] = {}, out[kSlots] = {};
+};
+HostPipe g_pipes[kMaxDevices];
+std::mutex g_pipe_mu;  // held while a call enqueues (the events are shared)
+
+cudaError_t get_pipe(HostPipe** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  HostPipe& P = g_pipes[dev];
+  if (!P.h2d) {
+    const unsigned ev = cudaEventDisableTiming;
+    if ((e = cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&P.comp, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&P.start, ev)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&P.k_in, ev)) != cudaSuccess) return e;
+    for (int i = 0; i < kSlots; ++i) {
+      if ((e = cudaEventCreateWithFlags(&P.in[i], ev)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&P.done[i], ev)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&P.out[i], ev)) != cudaSuccess) return e;
+    }
+  }
+  *out = &P;
+  return cudaSuccess;
+}
+
+// Byte layout of the device scratch: K | kSlots x (I chunk | O chunk) | workspace.
+struct HostLayout {
+  int64_t per_chunk, n_chunks, slots;
+  size_t i_img, o_img, k_bytes;  // bytes per image of I and O, bytes of K
+  size_t off_slot0, slot_bytes, off_o, off_ws, ws_bytes, total;
+};
+
+mec_status_t host_layout(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, const mec_options_t* opt,
+                         int n_chunks, HostLayout* h) {
+  Plan p;
+  mec_status_t st = make_plan(s, s_h, s_w, dt, &p, opt ? opt->pad_h : 0, opt ? opt->pad_w : 0);
+  if (st != MEC_OK) return st;
+  const int64_t nc = std::min<int64_t>(std::max(n_chunks, 1), s->i_n);
+  h->per_chunk = (s->i_n + nc - 1) / nc;
+  h->n_chunks = (s->i_n + h->per_chunk - 1) / h->per_chunk;
+  h->slots = std::min<int64_t>(kSlots, h->n_chunks);
+  h->i_img = static_cast<size_t>(s->i_h * s->i_w * s->i_c) * p.elt;
+  h->o_img = static_cast<size_t>(p.o_h * p.o_w * s->k_c) * p.elt;
+  h->k_bytes = static_cast<size_t>(s->k_h * s->k_w * s->i_c * s->k_c) * p.elt;
+  mec_shape_t sc = *s;
+  sc.i_n = h->per_chunk;
+  Plan pc;
+  st = make_plan(&sc, s_h, s_w, dt, &pc, opt ? opt->pad_h : 0, opt ? opt->pad_w : 0);
+  if (st != MEC_OK) return st;
+  h->off_slot0 = round_up(h->k_bytes, 1024);
+  h->off_o = round_up(h->i_img * h->per_chunk, 1024);
+  h->slot_bytes = h->off_o + round_up(h->o_img * h->per_chunk, 1024);
+  h->off_ws = h->off_slot0 + h->slots * h->slot_bytes;
+  h->ws_bytes = pc.ws_bytes;
+  h->total = h->off_ws + h->ws_bytes + 1024;  // + alignment slack of the base
+  return MEC_OK;
+}
+
+}  // namespace
+}  // namespace mec
+
+extern "C" {
+
+size_t mec_host_scratch_bytes(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt,
+                              const mec_options_t* opt, int n_chunks) {
+  mec::HostLayout h;
+  if (mec::host_layout(s, s_h, s_w, dt, opt, n_chunks, &h) != MEC_OK) return 0;
+  return h.total;
+}
+
+mec_status_t mec_conv_forward_host(const void* I_host, const void* K_host, void* O_host,
+                                   const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt,
+                                   void* stream, mec_options_t* opt, int n_chunks,
+                                   void* dev_scratch, size_t dev_scratch_bytes) {
+  mec_options_t def;
+  if (!opt) {
+    mec_options_init(&def);
+    opt = &def;
+  }
+  if (!I_host || !K_host || !O_host) return MEC_ERR_INVALID_ARG;
+  mec::HostLayout h;
+  mec_status_t st = mec::host_layout(s, s_h, s_w, dt, opt, n_chunks, &h);
+  if (st != MEC_OK) return st;
+  if (opt->sola_fix == MEC_SOLA_FIX_NONE) return MEC_ERR_UNSUPPORTED;
+  if (opt->path < MEC_PATH_AUTO || opt->path > MEC_PATH_FUSED) return MEC_ERR_INVALID_ARG;
+  // Alg.2 l.8 on the full shape, then forced for every chunk
+  Plan pf;
+  st = mec::make_plan(s, s_h, s_w, dt, &pf, opt->pad_h, opt->pad_w);
+  if (st != MEC_OK) return st;
+  const int path = opt->path == MEC_PATH_AUTO ? mec::select_path_plan(pf, opt->T > 0 ? opt->T : MEC_DEFAULT_T)
+                                              : opt->path;
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  if (dev_scratch) {
+    if (!mec::aligned16(dev_scratch)) return MEC_ERR_MISALIGNED;
+    if (dev_scratch_bytes < h.total) return MEC_ERR_NO_MEMORY;
+  }
+  std::lock_guard<std::mutex> lk(mec::g_pipe_mu);
+  mec::HostPipe* P = nullptr;
+  cudaError_t e = mec::get_pipe(&P);
+  if (e != cudaSuccess) return mec::cuda_fail(e, "mec host pipeline");
+  bool pooled = false;
+  void* scratch = dev_scratch;
+  if (!scratch) {
+    cudaMemPool_t pool;
+    if ((e = mec::get_pool(&pool)) != cudaSuccess) return mec::cuda_fail(e, "mec pool");
+    if (cudaMallocFromPoolAsync(&scratch, h.total, pool, user) != cudaSuccess) {
+      cudaGetLastError();
+      snprintf(mec::g_err, sizeof(mec::g_err), "host-call scratch allocation of %zu bytes failed", h.total);
+      return MEC_ERR_NO_MEMORY;
+    }
+    pooled = true;
+  }
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(scratch) + 1023) & ~static_cast<uintptr_t>(1023));
+  const unsigned char* Ih = static_cast<const unsigned char*>(I_host);
+  unsigned char* Oh = static_cast<unsigned char*>(O_host);
+  int kernels = 0;
+  mec_options_t co = *opt;
+  co.path = path;
+  co.workspace = base + h.off_ws;
+  co.workspace_bytes = h.ws_bytes;
+  for (auto& ev : co.stage_events) ev = nullptr;
+  // the caller's earlier work (and the pool allocation) precede every copy
+  e = cudaEventRecord(P->start, user);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(P->h2d, P->start, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(P->comp, P->start, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(P->d2h, P->start, 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(base, K_host, h.k_bytes, cudaMemcpyHostToDevice, P->h2d);
+  if (e == cudaSuccess) e = cudaEventRecord(P->k_in, P->h2d);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(P->comp, P->k_in, 0);
+  for (int64_t c = 0; c < h.n_chunks && e == cudaSuccess; ++c) {
+    const int sl = static_cast<int>(c % h.slots);
+    const int64_t n0 = c * h.per_chunk;
+    const int64_t nb = std::min<int64_t>(h.per_chunk, s->i_n - n0);
+    unsigned char* Id = base + h.off_slot0 + sl * h.slot_bytes;
+    unsigned char* Od = Id + h.off_o;
+    // copy in: the slot's I is free once chunk c - slots has been computed
+    if (c >= h.slots) e = cudaStreamWaitEvent(P->h2d, P->done[sl], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(Id, Ih + n0 * h.i_img, nb * h.i_img, cudaMemcpyHostToDevice, P->h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(P->in[sl], P->h2d);
+    // compute: needs its I, and the slot's O drained by chunk c - slots' copy out
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(P->comp, P->in[sl], 0);
+    if (e == cudaSuccess && c >= h.slots) e = cudaStreamWaitEvent(P->comp, P->out[sl], 0);
+    if (e != cudaSuccess) break;
+    mec_shape_t sc = *s;
+    sc.i_n = nb;
+    st = mec_conv_forward_ex(Id, base, Od, &sc, s_h, s_w, dt, P->comp, &co);
+    if (st != MEC_OK) break;
+    kernels += mec::g_launches;
+    e = cudaEventRecord(P->done[sl], P->comp);
+    // copy out
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(P->d2h, P->done[sl], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(Oh + n0 * h.o_img, Od, nb * h.o_img, cudaMemcpyDeviceToHost, P->d2h);
+    if (e == cudaSuccess) e = cudaEventRecord(P->out[sl], P->d2h);
+  }
+  // the caller's stream waits for the last copy out (the D2H stream is in order)
+  if (e == cudaSuccess) e = cudaEventRecord(P->start, P->d2h);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(user, P->start, 0);
+  if (pooled) cudaFreeAsync(scratch, user);
+  if (st != MEC_OK) return st;
+  if (e != cudaSuccess) return mec::cuda_fail(e, "mec_conv_forward_host");
+  opt->selected_path = co.selected_path;
+  opt->selected_gemm = co.selected_gemm;
+  mec::g_launches = kernels;
+  return MEC_OK;
+}
+
+}  // extern "C"

@@ -162,6 +162,60 @@ def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torc
     return (out, *extra) if extra else out
 
 
+def host_scratch_bytes(i_n, i_h, i_w, i_c, k_h, k_w, k_c, s_h, s_w, dtype, n_chunks,
+                       pad_h: int = 0, pad_w: int = 0) -> int:
+    """mec_host_scratch_bytes: device scratch of conv_forward_host for this problem."""
+    opt = _lib.MecOptions()
+    _lib.lib().mec_options_init(ctypes.byref(opt))
+    opt.pad_h, opt.pad_w = int(pad_h), int(pad_w)
+    return int(_lib.lib().mec_host_scratch_bytes(ctypes.byref(_shape(i_n, i_h, i_w, i_c, k_h, k_w, k_c)),
+                                                 s_h, s_w, dtype_code(dtype), ctypes.byref(opt),
+                                                 int(n_chunks)))
+
+
+def conv_forward_host(I_h: torch.Tensor, K_h: torch.Tensor, s_h: int, s_w: int, out: torch.Tensor | None = None,
+                      n_chunks: int = 4, path: int = MEC_PATH_AUTO, T: int = MEC_DEFAULT_T,
+                      sola_fix: int = MEC_SOLA_FIX_EPILOGUE, scratch: torch.Tensor | None = None,
+                      pad_h: int = 0, pad_w: int = 0, device=None, return_path: bool = False):
+    """mec_conv_forward_host: O = MEC(I, K, s) on HOST tensors (pinned for asynchronous copies):
+    the copies in and out run inside the call, pipelined over n_chunks chunks of images.
+    Enqueued on the current stream of `device` (default: the current CUDA device); O is
+    complete once that stream is synchronised.  scratch: a device uint8 tensor of at least
+    host_scratch_bytes(...) bytes (None = the library's stream-ordered pool)."""
+    for t, n in ((I_h, "I"), (K_h, "K")):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{n} must be a contiguous HOST tensor")
+    if K_h.dtype != I_h.dtype:
+        raise TypeError("I and K must have the same dtype")
+    i_n, i_h, i_w, i_c = I_h.shape
+    k_h, k_w, k_ci, k_c = K_h.shape
+    if k_ci != i_c:
+        raise ValueError("K's third extent must equal i_c (Table 1)")
+    o_h, o_w = out_dims(i_h + 2 * pad_h, i_w + 2 * pad_w, k_h, k_w, s_h, s_w)
+    if out is None:
+        out = torch.empty((i_n, o_h, o_w, k_c), dtype=I_h.dtype, pin_memory=True)
+    if out.is_cuda or not out.is_contiguous():
+        raise ValueError("O must be a contiguous HOST tensor")
+    assert out.dtype == I_h.dtype and out.numel() == i_n * o_h * o_w * k_c
+    opt = _lib.MecOptions()
+    _lib.lib().mec_options_init(ctypes.byref(opt))
+    opt.path, opt.T, opt.sola_fix = int(path), int(T), int(sola_fix)
+    opt.pad_h, opt.pad_w = int(pad_h), int(pad_w)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    sp, sb = None, 0
+    if scratch is not None:
+        _cuda(scratch, "scratch")
+        sp, sb = scratch.data_ptr(), scratch.numel() * scratch.element_size()
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        st = _lib.lib().mec_conv_forward_host(I_h.data_ptr(), K_h.data_ptr(), out.data_ptr(),
+                                              ctypes.byref(_shape(i_n, i_h, i_w, i_c, k_h, k_w, k_c)),
+                                              s_h, s_w, dtype_code(I_h.dtype), stream, ctypes.byref(opt),
+                                              int(n_chunks), sp, sb)
+    _lib.check(st, "mec_conv_forward_host")
+    return (out, opt.selected_path) if return_path else out
+
+
 def maxpool(X: torch.Tensor, p_h: int, p_w: int, s_h: int, s_w: int, hnwc: bool = False,
             out: torch.Tensor | None = None) -> torch.Tensor:
     """mec_maxpool: max pooling of a conv output X, given as (i_n, h, w, c) n-h-w-c or, with

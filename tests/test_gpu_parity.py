@@ -596,3 +596,75 @@ def test_sweep_gemm_selected_for_C1_C2_C3(cuda_ok):
         I, K = make_inputs(shape, "bf16", seed=6200)
         _, g = mec.conv_forward(to_dev(I, "bf16"), to_dev(K, "bf16"), s, s, return_gemm=True)
         assert g == 2, shape
+
+
+# ---- end to end on host buffers (mec_conv_forward_host): copies pipelined over image chunks
+HOST_CASES = [
+    # shape, s_h, s_w, n_chunks (ragged last chunk, more chunks than slots, chunks > i_n clamped)
+    ((5, 20, 17, 5, 4, 3, 24), 2, 1, 2),
+    ((7, 30, 30, 16, 3, 3, 40), 1, 1, 4),
+    ((3, 12, 12, 7, 2, 2, 17), 3, 3, 9),
+    ((6, 27, 27, 3, 11, 11, 96), 4, 4, 6),
+    ((1, 8, 9, 6, 8, 9, 48), 1, 1, 1),
+]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("case", range(len(HOST_CASES)))
+def test_conv_forward_host_pipelined(cuda_ok, case, dtype):
+    """The host-buffer call equals the oracle, and equals the device call element for element
+    (each chunk is a sub-batch of the same Algorithm 2 path: the arithmetic per output element
+    does not depend on the chunking)."""
+    shape, s_h, s_w, nch = HOST_CASES[case]
+    I, K = make_inputs(shape, dtype, seed=7000 + case)
+    ref = oracle.direct_conv(I, K, s_h, s_w)
+    I_h = torch.from_numpy(np.ascontiguousarray(I)).to(TDT[dtype]).pin_memory()
+    K_h = torch.from_numpy(np.ascontiguousarray(K)).to(TDT[dtype]).pin_memory()
+    O_h, path = mec.conv_forward_host(I_h, K_h, s_h, s_w, n_chunks=nch, return_path=True)
+    torch.cuda.synchronize()
+    assert path == mec.select_path(shape, s_h, s_w)
+    check_O(O_h, ref, dtype, shape[4] * shape[5] * shape[3])
+    O_d = mec.conv_forward(I_h.cuda(), K_h.cuda(), s_h, s_w)
+    torch.cuda.synchronize()
+    assert torch.equal(O_h, O_d.cpu())
+
+
+def test_conv_forward_host_scratch_and_repeat(cuda_ok):
+    """Caller scratch, pageable host memory, back-to-back calls reusing the library's streams
+    and events, and a too-small scratch (MEC_ERR_NO_MEMORY)."""
+    shape, s = (9, 27, 27, 3, 11, 11, 96), 4
+    I, K = make_inputs(shape, "bf16", seed=7100)
+    ref = oracle.direct_conv(I, K, s, s)
+    I_h = torch.from_numpy(I).to(torch.bfloat16)  # pageable
+    K_h = torch.from_numpy(K).to(torch.bfloat16)
+    nb = mec.host_scratch_bytes(*shape, s, s, torch.bfloat16, 4)
+    scratch = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    outs = [mec.conv_forward_host(I_h, K_h, s, s, n_chunks=4, scratch=scratch) for _ in range(3)]
+    torch.cuda.synchronize()
+    for O in outs:
+        check_O(O, ref, "bf16", 11 * 11 * 3)
+        assert torch.equal(O, outs[0])
+    with pytest.raises(MecError):
+        mec.conv_forward_host(I_h, K_h, s, s, n_chunks=4, scratch=scratch[:nb - 2048])
+    with pytest.raises(MecError):
+        mec.conv_forward_host(I_h, K_h, s, s, sola_fix=MEC_SOLA_FIX_NONE)
+
+
+def test_C1_conv_forward_host_full_batch_sampled(cuda_ok):
+    """The bench's e2e launch configuration: C1 at its full batch through the host-buffer call."""
+    c = synth.config("C1")
+    shape = (c["i_n"], c["i_h"], c["i_w"], c["i_c"], c["k_h"], c["k_w"], c["k_c"])
+    seed = synth.SEED_BASE + c["index"]
+    kind = synth.KIND_GRID8
+    Id = torch.empty(shape[:4], dtype=torch.bfloat16, device="cuda")
+    Kd = torch.empty((c["k_h"], c["k_w"], c["i_c"], c["k_c"]), dtype=torch.bfloat16, device="cuda")
+    mec.synth_fill(Id, seed, synth.TENSOR_I, kind)
+    mec.synth_fill(Kd, seed, synth.TENSOR_K, kind)
+    I_h, K_h = Id.cpu().pin_memory(), Kd.cpu().pin_memory()
+    O = mec.conv_forward_host(I_h, K_h, c["s_h"], c["s_w"], n_chunks=4)
+    torch.cuda.synchronize()
+    K = synth.kernel_tensor(c, kind, seed)
+    for n in [0, 13, 31]:
+        I = synth.input_images(c, n, 1, kind, seed)
+        ref = oracle.direct_conv(I, K, c["s_h"], c["s_w"], n_threads=8)
+        check_O(O[n:n + 1], ref, "bf16", c["k_h"] * c["k_w"] * c["i_c"])
