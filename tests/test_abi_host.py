@@ -170,3 +170,36 @@ def test_product_package_does_not_import_oracle():
             assert "oracle" not in txt.replace("oracle/", "").lower() or "import oracle" not in txt, p
             assert "import oracle" not in txt and "from oracle" not in txt, p
             assert "mec_oracle" not in txt, p
+
+
+def test_host_call_scratch_layout_and_validation():
+    """mec_host_scratch_bytes / mec_conv_forward_host (ABI 4): the scratch holds K, a ring of
+    min(3, chunks) I and O chunk slots and the workspace of one chunk; every argument error is
+    returned before any device work (fake pointers are never touched)."""
+    L = _lib.lib()
+    bf = _lib.MEC_DTYPE_BF16
+    shp = (32, 227, 227, 3, 11, 11, 96)
+    s = _lib.MecShape(*shp)
+    i_img, o_img, k_b = 227 * 227 * 3 * 2, 55 * 55 * 96 * 2, 11 * 11 * 3 * 96 * 2
+    up = lambda x: (x + 1023) // 1024 * 1024  # noqa: E731
+    for nch, per, slots in [(1, 32, 1), (2, 16, 2), (4, 8, 3), (5, 7, 3), (64, 1, 3)]:
+        sub = _lib.MecShape(per, *shp[1:])
+        wsb = L.mec_workspace_bytes(ctypes.byref(sub), 4, 4, bf)
+        want = up(k_b) + slots * (up(i_img * per) + up(o_img * per)) + wsb + 1024
+        assert L.mec_host_scratch_bytes(ctypes.byref(s), 4, 4, bf, None, nch) == want, nch
+    bad = _lib.MecShape(1, 2, 2, 1, 3, 3, 1)
+    assert L.mec_host_scratch_bytes(ctypes.byref(bad), 1, 1, bf, None, 1) == 0
+    fake = ctypes.c_void_p(0x1000)
+    opt = _lib.MecOptions()
+    L.mec_options_init(ctypes.byref(opt))
+    call = lambda sh, o, scr, nb, I=fake: L.mec_conv_forward_host(  # noqa: E731
+        I, fake, fake, ctypes.byref(sh), 4, 4, bf, None, o, 4, scr, nb)
+    assert call(s, ctypes.byref(opt), fake, 1 << 40, I=None) == _lib.MEC_ERR_INVALID_ARG
+    assert call(bad, ctypes.byref(opt), fake, 1 << 40) == _lib.MEC_ERR_INVALID_ARG
+    need = L.mec_host_scratch_bytes(ctypes.byref(s), 4, 4, bf, None, 4)
+    assert call(s, ctypes.byref(opt), fake, need - 1) == _lib.MEC_ERR_NO_MEMORY
+    assert call(s, ctypes.byref(opt), ctypes.c_void_p(0x1008), need) == _lib.MEC_ERR_MISALIGNED
+    opt.sola_fix = _lib.MEC_SOLA_FIX_NONE
+    assert call(s, ctypes.byref(opt), fake, need) == _lib.MEC_ERR_UNSUPPORTED
+    opt.sola_fix, opt.path = _lib.MEC_SOLA_FIX_EPILOGUE, 7
+    assert call(s, ctypes.byref(opt), fake, need) == _lib.MEC_ERR_INVALID_ARG
