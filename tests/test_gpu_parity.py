@@ -668,3 +668,21 @@ def test_C1_conv_forward_host_full_batch_sampled(cuda_ok):
         I = synth.input_images(c, n, 1, kind, seed)
         ref = oracle.direct_conv(I, K, c["s_h"], c["s_w"], n_threads=8)
         check_O(O[n:n + 1], ref, "bf16", c["k_h"] * c["k_w"] * c["i_c"])
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("path", ["A", "B", "fused"])
+def test_conv_forward_host_padded_and_forced_paths(cuda_ok, path, dtype):
+    """The host-buffer call with virtual zero padding and each forced path (the fused TMA variant
+    included), over chunks with a ragged tail: equal to the oracle on the padded input."""
+    from paper_1706_06873_b200._lib import MEC_PATH_FUSED
+    shape, s, ph, pw = (5, 9, 9, 128, 3, 3, 32), 2, 1, 1
+    I, K = make_inputs(shape, dtype, seed=7200)
+    ref = oracle.direct_conv(_pad(I, ph, pw), K, s, s, n_threads=8)
+    p = {"A": MEC_PATH_SOLUTION_A, "B": MEC_PATH_SOLUTION_B, "fused": MEC_PATH_FUSED}[path]
+    I_h = torch.from_numpy(np.ascontiguousarray(I)).to(TDT[dtype]).pin_memory()
+    K_h = torch.from_numpy(np.ascontiguousarray(K)).to(TDT[dtype]).pin_memory()
+    O, ran = mec.conv_forward_host(I_h, K_h, s, s, n_chunks=3, path=p, pad_h=ph, pad_w=pw, return_path=True)
+    torch.cuda.synchronize()
+    assert ran == p
+    check_O(O, ref, dtype, shape[3] * shape[4] * shape[5])
