@@ -38,9 +38,29 @@ def main(h2d_bytes=9963264, d2h_bytes=18585600):
         cur.wait_stream(s2)
 
     bo = timed(both)
+
+    def chunked(n):
+        hb, ob = h2d_bytes // n // 16 * 16, d2h_bytes // n // 16 * 16
+
+        def f():
+            cur = torch.cuda.current_stream()
+            s1.wait_stream(cur)
+            s2.wait_stream(cur)
+            for c in range(n):
+                with torch.cuda.stream(s1):
+                    di[c * hb:(c + 1) * hb].copy_(hi[c * hb:(c + 1) * hb], non_blocking=True)
+                with torch.cuda.stream(s2):
+                    ho[c * ob:(c + 1) * ob].copy_(do[c * ob:(c + 1) * ob], non_blocking=True)
+            cur.wait_stream(s1)
+            cur.wait_stream(s2)
+        torch.cuda.synchronize()
+        torch.cuda._sleep(4_000_000)
+        return timed(f, reps=5)
+
+    chunk_ms = {n: chunked(n) for n in (1, 4, 8)}
     print(json.dumps({"h2d_ms": h2d, "h2d_GBps": h2d_bytes / h2d / 1e6, "d2h_ms": d2h,
                       "d2h_GBps": d2h_bytes / d2h / 1e6, "both_concurrent_ms": bo,
-                      "serial_ms": h2d + d2h}))
+                      "serial_ms": h2d + d2h, "both_chunked_ms": chunk_ms}))
 
 
 
