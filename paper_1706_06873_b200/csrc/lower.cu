@@ -416,16 +416,19 @@ __global__ void __launch_bounds__(512) lower_kernel(const LowerParams p) {
     lower_copies<T>(p, smem, static_cast<int64_t>(blockIdx.x) - n_prep);
     return;
   }
-  if (blockIdx.x >= p.n_lower_blocks) {
+  // weight-prep CTAs first here too: placed after the lowering CTAs they were
+  // scheduled last and their tile loops ran as a serial tail (cv12 / cv6,
+  // whose K is MBs, measured)
+  const int64_t n_prep = gridDim.x - p.n_lower_blocks;
+  if (blockIdx.x < n_prep) {
     const int64_t n_tiles = p.n_var * ((p.kdim_pad + 31) / 32) * ((p.kc_pad + 31) / 32);
-    for (int64_t t = blockIdx.x - p.n_lower_blocks; t < n_tiles;
-         t += gridDim.x - p.n_lower_blocks)
-      prep_weight_tile<T>(p, t);
+    for (int64_t t = blockIdx.x; t < n_tiles; t += n_prep) prep_weight_tile<T>(p, t);
     return;
   }
 
-  const int64_t n = blockIdx.x / p.bands;
-  const int64_t h0 = (blockIdx.x % p.bands) * static_cast<int64_t>(p.hb);
+  const int64_t blk = static_cast<int64_t>(blockIdx.x) - n_prep;
+  const int64_t n = blk / p.bands;
+  const int64_t h0 = (blk % p.bands) * static_cast<int64_t>(p.hb);
   const uint32_t rows = static_cast<uint32_t>(min(static_cast<int64_t>(p.hb), p.i_h - h0));
 
   uint32_t shift_elems = 0;
@@ -729,7 +732,9 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   int64_t prep_blocks = 0;
   if (Kt != nullptr) {
     const int64_t tiles = p.n_var * ((p.kdim_pad + 31) / 32) * ((pl.kc_pad + 31) / 32);
-    prep_blocks = std::min<int64_t>(tiles, 2LL * num_sms());
+    // (a 32 x 32 tile per loop trip: up to 4 CTAs per SM keep the loops short)
+    prep_blocks = std::min<int64_t>(tiles, (getenv("MEC_PREP_PER_SM") ? atoi(getenv("MEC_PREP_PER_SM")) : 4) *
+                                               static_cast<int64_t>(num_sms()));
   }
   if (L == nullptr) {  // weight operand only (fused path)
     if (prep_blocks == 0) return cudaSuccess;
