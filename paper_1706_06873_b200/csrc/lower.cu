@@ -123,6 +123,7 @@ struct LowerParams {
   int wcls;           // column-class period 16 / gcd(wstep_b, 16)
   uint32_t raw_bytes;   // smem bytes per raw band buffer (two, double-buffered)
   int64_t total_bands;  // i_n bands (the persistent CTAs loop over them)
+  bool prep_first;      // plain path: weight-prep CTAs before the lowering CTAs (large K)
   bool direct;          // aligned-copies path without the copies: every output granule is
                         // extracted from the raw band (two aligned LDS.128 per part)
 };
@@ -416,17 +417,19 @@ __global__ void __launch_bounds__(512) lower_kernel(const LowerParams p) {
     lower_copies<T>(p, smem, static_cast<int64_t>(blockIdx.x) - n_prep);
     return;
   }
-  // weight-prep CTAs first here too: placed after the lowering CTAs they were
-  // scheduled last and their tile loops ran as a serial tail (cv12 / cv6,
-  // whose K is MBs, measured)
+  // weight-prep CTAs: after the lowering CTAs (they fill the tail), or first
+  // when K is large (cv12 / cv6, MBs of K: placed last they ran their tile
+  // loops as a serial tail, measured)
   const int64_t n_prep = gridDim.x - p.n_lower_blocks;
-  if (blockIdx.x < n_prep) {
+  const int64_t prep_idx = p.prep_first ? static_cast<int64_t>(blockIdx.x)
+                                        : static_cast<int64_t>(blockIdx.x) - p.n_lower_blocks;
+  if (prep_idx >= 0 && prep_idx < n_prep) {
     const int64_t n_tiles = p.n_var * ((p.kdim_pad + 31) / 32) * ((p.kc_pad + 31) / 32);
-    for (int64_t t = blockIdx.x; t < n_tiles; t += n_prep) prep_weight_tile<T>(p, t);
+    for (int64_t t = prep_idx; t < n_tiles; t += n_prep) prep_weight_tile<T>(p, t);
     return;
   }
 
-  const int64_t blk = static_cast<int64_t>(blockIdx.x) - n_prep;
+  const int64_t blk = static_cast<int64_t>(blockIdx.x) - (p.prep_first ? n_prep : 0);
   const int64_t n = blk / p.bands;
   const int64_t h0 = (blk % p.bands) * static_cast<int64_t>(p.hb);
   const uint32_t rows = static_cast<uint32_t>(min(static_cast<int64_t>(p.hb), p.i_h - h0));
@@ -732,9 +735,16 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   int64_t prep_blocks = 0;
   if (Kt != nullptr) {
     const int64_t tiles = p.n_var * ((p.kdim_pad + 31) / 32) * ((pl.kc_pad + 31) / 32);
-    // (a 32 x 32 tile per loop trip: up to 4 CTAs per SM keep the loops short)
-    prep_blocks = std::min<int64_t>(tiles, (getenv("MEC_PREP_PER_SM") ? atoi(getenv("MEC_PREP_PER_SM")) : 4) *
-                                               static_cast<int64_t>(num_sms()));
+    // (a 32 x 32 tile per loop trip).  Measured (DESIGN.md "Weight-prep
+    // CTAs"): with >= 1024 tiles (cv12 2304, cv6 1152) the prep is the
+    // critical path: those CTAs go first, about 4 tiles each (~4 resp. 2 per
+    // SM).  Below (cv5 / cv11 ~600 tiles, C1 36) they go last, 2 per SM at
+    // most, and fill the lowering's tail.
+    p.prep_first = tiles >= 1024;
+    const int64_t per_sm = getenv("MEC_PREP_PER_SM") ? atoi(getenv("MEC_PREP_PER_SM")) : 0;
+    prep_blocks = std::min<int64_t>(tiles, per_sm > 0      ? per_sm * num_sms()
+                                           : p.prep_first ? (tiles + 3) / 4
+                                                          : 2LL * num_sms());
   }
   if (L == nullptr) {  // weight operand only (fused path)
     if (prep_blocks == 0) return cudaSuccess;
