@@ -129,34 +129,50 @@ struct LowerParams {
 };
 
 template <typename T>
-__device__ __forceinline__ void prep_weight_tile(const LowerParams& p, int64_t tile) {
+__device__ __forceinline__ void prep_weight_tile(const LowerParams& p, int64_t tile64) {
   // Kt[v][c][j] = K[j - v*delta_step][c] where 0 <= j - v*delta_step < kdim
   // and c < k_c; zero elsewhere.  32x32 tiles transposed through smem.
+  // 32-bit index math (tile, row and column indices all fit) and four loads
+  // in flight per thread before the smem stores: the 64-bit divisions and
+  // one-load-at-a-time loop made this instruction- and latency-bound
+  // (ncu, cv12 weight prep: 2600 warp instructions per tile, long-scoreboard
+  // stalls dominant).
   __shared__ T tbuf[32][33];
-  const int64_t tiles_j = (p.kdim_pad + 31) / 32;
-  const int64_t tiles_c = (p.kc_pad + 31) / 32;
-  const int64_t v = tile / (tiles_j * tiles_c);
+  const uint32_t tiles_j = static_cast<uint32_t>((p.kdim_pad + 31) / 32);
+  const uint32_t tiles_c = static_cast<uint32_t>((p.kc_pad + 31) / 32);
+  uint32_t tile = static_cast<uint32_t>(tile64);
+  const uint32_t v = tile / (tiles_j * tiles_c);
   tile -= v * tiles_j * tiles_c;
-  const int64_t jt = tile % tiles_j, ct = tile / tiles_j;
-  const int64_t delta = v * p.delta_step;
+  const uint32_t jt = tile % tiles_j, ct = tile / tiles_j;
+  const int32_t delta = static_cast<int32_t>(v * p.delta_step);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const T* K = reinterpret_cast<const T*>(p.K);
-  T* Kt = reinterpret_cast<T*>(p.Kt) + v * p.kc_pad * p.kdim_pad;
-  for (int r = ty; r < 32; r += nw) {
-    int64_t j = jt * 32 + r - delta;
-    const int64_t c = ct * 32 + tx;
-    bool ok = j >= 0;
-    if (p.kwc_pad > 0 && ok) {  // gather layout: per-kernel-row padding
-      const int64_t a = j / p.kwc_pad, rr = j - a * p.kwc_pad;
-      ok = rr < p.kwc_src;
-      j = a * p.kwc_src + rr;
+  T* Kt = reinterpret_cast<T*>(p.Kt) + static_cast<int64_t>(v) * p.kc_pad * p.kdim_pad;
+  const int32_t kdim = static_cast<int32_t>(p.kdim), k_c = static_cast<int32_t>(p.k_c);
+  const int32_t kwc_pad = static_cast<int32_t>(p.kwc_pad), kwc_src = static_cast<int32_t>(p.kwc_src);
+  const int32_t c = static_cast<int32_t>(ct * 32 + tx);
+  for (int r0 = ty; r0 < 32; r0 += 4 * nw) {
+    T val[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = r0 + k * nw;
+      int32_t j = static_cast<int32_t>(jt * 32) + r - delta;
+      bool ok = r < 32 && j >= 0;
+      if (kwc_pad > 0 && ok) {  // gather layout: per-kernel-row padding
+        const int32_t a = j / kwc_pad, rr = j - a * kwc_pad;
+        ok = rr < kwc_src;
+        j = a * kwc_src + rr;
+      }
+      val[k] = (ok && j < kdim && c < k_c) ? K[static_cast<int64_t>(j) * k_c + c] : T(0);
     }
-    tbuf[r][tx] = (ok && j < p.kdim && c < p.k_c) ? K[j * p.k_c + c] : T(0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (r0 + k * nw < 32) tbuf[r0 + k * nw][tx] = val[k];
   }
   __syncthreads();
   for (int r = ty; r < 32; r += nw) {
-    const int64_t c = ct * 32 + r, j = jt * 32 + tx;
-    if (c < p.kc_pad && j < p.kdim_pad) Kt[c * p.kdim_pad + j] = tbuf[tx][r];
+    const int64_t cc = ct * 32 + r, jj = jt * 32 + tx;
+    if (cc < p.kc_pad && jj < p.kdim_pad) Kt[cc * p.kdim_pad + jj] = tbuf[tx][r];
   }
   __syncthreads();
 }
