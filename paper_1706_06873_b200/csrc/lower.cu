@@ -124,6 +124,7 @@ struct LowerParams {
   uint32_t raw_bytes;   // smem bytes per raw band buffer (two, double-buffered)
   int64_t total_bands;  // i_n bands (the persistent CTAs loop over them)
   bool prep_first;      // plain path: weight-prep CTAs before the lowering CTAs (large K)
+  bool prep64;          // weight prep in 64 x 64 tiles with 16-byte vectors (bf16, k_c % 8 == 0)
   bool direct;          // aligned-copies path without the copies: every output granule is
                         // extracted from the raw band (two aligned LDS.128 per part)
 };
@@ -175,6 +176,73 @@ __device__ __forceinline__ void prep_weight_tile(const LowerParams& p, int64_t t
     if (cc < p.kc_pad && jj < p.kdim_pad) Kt[cc * p.kdim_pad + jj] = tbuf[tx][r];
   }
   __syncthreads();
+}
+
+constexpr uint32_t kPrep64Stride = 66;  // elements per smem row (odd word count: 33)
+constexpr size_t kPrep64Smem = 64 * kPrep64Stride * 2;
+
+// The same Kt as prep_weight_tile, in 64 (j) x 64 (c) tiles of 2-byte elements:
+// 16-byte loads along c (k_c % 8 == 0, so a vector is wholly in or out of
+// range) into the launch's dynamic shared memory, then 16-byte stores along j
+// (kdim_pad % 64 == 0), eight lanes per 128-byte row segment of Kt.
+__device__ __forceinline__ void prep_weight_tile64(const LowerParams& p, uint32_t tile, unsigned char* sm) {
+  uint16_t* tb = reinterpret_cast<uint16_t*>(sm);
+  const uint32_t tiles_j = static_cast<uint32_t>(p.kdim_pad / 64);
+  const uint32_t tiles_c = static_cast<uint32_t>((p.kc_pad + 63) / 64);
+  const uint32_t v = tile / (tiles_j * tiles_c);
+  tile -= v * tiles_j * tiles_c;
+  const uint32_t jt = tile % tiles_j, ct = tile / tiles_j;
+  const int32_t delta = static_cast<int32_t>(v * p.delta_step);
+  const uint16_t* K = reinterpret_cast<const uint16_t*>(p.K);
+  uint16_t* Kt = reinterpret_cast<uint16_t*>(p.Kt) + static_cast<int64_t>(v) * p.kc_pad * p.kdim_pad;
+  const int32_t kdim = static_cast<int32_t>(p.kdim), k_c = static_cast<int32_t>(p.k_c);
+  const int32_t kwc_pad = static_cast<int32_t>(p.kwc_pad), kwc_src = static_cast<int32_t>(p.kwc_src);
+  for (uint32_t i = threadIdx.x; i < 512; i += blockDim.x) {
+    const uint32_t r = i >> 3, cv = i & 7;
+    int32_t j = static_cast<int32_t>(jt * 64 + r) - delta;
+    const int32_t c = static_cast<int32_t>(ct * 64 + cv * 8);
+    bool ok = j >= 0;
+    if (kwc_pad > 0 && ok) {  // gather / strip-padded layout: per-kernel-row padding
+      const int32_t a = j / kwc_pad, rr = j - a * kwc_pad;
+      ok = rr < kwc_src;
+      j = a * kwc_src + rr;
+    }
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (ok && j < kdim && c < k_c) val = *reinterpret_cast<const uint4*>(K + static_cast<int64_t>(j) * k_c + c);
+    uint32_t* d = reinterpret_cast<uint32_t*>(tb + r * kPrep64Stride + cv * 8);
+    d[0] = val.x;
+    d[1] = val.y;
+    d[2] = val.z;
+    d[3] = val.w;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < 512; i += blockDim.x) {
+    const uint32_t jv = i & 7, cr = i >> 3;
+    const int64_t c = static_cast<int64_t>(ct) * 64 + cr;
+    if (c < p.kc_pad) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        w[q] = static_cast<uint32_t>(tb[(jv * 8 + 2 * q) * kPrep64Stride + cr]) |
+               (static_cast<uint32_t>(tb[(jv * 8 + 2 * q + 1) * kPrep64Stride + cr]) << 16);
+      *reinterpret_cast<uint4*>(Kt + c * p.kdim_pad + jt * 64 + jv * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ int64_t prep_units(const LowerParams& p) {
+  if (sizeof(T) == 2 && p.prep64) return p.n_var * (p.kdim_pad / 64) * ((p.kc_pad + 63) / 64);
+  return p.n_var * ((p.kdim_pad + 31) / 32) * ((p.kc_pad + 31) / 32);
+}
+
+template <typename T>
+__device__ __forceinline__ void prep_unit(const LowerParams& p, int64_t t, unsigned char* sm) {
+  if (sizeof(T) == 2 && p.prep64)
+    prep_weight_tile64(p, static_cast<uint32_t>(t), sm);
+  else
+    prep_weight_tile<T>(p, t);
 }
 
 // bytes [4 KK + sh_b / 8, + 16) of the 32-byte little-endian string x:y
@@ -426,8 +494,8 @@ __global__ void __launch_bounds__(512) lower_kernel(const LowerParams p) {
     // scheduled first instead of waiting for a free slot at the end
     const int64_t n_prep = gridDim.x - p.n_lower_blocks;
     if (blockIdx.x < n_prep) {
-      const int64_t n_tiles = p.n_var * ((p.kdim_pad + 31) / 32) * ((p.kc_pad + 31) / 32);
-      for (int64_t t = blockIdx.x; t < n_tiles; t += n_prep) prep_weight_tile<T>(p, t);
+      const int64_t n_tiles = prep_units<T>(p);
+      for (int64_t t = blockIdx.x; t < n_tiles; t += n_prep) prep_unit<T>(p, t, smem);
       return;
     }
     lower_copies<T>(p, smem, static_cast<int64_t>(blockIdx.x) - n_prep);
@@ -440,8 +508,8 @@ __global__ void __launch_bounds__(512) lower_kernel(const LowerParams p) {
   const int64_t prep_idx = p.prep_first ? static_cast<int64_t>(blockIdx.x)
                                         : static_cast<int64_t>(blockIdx.x) - p.n_lower_blocks;
   if (prep_idx >= 0 && prep_idx < n_prep) {
-    const int64_t n_tiles = p.n_var * ((p.kdim_pad + 31) / 32) * ((p.kc_pad + 31) / 32);
-    for (int64_t t = prep_idx; t < n_tiles; t += n_prep) prep_weight_tile<T>(p, t);
+    const int64_t n_tiles = prep_units<T>(p);
+    for (int64_t t = prep_idx; t < n_tiles; t += n_prep) prep_unit<T>(p, t, smem);
     return;
   }
 
@@ -757,19 +825,25 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
     // SM).  Below (cv5 / cv11 ~600 tiles, C1 36) they go last, 2 per SM at
     // most, and fill the lowering's tail.
     p.prep_first = tiles >= 1024;
+    // 64 x 64 tiles (one per prep CTA when they go first) where the vectors fit
+    p.prep64 = pl.elt == 2 && s.k_c % 8 == 0 && p.kdim_pad % 64 == 0 &&
+               reinterpret_cast<uintptr_t>(K) % 16 == 0 && reinterpret_cast<uintptr_t>(Kt) % 16 == 0 &&
+               !getenv("MEC_PREP32");
+    const int64_t units = p.prep64 ? p.n_var * (p.kdim_pad / 64) * ((pl.kc_pad + 63) / 64) : tiles;
     const int64_t per_sm = getenv("MEC_PREP_PER_SM") ? atoi(getenv("MEC_PREP_PER_SM")) : 0;
-    prep_blocks = std::min<int64_t>(tiles, per_sm > 0      ? per_sm * num_sms()
-                                           : p.prep_first ? (tiles + 3) / 4
+    prep_blocks = std::min<int64_t>(units, per_sm > 0      ? per_sm * num_sms()
+                                           : p.prep_first ? (p.prep64 ? units : (units + 3) / 4)
                                                           : 2LL * num_sms());
   }
+  const size_t prep_smem = p.prep64 ? kPrep64Smem : 64;
   if (L == nullptr) {  // weight operand only (fused path)
     if (prep_blocks == 0) return cudaSuccess;
     LowerParams q = p;
     q.n_lower_blocks = 0;
     if (pl.elt == 2)
-      lower_kernel<uint16_t><<<static_cast<unsigned>(prep_blocks), 256, 64, st>>>(q);
+      lower_kernel<uint16_t><<<static_cast<unsigned>(prep_blocks), 256, prep_smem, st>>>(q);
     else
-      lower_kernel<uint32_t><<<static_cast<unsigned>(prep_blocks), 256, 64, st>>>(q);
+      lower_kernel<uint32_t><<<static_cast<unsigned>(prep_blocks), 256, prep_smem, st>>>(q);
     if (launches) ++*launches;
     return cudaGetLastError();
   }
@@ -785,9 +859,9 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
       LowerParams q = p;
       q.n_lower_blocks = 0;
       if (pl.elt == 2)
-        lower_kernel<uint16_t><<<static_cast<unsigned>(prep_blocks), 256, 64, st>>>(q);
+        lower_kernel<uint16_t><<<static_cast<unsigned>(prep_blocks), 256, prep_smem, st>>>(q);
       else
-        lower_kernel<uint32_t><<<static_cast<unsigned>(prep_blocks), 256, 64, st>>>(q);
+        lower_kernel<uint32_t><<<static_cast<unsigned>(prep_blocks), 256, prep_smem, st>>>(q);
       if (launches) ++*launches;
     }
     const int64_t total = s.i_n * pl.o_w * pl.l_cols;
@@ -927,6 +1001,7 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   if (grid > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
   if (spad && p.ncls == 0) return launch_direct();
   set_lower_attributes();
+  if (p.prep64 && prep_blocks > 0) smem = std::max(smem, kPrep64Smem);
   if (smem > kLowerMaxSmem) return cudaErrorInvalidConfiguration;
   if (pl.elt == 2)
     lower_kernel<uint16_t><<<static_cast<unsigned>(grid), threads, smem, st>>>(p);
