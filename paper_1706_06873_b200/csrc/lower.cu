@@ -829,6 +829,7 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
     p.prep64 = pl.elt == 2 && s.k_c % 8 == 0 && p.kdim_pad % 64 == 0 &&
                reinterpret_cast<uintptr_t>(K) % 16 == 0 && reinterpret_cast<uintptr_t>(Kt) % 16 == 0 &&
                !getenv("MEC_PREP32");
+    if (const char* e = getenv("MEC_PREP_FIRST")) p.prep_first = atoi(e) != 0;  // (experiments)
     const int64_t units = p.prep64 ? p.n_var * (p.kdim_pad / 64) * ((pl.kc_pad + 63) / 64) : tiles;
     const int64_t per_sm = getenv("MEC_PREP_PER_SM") ? atoi(getenv("MEC_PREP_PER_SM")) : 0;
     prep_blocks = std::min<int64_t>(units, per_sm > 0      ? per_sm * num_sms()
