@@ -187,6 +187,12 @@ def test_host_call_scratch_layout_and_validation():
         wsb = L.mec_workspace_bytes(ctypes.byref(sub), 4, 4, bf)
         want = up(k_b) + slots * (up(i_img * per) + up(o_img * per)) + wsb + 1024
         assert L.mec_host_scratch_bytes(ctypes.byref(s), 4, 4, bf, None, nch) == want, nch
+    # n_chunks is clamped to [1, i_n]
+    one = L.mec_host_scratch_bytes(ctypes.byref(s), 4, 4, bf, None, 1)
+    assert L.mec_host_scratch_bytes(ctypes.byref(s), 4, 4, bf, None, 0) == one
+    assert L.mec_host_scratch_bytes(ctypes.byref(s), 4, 4, bf, None, -5) == one
+    assert (L.mec_host_scratch_bytes(ctypes.byref(s), 4, 4, bf, None, 1000)
+            == L.mec_host_scratch_bytes(ctypes.byref(s), 4, 4, bf, None, 32))
     bad = _lib.MecShape(1, 2, 2, 1, 3, 3, 1)
     assert L.mec_host_scratch_bytes(ctypes.byref(bad), 1, 1, bf, None, 1) == 0
     fake = ctypes.c_void_p(0x1000)
