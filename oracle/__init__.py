@@ -8,18 +8,25 @@ CUDA path); neither imports the other.  Every function cites the PAPER.md
 passage it follows (``P:<line>``); the readings of ambiguous passages are
 listed in DESIGN.md section 3.
 
-Parity status of each function (what pins it, see tests/test_oracle_*.py):
+Parity status of every exported function (the pins live in
+tests/test_oracle_pins.py; none of them re-calls the oracle's own formula):
   out_dims        -- Eq.1; Fig.1 caption (7,3,1 -> 5); Table 3 cv4 (floor)
-  elems_*         -- Fig.1/Fig.2 sizes (25x9, 5x21); Table 3 MEM column; Eq.4
-  select_path     -- Alg.2 l.8 evaluated by hand for the BASELINE configs
+  elems_L_mec,
+  elems_L_im2col  -- Fig.1/Fig.2 sizes (25x9, 5x21); Table 3 MEM column; Eq.4
+  elems_O         -- the #O > #L refusal cases of Alg.2 l.8 (cv3, cv7)
+  select_path     -- Alg.2 l.8 evaluated by hand for the BASELINE configs,
+                     inclusive threshold
   direct_conv     -- ramp closed form; torch.nn.functional.conv2d (fp64);
                      1x1 == GEMM; k == i == dot products
-  im2col          -- Fig.1(b) 25x9; row contents vs direct indexing
+  im2col          -- Fig.1(b) 25x9; numpy matmul of it == torch conv2d
   lower           -- Fig.2 partitions A=I[0:7,0:3], B=I[0:7,1:4];
-                     horizontal-redundancy invariant; 1x1 == transpose
+                     numpy sliding windows; horizontal-redundancy invariant;
+                     1x1 == transpose
   vanilla_mec     -- == direct conv on Fig.1 shapes; P/Q partitions
-  conv_solA/solB  -- == torch conv2d (fp64) on random tiny shapes
-No function is "parity unpinned".
+  conv_solA/solB,
+  mec             -- == torch conv2d (fp64) on random tiny shapes; A == B
+No function is "parity unpinned".  (Round 2 removed an unused plain matmul
+helper that had no pin of its own.)
 """
 from __future__ import annotations
 
@@ -72,8 +79,6 @@ def _load():
             lib.mec_oracle_select_path.argtypes = [sp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
             lib.mec_oracle_direct_conv.argtypes = [dp, dp, dp, sp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
             lib.mec_oracle_im2col.argtypes = [dp, dp, sp, ctypes.c_int, ctypes.c_int]
-            lib.mec_oracle_matmul.argtypes = [dp, dp, dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
-            lib.mec_oracle_matmul.restype = None
             lib.mec_oracle_lower.argtypes = [ctypes.c_void_p, ctypes.c_void_p, sp, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_size_t]
             lib.mec_oracle_vanilla_mec.argtypes = [dp, dp, dp] + [ctypes.c_int64] * 4 + [ctypes.c_int] * 2
@@ -153,15 +158,6 @@ def im2col(I: np.ndarray, k_h: int, k_w: int, s_h: int, s_w: int) -> np.ndarray:
     oh, ow = out_dims(shp, s_h, s_w)
     C = np.empty((I.shape[0] * oh * ow, k_h * k_w * I.shape[3]), dtype=np.float64)
     _check(_load().mec_oracle_im2col(_dptr(I), _dptr(C), ctypes.byref(_shape(shp)), s_h, s_w))
-    return C
-
-
-def matmul(A: np.ndarray, B: np.ndarray) -> np.ndarray:
-    """Plain triple-loop fp64 matmul."""
-    A = np.ascontiguousarray(A, dtype=np.float64)
-    B = np.ascontiguousarray(B, dtype=np.float64)
-    C = np.empty((A.shape[0], B.shape[1]), dtype=np.float64)
-    _load().mec_oracle_matmul(_dptr(A), _dptr(B), _dptr(C), A.shape[0], A.shape[1], B.shape[1])
     return C
 
 

@@ -167,16 +167,6 @@ int mec_oracle_im2col(const double* I, double* C, const mec_oracle_shape* s,
   return 0;
 }
 
-void mec_oracle_matmul(const double* A, const double* B, double* C, int64_t m,
-                       int64_t k, int64_t n) {
-  for (int64_t i = 0; i < m; ++i)
-    for (int64_t j = 0; j < n; ++j) {
-      double acc = 0.0;
-      for (int64_t p = 0; p < k; ++p) acc += A[i * k + p] * B[p * n + j];
-      C[i * n + j] = acc;
-    }
-}
-
 /* Sub-matrix GEMM in the BLAS style of Sec. 2.1: A is the p x q
  * sub-matrix with top-left element *A and leading dimension lda; B is q x r
  * with leading dimension r; C is p x r with leading dimension ldc. */

@@ -55,10 +55,6 @@ int mec_oracle_direct_conv(const double* I, const double* K, double* O,
 int mec_oracle_im2col(const double* I, double* C, const mec_oracle_shape* s,
                       int s_h, int s_w);
 
-/* Plain triple-loop C = A (m x k) * B (k x n), row-major, double. */
-void mec_oracle_matmul(const double* A, const double* B, double* C,
-                       int64_t m, int64_t k, int64_t n);
-
 /* MEC compact lowering, Alg.2 l.3-6:
  *   L[n,w,h,0:k_w,0:i_c] = I[n,h,s_w w : s_w w + k_w, 0:i_c]
  * for n < i_n, w < o_w, h < i_h (all input rows: reading Q5).
