@@ -6,16 +6,22 @@ batch: compact lowering (+ weight operand prep) -> window GEMMs (paper
 Solution A or B by the threshold rule of Alg.2 l.8) -> Solution A's format
 fix, i.e. one mec_conv_forward_ex call through the C ABI.
 
-Default workload (N=1): BASELINE.json configs[1], AlexNet conv1 (Table 2 cv1)
-I 32x227x227x3, K 11x11x3x96, stride 4, bf16.  Synthetic inputs from the
-counter-based generator (synth/), generated on the device.  Multi-GPU
-(torchrun, one process per GPU): each rank processes its own batch of the
-same size (weak scaling; global images r*i_n .. (r+1)*i_n), K is broadcast
-once from rank 0 with NCCL, no other collective on the path; time = max over
-ranks of the device-timed steps.
+Default workload (N=1): BASELINE.json configs[2], VGG-16 conv1_2
+I 64x224x224x64, K 3x3x64x64, stride 1 -- the largest single-GPU config --
+in bf16 (the JSON line's `value`), with the same config in tf32 (closest to
+the paper's fp32) measured in the same run and reported under "tf32".
+Synthetic inputs from the counter-based generator (synth/), generated on the
+device.
+
+Multi-GPU (torchrun, one process per GPU; Alg.2 runs every loop "in parallel"
+over the images): --scaling strong (default) shards the
+configured global batch i_n over the ranks with dist.shard (rank r owns the
+global images [r i_n/g, (r+1) i_n/g)); --scaling weak gives every rank a full
+batch of its own.  K is broadcast once from rank 0 with NCCL, no other
+collective is on the path; time = max over ranks of the device-timed steps.
 
 L2 (126 MB) is flushed before every timed step (a 2x L2 write, then a 2x L2
-read so the write's dirty lines are written back outside the step's CUDA events): C1's working set fits in L2.
+read so the write's dirty lines are written back outside the step's events).
 
 --impl reference: the CPU oracle (oracle/, plain C fp64) timed on this box's
 host cores on a bounded sample of the same workload (rank 0 only).
@@ -36,16 +42,20 @@ sys.path.insert(0, ROOT)
 
 METRIC = "conv TFLOP/s (2·N·OH·OW·KH·KW·IC·KC/t) + lowered bytes vs im2col, 1/2/4/8 B200"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+# configs measured a second time in tf32 in the same run (BASELINE.json configs[2]: "bf16 and tf32")
+TF32_SIBLING = {"C2": "C2_tf32"}
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["mec", "reference"], default="mec")
-    ap.add_argument("--config", default="C1", help="synth.configs.CONFIGS key (default C1)")
-    ap.add_argument("--batch", type=int, default=None, help="override images per GPU")
+    ap.add_argument("--config", default="C2", help="synth.configs.CONFIGS key (default C2)")
+    ap.add_argument("--batch", type=int, default=None, help="override the global batch i_n")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: shard the global batch over the ranks; weak: a full batch per rank")
     ap.add_argument("--path", choices=["auto", "A", "B", "fused"], default="auto")
     ap.add_argument("--sola-fix", choices=["epilogue", "literal"], default="epilogue")
     ap.add_argument("--T", type=int, default=100)
@@ -53,12 +63,14 @@ def parse():
                     help="window GEMM output rows per tile (multi-row schedule; 0 = library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tf32", action="store_true", help="skip the tf32 variant of the config")
+    ap.add_argument("--no-tf32-peak", action="store_true", help="skip the in-run tf32 peak measurement")
     ap.add_argument("--e2e-chunks", type=int, default=4,
                     help="image chunks of the e2e host-buffer call (copies pipelined with the kernels)")
     ap.add_argument("--no-flush", action="store_true", help="(diagnostic) do not flush L2")
     ap.add_argument("--no-fused-alt", action="store_true",
                     help="with --path auto, skip measuring the fused path alongside (north_star (3))")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def load_peaks():
@@ -70,6 +82,16 @@ def load_peaks():
     return dict(FALLBACK_PEAKS), "fallback (B200_PROFILING.md)"
 
 
+def load_ncu(workload_name):
+    """Per-kernel ncu metrics of this workload from the committed captures
+    (profiles/ncu_metrics.json, written by tools/profile_summary.py)."""
+    p = os.path.join(ROOT, "profiles", "ncu_metrics.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        return json.load(f).get(workload_name, {})
+
+
 def workload(cfg):
     i_n, i_h, i_w, i_c = cfg["i_n"], cfg["i_h"], cfg["i_w"], cfg["i_c"]
     k_h, k_w, k_c, s_h, s_w = cfg["k_h"], cfg["k_w"], cfg["k_c"], cfg["s_h"], cfg["s_w"]
@@ -79,6 +101,22 @@ def workload(cfg):
     return dict(shape=(i_n, i_h, i_w, i_c, k_h, k_w, k_c), o_h=o_h, o_w=o_w, flops=flops,
                 nI=i_n * i_h * i_w * i_c, nK=k_h * k_w * i_c * k_c, nO=i_n * o_h * o_w * k_c,
                 nL=i_n * o_w * i_h * k_w * i_c, nIm2col=i_n * o_h * o_w * k_h * k_w * i_c)
+
+
+def rank_work(global_batch: int, rank: int, ws: int, scaling: str) -> dict:
+    """The images this rank processes (host logic, tested on CPU with gloo).
+
+    strong: the configured global batch is sharded (dist.shard), rank r owns
+    global images [b, e); weak: every rank runs a full batch of its own, at
+    global images [r B, (r+1) B).  `index_offset_images` is the global image
+    index of the rank's first image (the synthetic generator indexes globally,
+    so every shard is a slice of the single-GPU tensor)."""
+    from paper_1706_06873_b200 import dist
+
+    if scaling == "strong":
+        b, e = dist.shard(global_batch, rank, ws)
+        return {"n0": b, "n_local": e - b, "global_batch": global_batch}
+    return {"n0": rank * global_batch, "n_local": global_batch, "global_batch": global_batch * ws}
 
 
 class ClockSampler:
@@ -104,7 +142,6 @@ class ClockSampler:
         self._stop = threading.Event()
 
     def _poll(self):
-        nv = self.nv
         while not self._stop.is_set():
             self.sample_once()
             time.sleep(0.002)
@@ -145,11 +182,22 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def cpu_sample_plan(t1_s: float, cores: int, i_n: int, run_target_s: float = 1.0,
+                    budget_s: float = 60.0) -> dict:
+    """n_sub images so one threaded run takes >= ~1 s; the mean of
+    10 runs (the paper's method) when both timed functions fit the
+    budget, else 3 runs.  t1_s = one image on one core."""
+    n_img = max(1, min(i_n, 4 * cores, math.ceil(run_target_s * cores / max(t1_s, 1e-4))))
+    threads = max(1, min(cores, n_img))
+    run_s = t1_s * math.ceil(n_img / threads)
+    runs = 10 if 2 * 10 * run_s <= budget_s else 3
+    return {"images": n_img, "threads": threads, "runs": runs, "est_run_s": run_s}
+
+
 def cpu_baseline(cfg, w, dtype_name, seed):
     """The oracle (as it stands) on a bounded sample of the workload: Alg.2
-    lowering + Solution-B window GEMMs in fp64, threads over images."""
-    import numpy as np
-
+    lowering + Solution-B window GEMMs (oracle.conv_solB), and the direct
+    convolution definition (oracle.direct_conv), fp64, threads over images."""
     import oracle
     import synth
 
@@ -157,30 +205,34 @@ def cpu_baseline(cfg, w, dtype_name, seed):
     kind = synth.KIND_GRID8 if dtype_name == "bf16" else synth.KIND_GRID11
     K = synth.kernel_tensor(cfg, kind, seed)
     per_img = w["flops"] / cfg["i_n"]
-    # calibrate with one image on one core, then size the sample to ~10-20 s of CPU work
     I1 = synth.input_images(cfg, 0, 1, kind, seed)
     t0 = time.perf_counter()
     oracle.conv_solB(I1, K, cfg["s_h"], cfg["s_w"], n_threads=1)
     t1 = time.perf_counter() - t0
-    n_img = int(max(1, min(cfg["i_n"], round(12.0 * cores / max(t1, 1e-3)))))
-    n_img = max(1, min(n_img, 4 * cores, cfg["i_n"]))
-    threads = min(cores, n_img)
+    plan = cpu_sample_plan(t1, cores, cfg["i_n"])
+    n_img, threads, runs = plan["images"], plan["threads"], plan["runs"]
     I = synth.input_images(cfg, 0, n_img, kind, seed)
-    t0 = time.perf_counter()
-    oracle.conv_solB(I, K, cfg["s_h"], cfg["s_w"], n_threads=threads)
-    dt = time.perf_counter() - t0
-    val = n_img * per_img / dt / 1e12
+    out = {}
+    for name, fn in (("conv_solB", oracle.conv_solB), ("direct_conv", oracle.direct_conv)):
+        ts = []
+        for _ in range(runs):
+            t0 = time.perf_counter()
+            fn(I, K, cfg["s_h"], cfg["s_w"], n_threads=threads)
+            ts.append(time.perf_counter() - t0)
+        m = statistics.mean(ts)
+        out[name] = {"mean_s": m, "runs": runs, "tflops": n_img * per_img / m / 1e12,
+                     "s_per_image": m / n_img}
+    val = out["conv_solB"]["tflops"]
     return {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-            "sample": f"{n_img} of {cfg['i_n']} images of {cfg['name']}: oracle.conv_solB "
-                      f"(Alg.2 lowering + Solution B window GEMMs, plain C, fp64), {threads} threads, "
-                      f"{dt:.2f} s; the extrapolated full-batch time is {dt * cfg['i_n'] / n_img:.1f} s",
-            "seconds": dt, "images": n_img, "host_cores_total": cores}
+            "sample": f"{n_img} of {cfg['i_n']} images of {cfg['name']} per run, mean of {runs} runs: "
+                      f"oracle.conv_solB (Alg.2 lowering + Solution B window GEMMs, plain C, fp64), "
+                      f"{threads} threads; oracle.direct_conv timed the same way",
+            "images": n_img, "host_cores_total": cores, "functions": out,
+            "extrapolated_full_batch_s": out["conv_solB"]["mean_s"] * cfg["i_n"] / n_img}
 
 
 def run_reference(args):
     """--impl reference: the CPU oracle on the box's host cores (rank 0 only)."""
-    import numpy as np  # noqa: F401
-
     import oracle
     import synth
 
@@ -195,7 +247,6 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     K = synth.kernel_tensor(cfg, kind, seed)
     per_img = w["flops"] / cfg["i_n"]
-    # bounded sample per step: one image per core (at most i_n), ~1-3 s of CPU work
     I1 = synth.input_images(cfg, 0, 1, kind, seed)
     t0 = time.perf_counter()
     oracle.conv_solB(I1, K, cfg["s_h"], cfg["s_w"], n_threads=1)
@@ -219,9 +270,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (counter-based generator, seed %d)" % seed,
-        "config": {"workload": cfg["name"], "sample_images_per_step": n_img},
+        "config": {"workload": cfg["name"], "global_batch": cfg["i_n"], "sample_images_per_step": n_img,
+                   "same_config": n_img == cfg["i_n"]},
         "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -230,11 +282,35 @@ def run_reference(args):
     return 0
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
+def measure_tf32_peak(dev):
+    """tf32 dense peak measured the MEASURED_PEAKS way -- torch.matmul
+    fp32 with allow_tf32, 8192^3, best of 10 (a measurement, not on the path)."""
+    import torch
 
+    prev = torch.backends.cuda.matmul.allow_tf32
+    try:
+        torch.backends.cuda.matmul.allow_tf32 = True
+        n = 8192
+        a = torch.randn(n, n, device=dev)
+        b = torch.randn(n, n, device=dev)
+        for _ in range(3):
+            torch.matmul(a, b)
+        best = float("inf")
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return 2 * n ** 3 / (best * 1e-3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def measure(args, cfg, rw, rank, ws, dev, peaks, peak_src, tf32_peak, primary=True):
+    """Times the hot path on this rank's images of `cfg`; returns the line fields."""
     import torch
 
     import synth
@@ -243,11 +319,9 @@ def main():
                                             MEC_PATH_SOLUTION_B, MEC_SOLA_FIX_EPILOGUE, MEC_SOLA_FIX_LITERAL,
                                             MecError)
 
-    rank, ws, dev = dist.init()
-    if dev.type != "cuda":
-        raise SystemExit("bench.py needs CUDA GPUs (no CPU fallback)")
-    cfg = synth.config(args.config, args.batch)
-    w = workload(cfg)
+    cfg_local = dict(cfg, i_n=rw["n_local"])
+    w = workload(cfg_local)
+    w_glob = workload(dict(cfg, i_n=rw["global_batch"]))
     dtype_name = "bf16" if cfg["dtype"] == "bf16" else "tf32"
     tdt = torch.bfloat16 if dtype_name == "bf16" else torch.float32
     elt = 2 if dtype_name == "bf16" else 4
@@ -258,10 +332,11 @@ def main():
     path = {"auto": MEC_PATH_AUTO, "A": MEC_PATH_SOLUTION_A, "B": MEC_PATH_SOLUTION_B,
             "fused": MEC_PATH_FUSED}[args.path]
     fix = MEC_SOLA_FIX_EPILOGUE if args.sola_fix == "epilogue" else MEC_SOLA_FIX_LITERAL
+    K_steps = args.steps
 
     # ---- inputs: this rank's images (global index offset), K from rank 0 by NCCL broadcast
     I = torch.empty((i_n, i_h, i_w, i_c), dtype=tdt, device=dev)
-    mec.synth_fill(I, seed, synth.TENSOR_I, kind, index_offset=rank * i_n * i_h * i_w * i_c)
+    mec.synth_fill(I, seed, synth.TENSOR_I, kind, index_offset=rw["n0"] * i_h * i_w * i_c)
     K = torch.empty((k_h, k_w, i_c, k_c), dtype=tdt, device=dev)
     if rank == 0:
         mec.synth_fill(K, seed, synth.TENSOR_K, kind)
@@ -278,11 +353,13 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def step(evs=None):
-        return mec.conv_forward(I, K, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, rows_per_tile=args.rows_per_tile,
-                                workspace=workspace, stage_events=evs, return_path=True)
+        return mec.conv_forward(I, K, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix,
+                                rows_per_tile=args.rows_per_tile, workspace=workspace, stage_events=evs,
+                                return_path=True, return_gemm=True)
 
-    # ---- memory: device-memory delta of one pooled call (library allocates L itself)
+    # ---- memory: device-memory delta of one pooled call (the library allocates L itself)
     torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)
     free0 = torch.cuda.mem_get_info(dev)[0]
     mec.conv_forward(I, K, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, rows_per_tile=args.rows_per_tile)
     torch.cuda.synchronize()
@@ -293,14 +370,13 @@ def main():
     for _ in range(max(args.warmup, 0)):
         if not args.no_flush:
             mec.l2_flush(flush)
-        _, chosen = step()
+        _, chosen, gemm_kernel = step()
     torch.cuda.synchronize()
     launches_per_step = mec.last_launch_count()
 
     # ---- timed region: K steps, CUDA events on the launching stream around each
     # step only (events between the step's kernels would serialise the window
     # GEMM's programmatic dependent launch)
-    K_steps = args.steps
     sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K_steps)]
     sampler = ClockSampler(dev.index)
     dist.barrier()
@@ -316,7 +392,7 @@ def main():
     dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in sev]
     tot_ms = dist.max_over_ranks(sum(step_ms), dev)
-    value = w["flops"] * ws * K_steps / (tot_ms * 1e-3) / 1e12
+    value = w_glob["flops"] * K_steps / (tot_ms * 1e-3) / 1e12
 
     # ---- per-kernel times (roofline): K more steps with the library's stage
     # events between the kernels (kernels serialised, so each is timed alone)
@@ -332,38 +408,41 @@ def main():
     torch.cuda.synchronize()
     lower_ms = [e[0].elapsed_time(e[1]) for e in evs]
     gemm_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    fix_ms = [e[2].elapsed_time(e[3]) for e in evs]
+    literal = chosen == MEC_PATH_SOLUTION_A and fix == MEC_SOLA_FIX_LITERAL
+    fix_ms = [e[2].elapsed_time(e[3]) for e in evs] if literal else None
 
     # ---- CUDA-graph replay of the same step (launch gaps removed), diagnostic
     graph_ms = None
-    try:
-        g = torch.cuda.CUDAGraph()
-        s2 = torch.cuda.Stream(dev)
-        s2.wait_stream(stream)
-        with torch.cuda.stream(s2):
-            step()
-            with torch.cuda.graph(g, stream=s2):
+    if primary:
+        try:
+            g = torch.cuda.CUDAGraph()
+            s2 = torch.cuda.Stream(dev)
+            s2.wait_stream(stream)
+            with torch.cuda.stream(s2):
                 step()
-        stream.wait_stream(s2)
-        torch.cuda.synchronize()
-        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(K_steps)]
-        for a, b in gev:
-            if not args.no_flush:
-                mec.l2_flush(flush)
-            a.record()
-            g.replay()
-            b.record()
-        torch.cuda.synchronize()
-        graph_ms = statistics.mean(a.elapsed_time(b) for a, b in gev)
-    except Exception as e:  # noqa: BLE001
-        graph_ms = f"unavailable: {e}"
+                with torch.cuda.graph(g, stream=s2):
+                    step()
+            stream.wait_stream(s2)
+            torch.cuda.synchronize()
+            gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(K_steps)]
+            for a, b in gev:
+                if not args.no_flush:
+                    mec.l2_flush(flush)
+                a.record()
+                g.replay()
+                b.record()
+            torch.cuda.synchronize()
+            graph_ms = statistics.mean(a.elapsed_time(b) for a, b in gev)
+            del g
+        except Exception as e:  # noqa: BLE001
+            graph_ms = f"unavailable: {e}"
 
     # ---- end to end through the public API with host buffers (pinned), copies timed:
     # mec_conv_forward_host copies I and K in and O out inside the call, pipelined over
     # image chunks on three streams (the copies of neighbouring chunks overlap the kernels)
     e2e = None
-    if not args.no_e2e:
+    if primary and not args.no_e2e:
         I_h = I.cpu().pin_memory()
         K_h = K.cpu().pin_memory()
         O_h = torch.empty(O.shape, dtype=O.dtype).pin_memory()
@@ -392,18 +471,18 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
         e2e_ms = dist.max_over_ranks(sum(a.elapsed_time(b) for a, b in eev), dev)
-        e2e = {"value": w["flops"] * ws * K_steps / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+        e2e = {"value": w_glob["flops"] * K_steps / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": (w["nI"] + w["nK"]) * elt, "d2h_bytes_per_step": w["nO"] * elt,
                "ms_per_step": e2e_ms / K_steps, "api": "mec_conv_forward_host",
                "chunks": nch, "kernels_per_step": e2e_launches / K_steps}
+        del I_h, K_h, O_h, scratch
 
-    # ---- roofline of the dominant kernel
-    peaks, peak_src = load_peaks()
+    # ---- roofline of the dominant kernel (algorithmic bytes / flops per launch)
     mean_lower = statistics.mean(lower_ms)
     mean_gemm = statistics.mean(gemm_ms)
-    mean_fix = statistics.mean(fix_ms)
+    mean_fix = statistics.mean(fix_ms) if fix_ms else None
     fused = chosen == MEC_PATH_FUSED
-    bytes_lower = (w["nI"] + w["nL"]) * elt                 # read I, write L (SURVEY 8(d))
+    bytes_lower = (w["nI"] + w["nL"]) * elt                 # read I, write L
     bytes_gemm = (w["nL"] + w["nK"] + w["nO"]) * elt        # L read once, K, write O
     if fused:  # (a6): no L; the GEMM reads I (windows) and K, writes O
         bytes_lower = (w["nK"] * 2) * elt                   # weight operand prep: read K, write Kt
@@ -412,32 +491,35 @@ def main():
     hbm = peaks["hbm_gbs"]
     tc = peaks["bf16_tflops"] if dtype_name == "bf16" else peaks["bf16_tflops"] / 2.0
     tc_src = "bf16 measured burst" if dtype_name == "bf16" else "tf32 = bf16 measured burst x 1/2 (nominal ratio)"
-    kernels = {
-        ("weight_prep" if fused else "mec_lower"): (mean_lower, "hbm", bytes_lower / (mean_lower * 1e-3) / 1e9,
-                                                    hbm, "GB/s", bytes_lower),
-    }
+    kernels = {("weight_prep" if fused else "mec_lower"): (mean_lower, "hbm", bytes_lower / (mean_lower * 1e-3) / 1e9,
+                                                          hbm, "GB/s", bytes_lower)}
     t_mem, t_tc = bytes_gemm / (hbm * 1e9), flops / (tc * 1e12)
     gname = "fused_window_gemm" if fused else "window_gemm"
     if t_mem >= t_tc:
         kernels[gname] = (mean_gemm, "hbm", bytes_gemm / (mean_gemm * 1e-3) / 1e9, hbm, "GB/s", bytes_gemm)
     else:
         kernels[gname] = (mean_gemm, "tensor", flops / (mean_gemm * 1e-3) / 1e12, tc, "TFLOP/s", flops)
-    if chosen == MEC_PATH_SOLUTION_A and fix == MEC_SOLA_FIX_LITERAL:
+    if literal:
         bfix = 4 * w["nO"] * elt
         kernels["sola_format_fix"] = (mean_fix, "hbm", bfix / (mean_fix * 1e-3) / 1e9, hbm, "GB/s", bfix)
     dom = max(kernels, key=lambda k: kernels[k][0])
     ms, bound, ach, peak, unit, alg = kernels[dom]
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            tj = json.load(f)
-        traffic = tj.get(cfg["name"], {}).get(dom)
+    ncu = load_ncu(cfg["name"])
+    nk = ncu.get(dom, {})
     roof = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-            "traffic": traffic, "kernel": dom, "kernel_ms": ms, "algorithmic_per_launch": alg,
+            "traffic": nk.get("dram_bytes"), "kernel": dom, "kernel_ms": ms, "algorithmic_per_launch": alg,
             "peak_source": peak_src if bound == "hbm" else f"{tc_src} ({peak_src})",
+            "traffic_source": nk.get("source"),
             "all_kernels": {k: {"ms": v[0], "bound": v[1], "achieved": v[2], "unit": v[4],
-                                "frac": v[2] / v[3]} for k, v in kernels.items()}}
+                                "frac": v[2] / v[3], "algorithmic_per_launch": v[5]} for k, v in kernels.items()}}
+    g_flops_rate = flops / (mean_gemm * 1e-3) / 1e12
+    tpu = {"gemm_tflops": g_flops_rate, "of_dense_peak": g_flops_rate / tc, "peak_tflops": tc,
+           "peak_source": f"{tc_src} ({peak_src})",
+           "ncu_sm__pipe_tensor_cycles_active_pct": ncu.get(gname, {}).get("tensor_pipe_pct"),
+           "ncu_source": ncu.get(gname, {}).get("source")}
+    if dtype_name == "tf32" and tf32_peak:
+        tpu["of_tf32_peak_measured_in_run"] = g_flops_rate / tf32_peak
+        tpu["tf32_peak_measured_in_run_tflops"] = tf32_peak
 
     # ---- north_star (3): the optional fused path measured against the two-kernel
     # path, same workload, same timing rules (reported alongside; `value` stays the
@@ -484,58 +566,101 @@ def main():
                           "achieved": flops / (f_gemm * 1e-3) / 1e12, "peak": tc}
             f_roof["frac"] = f_roof["achieved"] / f_roof["peak"]
             fused_alt = {"path": "fused_lowering_in_gemm",
-                         "value": w["flops"] * ws * K_steps / (f_tot * 1e-3) / 1e12, "unit": "TFLOP/s",
+                         "value": w_glob["flops"] * K_steps / (f_tot * 1e-3) / 1e12, "unit": "TFLOP/s",
                          "ms_per_step": f_tot / K_steps,
                          "stages_ms": {"weight_prep": f_prep, "fused_window_gemm": f_gemm},
                          "roofline": f_roof, "gpu_launches": mec.last_launch_count() * K_steps}
         except MecError as e:
             fused_alt = {"path": "fused_lowering_in_gemm", "unavailable": str(e)}
 
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = cpu_baseline(cfg, w, dtype_name, seed)
-        except Exception as e:  # noqa: BLE001
-            cpu = {"value": None, "error": str(e)}
-
     names = {MEC_PATH_SOLUTION_A: "solution_A_batch_folded", MEC_PATH_SOLUTION_B: "solution_B_per_image",
              MEC_PATH_FUSED: "fused_lowering_in_gemm"}
-    line = {
-        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": K_steps,
-        "warmup": args.warmup, "ms_per_step": tot_ms / K_steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": dtype_name,
+    stages = {"lower": mean_lower, "gemm": mean_gemm}
+    if literal:
+        stages["format_fix"] = mean_fix
+    res = {
+        "value": value, "ms_per_step": tot_ms / K_steps, "dtype": dtype_name,
         "data": f"synthetic (counter-based generator on device, seed {seed}, GRID values exact in {dtype_name})",
         "config": {
-            "workload": cfg["name"], "i_n_per_gpu": i_n, "global_batch": i_n * ws,
-            "I": [i_n, i_h, i_w, i_c], "K": [k_h, k_w, i_c, k_c], "stride": [s_h, s_w],
+            "workload": cfg["name"], "global_batch": rw["global_batch"], "i_n_per_gpu": i_n,
+            "first_image": rw["n0"], "I": [i_n, i_h, i_w, i_c], "K": [k_h, k_w, i_c, k_c], "stride": [s_h, s_w],
             "O": [i_n, w["o_h"], w["o_w"], k_c],
             "path": names.get(chosen, str(chosen)),
             "path_rule": f"Alg.2 l.8: Solution A iff o_w <= T={args.T} and #O <= #L" if path == MEC_PATH_AUTO
             else "forced",
             "north_star_letter": "B" if chosen == MEC_PATH_SOLUTION_A else "A",
             "sola_fix": args.sola_fix if chosen == MEC_PATH_SOLUTION_A else None,
-            "rows_per_tile": args.rows_per_tile or 1,
-            "l2": "flushed before every timed step: a 2x L2 write, then a 2x L2 read that writes its dirty lines back (outside the timed region)" if not args.no_flush else "warm (not flushed)",
-            "parallelism": f"dp{ws} (images sharded per GPU, K broadcast once by NCCL)",
+            "window_gemm_kernel": {1: "one_window_per_tile", 2: "h_sweep", 3: "wide_2sm"}.get(gemm_kernel,
+                                                                                              str(gemm_kernel)),
+            "l2": "flushed before every timed step: a 2x L2 write, then a 2x L2 read that writes its dirty "
+                  "lines back (outside the timed region)" if not args.no_flush else "warm (not flushed)",
+            "parallelism": f"dp{ws} ({args.scaling} scaling: images sharded per GPU, K broadcast once by NCCL)",
         },
         "lowered_bytes": {
             "mec_L": w["nL"] * elt, "im2col_L": w["nIm2col"] * elt,
             "im2col_over_mec": w["nIm2col"] / w["nL"], "workspace_allocated": ws_bytes,
             "pooled_call_device_mem_delta": pooled_delta,
         },
-        "stages_ms": {"lower": mean_lower, "gemm": mean_gemm, "format_fix": mean_fix},
+        "stages_ms": stages,
         "stages_timing": "per-kernel CUDA events in a separate run of K steps (kernels serialised); "
                          "value / ms_per_step time whole steps with no events inside them",
         "graph_ms_per_step": graph_ms,
         "roofline": roof,
-        "cpu_baseline": cpu,
+        "tensor_pipe_util": tpu,
         "e2e": e2e,
         "fused_path": fused_alt,
         "gpu_launches": launches_per_step * K_steps,
-        "gpu_launches_detail": {"per_step": launches_per_step, "l2_flush_kernels": 0 if args.no_flush else 2 * K_steps},
+        "gpu_launches_detail": {"per_step": launches_per_step,
+                                "l2_flush_kernels": 0 if args.no_flush else 2 * K_steps},
         "clocks": sampler.summary(),
         "k_broadcast_verified": k_bcast_ok,
     }
+    del I, K, O, workspace, flush
+    torch.cuda.empty_cache()
+    return res
+
+
+def main(argv=None):
+    args = parse(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    import synth
+    from paper_1706_06873_b200 import dist
+
+    rank, ws, dev = dist.init()
+    if dev.type != "cuda":
+        raise SystemExit("bench.py needs CUDA GPUs (no CPU fallback)")
+    cfg = synth.config(args.config, args.batch)
+    rw = rank_work(cfg["i_n"], rank, ws, args.scaling)
+    peaks, peak_src = load_peaks()
+    want_tf32 = cfg["dtype"] != "bf16" or (args.config in TF32_SIBLING and not args.no_tf32)
+    tf32_peak = measure_tf32_peak(dev) if (want_tf32 and not args.no_tf32_peak) else None
+
+    line = {"metric": METRIC, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None}
+    res = measure(args, cfg, rw, rank, ws, dev, peaks, peak_src, tf32_peak, primary=True)
+    line.update(res)
+    if args.config in TF32_SIBLING and not args.no_tf32:
+        cfg32 = synth.config(TF32_SIBLING[args.config], args.batch)
+        r32 = measure(args, cfg32, rank_work(cfg32["i_n"], rank, ws, args.scaling), rank, ws, dev, peaks,
+                      peak_src, tf32_peak, primary=False)
+        line["tf32"] = {k: r32[k] for k in ("value", "ms_per_step", "dtype", "config", "stages_ms", "roofline",
+                                             "tensor_pipe_util", "fused_path", "lowered_bytes", "clocks",
+                                             "gpu_launches")}
+        line["gpu_launches"] += r32["gpu_launches"]
+    if tf32_peak:
+        line["tf32_peak_measured_in_run"] = {"tflops": tf32_peak,
+                                             "how": "torch.matmul fp32, allow_tf32, 8192^3, best of 10"}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(cfg, workload(cfg), line["dtype"], synth.SEED_BASE + cfg["index"])
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "error": str(e)}
+    line["cpu_baseline"] = cpu
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.finalize()

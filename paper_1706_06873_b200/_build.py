@@ -63,16 +63,22 @@ def build(force: bool = False, verbose: bool = False, extra_flags=(), so_path: s
 
 def _build(verbose, extra_flags):
     os.makedirs(BUILD, exist_ok=True)
-    objs = []
-    log = []
-    for src in _sources():
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(src):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         cmd = [nvcc(), *NVCC_FLAGS, *extra_flags, "-I", os.path.join(ROOT, "include"), "-c", src,
                "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, r
+
+    with ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1))) as ex:
+        results = list(ex.map(one, _sources()))
+    objs, log = [], []
+    for src, obj, r in results:
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:
-            sys.stderr.write("\n".join(log))
+            sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
     tmp = SO + f".tmp{os.getpid()}"

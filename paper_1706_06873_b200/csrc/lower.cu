@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 
@@ -761,17 +762,18 @@ __global__ void __launch_bounds__(256) lower_direct_kernel(const T* __restrict__
 // CTAs; with the default L1-leaning carveout C1's bands took 2.25 waves).
 constexpr size_t kLowerMaxSmem = 200 * 1024;
 void set_lower_attributes() {
-  static bool done = false;
-  if (done) return;
-  HOST_CK(cudaFuncSetAttribute(lower_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(kLowerMaxSmem)));
-  HOST_CK(cudaFuncSetAttribute(lower_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(kLowerMaxSmem)));
-  HOST_CK(cudaFuncSetAttribute(lower_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared));
-  HOST_CK(cudaFuncSetAttribute(lower_kernel<uint32_t>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared));
-  done = true;
+  // function attributes are per device: once per device, thread-safe
+  static std::once_flag once[kMaxDevices];
+  std::call_once(once[current_device()], [] {
+    HOST_CK(cudaFuncSetAttribute(lower_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kLowerMaxSmem)));
+    HOST_CK(cudaFuncSetAttribute(lower_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kLowerMaxSmem)));
+    HOST_CK(cudaFuncSetAttribute(lower_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
+    HOST_CK(cudaFuncSetAttribute(lower_kernel<uint32_t>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared));
+  });
 }
 
 cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, const void* K,

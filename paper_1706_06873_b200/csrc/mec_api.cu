@@ -40,7 +40,6 @@ std::once_flag g_encode_once;
 
 // One library-owned stream-ordered memory pool per device, with an infinite
 // release threshold so repeated calls reuse the same L workspace.
-constexpr int kMaxDevices = 64;
 cudaMemPool_t g_pools[kMaxDevices] = {};
 std::mutex g_pool_mu;
 
@@ -353,6 +352,111 @@ mec_status_t mec_lower_pitched(const void* I, void* L, const mec_shape_t* s, int
   return MEC_OK;
 }
 
+}  // extern "C"
+
+namespace mec {
+
+// Everything one MEC call decides before touching device memory: the plan,
+// the path (Alg.2 l.8 or forced), the conv-path plan and the weight-operand
+// layout.  Every check that can refuse a call lives here, so callers that
+// enqueue several calls (mec_conv_forward_host) can run it up front.
+struct Resolved {
+  Plan p;          // the (virtually padded) problem
+  Plan pc;         // the conv path's plan (strip-padded L where used)
+  int path;        // MEC_PATH_SOLUTION_A / _B / _FUSED
+  bool gather_kt;  // the fused gather variant's weight-operand layout
+};
+
+mec_status_t resolve(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, const mec_options_t* opt,
+                     Resolved* r) {
+  mec_status_t st = make_plan(s, s_h, s_w, dt, &r->p, opt->pad_h, opt->pad_w);
+  if (st != MEC_OK) return st;
+  const Plan& p = r->p;
+  if (opt->path < MEC_PATH_AUTO || opt->path > MEC_PATH_FUSED) return MEC_ERR_INVALID_ARG;
+  if (opt->sola_fix < MEC_SOLA_FIX_EPILOGUE || opt->sola_fix > MEC_SOLA_FIX_NONE) return MEC_ERR_INVALID_ARG;
+  if (opt->rows_per_tile < 0) return MEC_ERR_INVALID_ARG;
+  const int T = opt->T > 0 ? opt->T : MEC_DEFAULT_T;
+  int path = opt->path;
+  if (path == MEC_PATH_AUTO) path = select_path_plan(p, T);
+  if (path == MEC_PATH_FUSED && !fused_eligible(p) && !gather_eligible(p)) return MEC_ERR_UNSUPPORTED;
+  // P:211: Solution A's literal format fix repurposes L as auxiliary space,
+  // which requires |L| >= |O|.
+  if (path == MEC_PATH_SOLUTION_A && opt->sola_fix == MEC_SOLA_FIX_LITERAL && p.n_O > p.n_L)
+    return MEC_ERR_UNSUPPORTED;
+  r->path = path;
+  // the conv path's L: the strip-padded layout (DESIGN.md 6.6) where the plan
+  // has one and multi-row tiles are not switched off; the fused path reads I
+  const bool spad = p.kwc_s > 0 && path != MEC_PATH_FUSED && opt->rows_per_tile != 1;
+  r->pc = spad ? strip_padded_plan(p) : p;
+  r->gather_kt = path == MEC_PATH_FUSED && !fused_eligible(p);
+  return MEC_OK;
+}
+
+// Prepare the weight operand (Alg.2 l.7: K as a (k_h k_w i_c) x k_c matrix,
+// K-major, zero padded, shifted copies) into Kt with a prep-only launch.
+cudaError_t prepare_weights(const Resolved& r, const void* K, void* Kt, cudaStream_t st, int* launches) {
+  return launch_lower(r.pc, nullptr, nullptr, r.pc.pitch, K, Kt, st, launches, r.gather_kt);
+}
+
+// The launch sequence of one call on a resolved problem: lowering (with the
+// weight prep unless kt_ready) -> window GEMMs -> [literal format fix].
+cudaError_t run_conv(const Resolved& r, const void* I, const void* K, void* O, void* L, void* Kt, bool kt_ready,
+                     cudaStream_t st, mec_options_t* opt, int* launches) {
+  const Plan& p = r.p;
+  const Plan& pc = r.pc;
+  const int path = r.path;
+  auto rec = [&](int i) {
+    if (opt->stage_events[i]) cudaEventRecord(static_cast<cudaEvent_t>(opt->stage_events[i]), st);
+  };
+  rec(0);
+  // Alg.2 l.2-7: lowering into the pitch-padded L, and K as a (k_h k_w i_c) x k_c matrix
+  // (the fused path skips L: only the weight operand is prepared)
+  cudaError_t e = launch_lower(pc, I, path == MEC_PATH_FUSED ? nullptr : L, pc.pitch, kt_ready ? nullptr : K,
+                               kt_ready ? nullptr : Kt, st, launches, r.gather_kt);
+  if (e != cudaSuccess) return e;
+  rec(1);
+  GemmArgs ga{};
+  ga.L = path == MEC_PATH_FUSED ? I : L;
+  ga.fused = path == MEC_PATH_FUSED;
+  ga.Kt = Kt;
+  ga.O = O;
+  ga.rows_per_tile = opt->rows_per_tile;
+  if (path == MEC_PATH_FUSED) {  // batch-folded tiles of windows of I
+    ga.batch_folded = true;
+    ga.out_hnwc = false;
+  } else if (path == MEC_PATH_SOLUTION_A) {  // l.9: L as (i_n o_w) x (i_h k_w i_c)
+    ga.batch_folded = true;
+    ga.out_hnwc = opt->sola_fix != MEC_SOLA_FIX_EPILOGUE;
+  } else {  // l.21: L as i_n matrices of o_w x (i_h k_w i_c)
+    ga.batch_folded = false;
+    ga.out_hnwc = false;
+  }
+  // rows_per_tile 0 (auto): the h-sweep where it applies; 1 or more: the
+  // one-window-per-tile kernel (R output rows per tile)
+  e = cudaErrorNotSupported;
+  opt->selected_gemm = 2;
+  if (opt->rows_per_tile == 0) e = launch_sweep_gemm(pc, ga, st, launches);
+  if (e == cudaErrorNotSupported) {
+    opt->selected_gemm = 1;
+    e = launch_window_gemm(pc, ga, st, launches);
+  }
+  if (e != cudaSuccess) return e;
+  rec(2);
+  if (path == MEC_PATH_SOLUTION_A && opt->sola_fix == MEC_SOLA_FIX_LITERAL) {
+    e = launch_sola_copy(p, O, L, st, launches);  // l.13 Copy L = O
+    if (e != cudaSuccess) return e;
+    e = launch_sola_transpose(p, L, O, st, launches);  // l.14-19
+    if (e != cudaSuccess) return e;
+  }
+  rec(3);
+  opt->selected_path = path;
+  return cudaSuccess;
+}
+
+}  // namespace mec
+
+extern "C" {
+
 mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const mec_shape_t* s,
                                  int s_h, int s_w, mec_dtype_t dt, void* stream,
                                  mec_options_t* opt) {
@@ -361,25 +465,12 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
     mec_options_init(&def);
     opt = &def;
   }
-  Plan p;
-  mec_status_t st = mec::make_plan(s, s_h, s_w, dt, &p, opt->pad_h, opt->pad_w);
+  mec::Resolved r;
+  mec_status_t st = mec::resolve(s, s_h, s_w, dt, opt, &r);
   if (st != MEC_OK) return st;
   if (!I || !K || !O) return MEC_ERR_INVALID_ARG;
   if (!mec::aligned16(I) || !mec::aligned16(K) || !mec::aligned16(O)) return MEC_ERR_MISALIGNED;
-  if (opt->path < MEC_PATH_AUTO || opt->path > MEC_PATH_FUSED) return MEC_ERR_INVALID_ARG;
-  if (opt->sola_fix < MEC_SOLA_FIX_EPILOGUE || opt->sola_fix > MEC_SOLA_FIX_NONE)
-    return MEC_ERR_INVALID_ARG;
-  if (opt->rows_per_tile < 0) return MEC_ERR_INVALID_ARG;
-  const int T = opt->T > 0 ? opt->T : MEC_DEFAULT_T;
-  int path = opt->path;
-  if (path == MEC_PATH_AUTO) path = mec::select_path_plan(p, T);
-  if (path == MEC_PATH_FUSED && !mec::fused_eligible(p) && !mec::gather_eligible(p))
-    return MEC_ERR_UNSUPPORTED;
-  // P:211: Solution A's literal format fix repurposes L as auxiliary space,
-  // which requires |L| >= |O|.
-  if (path == MEC_PATH_SOLUTION_A && opt->sola_fix == MEC_SOLA_FIX_LITERAL && p.n_O > p.n_L)
-    return MEC_ERR_UNSUPPORTED;
-
+  const Plan& p = r.p;
   cudaStream_t stream_ = static_cast<cudaStream_t>(stream);
   void* ws = opt->workspace;
   bool pooled = false;
@@ -401,71 +492,17 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
   }
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(ws) + 1023) & ~static_cast<uintptr_t>(1023));
-  // the conv path's L: the strip-padded layout (DESIGN.md 6.6) where the plan
-  // has one and multi-row tiles are not switched off; the fused path reads I
-  const bool spad = p.kwc_s > 0 && path != MEC_PATH_FUSED && opt->rows_per_tile != 1;
-  const Plan pc = spad ? mec::strip_padded_plan(p) : p;
-  void* L = base;
-  void* Kt = base + pc.off_kt;
-
-  auto rec = [&](int i) {
-    if (opt->stage_events[i]) cudaEventRecord(static_cast<cudaEvent_t>(opt->stage_events[i]), stream_);
-  };
   int launches = 0;
-  cudaError_t e = cudaSuccess;
-  rec(0);
-  // Alg.2 l.2-7: lowering into the pitch-padded L, and K as a (k_h k_w i_c) x k_c matrix
-  // (the fused path skips L: only the weight operand is prepared)
-  e = mec::launch_lower(pc, I, path == MEC_PATH_FUSED ? nullptr : L, pc.pitch, K, Kt, stream_, &launches,
-                        path == MEC_PATH_FUSED && !mec::fused_eligible(p));
-  if (e != cudaSuccess) goto fail;
-  rec(1);
-  {
-    mec::GemmArgs ga{};
-    ga.L = path == MEC_PATH_FUSED ? I : L;
-    ga.fused = path == MEC_PATH_FUSED;
-    ga.Kt = Kt;
-    ga.O = O;
-    ga.rows_per_tile = opt->rows_per_tile;
-    if (path == MEC_PATH_FUSED) {  // batch-folded tiles of windows of I
-      ga.batch_folded = true;
-      ga.out_hnwc = false;
-    } else if (path == MEC_PATH_SOLUTION_A) {  // l.9: L as (i_n o_w) x (i_h k_w i_c)
-      ga.batch_folded = true;
-      ga.out_hnwc = opt->sola_fix != MEC_SOLA_FIX_EPILOGUE;
-    } else {  // l.21: L as i_n matrices of o_w x (i_h k_w i_c)
-      ga.batch_folded = false;
-      ga.out_hnwc = false;
-    }
-    // rows_per_tile 0 (auto): the h-sweep where it applies; 1 or more: the
-    // one-window-per-tile kernel (R output rows per tile)
-    e = cudaErrorNotSupported;
-    opt->selected_gemm = 2;
-    if (opt->rows_per_tile == 0) e = mec::launch_sweep_gemm(pc, ga, stream_, &launches);
-    if (e == cudaErrorNotSupported) {
-      opt->selected_gemm = 1;
-      e = mec::launch_window_gemm(pc, ga, stream_, &launches);
-    }
-    if (e != cudaSuccess) goto fail;
-  }
-  rec(2);
-  if (path == MEC_PATH_SOLUTION_A && opt->sola_fix == MEC_SOLA_FIX_LITERAL) {
-    e = mec::launch_sola_copy(p, O, L, stream_, &launches);  // l.13 Copy L = O
-    if (e != cudaSuccess) goto fail;
-    e = mec::launch_sola_transpose(p, L, O, stream_, &launches);  // l.14-19
-    if (e != cudaSuccess) goto fail;
-  }
-  rec(3);
+  const cudaError_t e = mec::run_conv(r, I, K, O, base, base + r.pc.off_kt, false, stream_, opt, &launches);
   if (pooled) cudaFreeAsync(ws, stream_);
-  opt->selected_path = path;
+  if (e != cudaSuccess) {
+    if (getenv("MEC_DEBUG_ERRORS"))
+      fprintf(stderr, "mec_conv_forward: failed after %d launches (path %d): %s\n", launches, r.path,
+              cudaGetErrorString(e));
+    return mec::cuda_fail(e, "mec_conv_forward");
+  }
   mec::g_launches = launches;
   return MEC_OK;
-fail:
-  if (pooled) cudaFreeAsync(ws, stream_);
-  if (getenv("MEC_DEBUG_ERRORS"))
-    fprintf(stderr, "mec_conv_forward: failed after %d launches (path %d): %s\n", launches, path,
-            cudaGetErrorString(e));
-  return mec::cuda_fail(e, "mec_conv_forward");
 }
 
 mec_status_t mec_conv_forward(const void* I, const void* K, void* O, const mec_shape_t* s,
@@ -513,24 +550,42 @@ struct HostPipe {
 HostPipe g_pipes[kMaxDevices];
 std::mutex g_pipe_mu;  // held while a call enqueues (the events are shared)
 
+void destroy_pipe(HostPipe& P) {
+  for (cudaStream_t* x : {&P.h2d, &P.comp, &P.d2h})
+    if (*x) cudaStreamDestroy(*x);
+  for (cudaEvent_t* x : {&P.start, &P.k_in})
+    if (*x) cudaEventDestroy(*x);
+  for (int i = 0; i < kSlots; ++i)
+    for (cudaEvent_t* x : {&P.in[i], &P.done[i], &P.out[i]})
+      if (*x) cudaEventDestroy(*x);
+  P = HostPipe{};
+}
+
+// The device's pipeline (streams + events), created on first use.  It is
+// built in a local and published only once every handle exists, so a failed
+// creation never leaves a half-built pipeline behind (null streams would be
+// the legacy default stream).  Called with g_pipe_mu held.
 cudaError_t get_pipe(HostPipe** out) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  const int dev = current_device();
   HostPipe& P = g_pipes[dev];
   if (!P.h2d) {
+    HostPipe q;
     const unsigned ev = cudaEventDisableTiming;
-    if ((e = cudaStreamCreateWithFlags(&P.h2d, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaStreamCreateWithFlags(&P.comp, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaStreamCreateWithFlags(&P.d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&P.start, ev)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&P.k_in, ev)) != cudaSuccess) return e;
-    for (int i = 0; i < kSlots; ++i) {
-      if ((e = cudaEventCreateWithFlags(&P.in[i], ev)) != cudaSuccess) return e;
-      if ((e = cudaEventCreateWithFlags(&P.done[i], ev)) != cudaSuccess) return e;
-      if ((e = cudaEventCreateWithFlags(&P.out[i], ev)) != cudaSuccess) return e;
+    cudaError_t e = cudaStreamCreateWithFlags(&q.h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&q.comp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&q.d2h, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q.start, ev);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q.k_in, ev);
+    for (int i = 0; i < kSlots && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&q.in[i], ev);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q.done[i], ev);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q.out[i], ev);
     }
+    if (e != cudaSuccess) {
+      destroy_pipe(q);
+      return e;
+    }
+    P = q;
   }
   *out = &P;
   return cudaSuccess;
@@ -595,13 +650,23 @@ mec_status_t mec_conv_forward_host(const void* I_host, const void* K_host, void*
   mec_status_t st = mec::host_layout(s, s_h, s_w, dt, opt, n_chunks, &h);
   if (st != MEC_OK) return st;
   if (opt->sola_fix == MEC_SOLA_FIX_NONE) return MEC_ERR_UNSUPPORTED;
-  if (opt->path < MEC_PATH_AUTO || opt->path > MEC_PATH_FUSED) return MEC_ERR_INVALID_ARG;
-  // Alg.2 l.8 on the full shape, then forced for every chunk
-  Plan pf;
-  st = mec::make_plan(s, s_h, s_w, dt, &pf, opt->pad_h, opt->pad_w);
+  // Every check of the per-chunk calls runs here, before anything is enqueued:
+  // Alg.2 l.8 on the full shape (forced for every chunk), forced-path
+  // eligibility, the literal fix's #O <= #L, rows_per_tile.  (All of them are
+  // independent of i_n, so the chunks pass them too.)
+  mec::Resolved rf;
+  st = mec::resolve(s, s_h, s_w, dt, opt, &rf);
   if (st != MEC_OK) return st;
-  const int path = opt->path == MEC_PATH_AUTO ? mec::select_path_plan(pf, opt->T > 0 ? opt->T : MEC_DEFAULT_T)
-                                              : opt->path;
+  mec_options_t co = *opt;
+  co.path = rf.path;
+  for (auto& ev : co.stage_events) ev = nullptr;
+  mec::Resolved rc;  // the full-size chunk (the last one may be smaller)
+  {
+    mec_shape_t sc = *s;
+    sc.i_n = h.per_chunk;
+    st = mec::resolve(&sc, s_h, s_w, dt, &co, &rc);
+    if (st != MEC_OK) return st;
+  }
   cudaStream_t user = static_cast<cudaStream_t>(stream);
   if (dev_scratch) {
     if (!mec::aligned16(dev_scratch)) return MEC_ERR_MISALIGNED;
@@ -627,12 +692,11 @@ mec_status_t mec_conv_forward_host(const void* I_host, const void* K_host, void*
       (reinterpret_cast<uintptr_t>(scratch) + 1023) & ~static_cast<uintptr_t>(1023));
   const unsigned char* Ih = static_cast<const unsigned char*>(I_host);
   unsigned char* Oh = static_cast<unsigned char*>(O_host);
+  unsigned char* ws = base + h.off_ws;
+  // the weight operand is the same for every chunk: prepared once, after the
+  // largest chunk's L in the workspace (a smaller last chunk's L ends earlier)
+  void* Kt = ws + rc.pc.off_kt;
   int kernels = 0;
-  mec_options_t co = *opt;
-  co.path = path;
-  co.workspace = base + h.off_ws;
-  co.workspace_bytes = h.ws_bytes;
-  for (auto& ev : co.stage_events) ev = nullptr;
   // the caller's earlier work (and the pool allocation) precede every copy
   e = cudaEventRecord(P->start, user);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(P->h2d, P->start, 0);
@@ -641,6 +705,7 @@ mec_status_t mec_conv_forward_host(const void* I_host, const void* K_host, void*
   if (e == cudaSuccess) e = cudaMemcpyAsync(base, K_host, h.k_bytes, cudaMemcpyHostToDevice, P->h2d);
   if (e == cudaSuccess) e = cudaEventRecord(P->k_in, P->h2d);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(P->comp, P->k_in, 0);
+  if (e == cudaSuccess) e = mec::prepare_weights(rc, base, Kt, P->comp, &kernels);
   for (int64_t c = 0; c < h.n_chunks && e == cudaSuccess; ++c) {
     const int sl = static_cast<int>(c % h.slots);
     const int64_t n0 = c * h.per_chunk;
@@ -656,21 +721,40 @@ mec_status_t mec_conv_forward_host(const void* I_host, const void* K_host, void*
     if (e == cudaSuccess) e = cudaStreamWaitEvent(P->comp, P->in[sl], 0);
     if (e == cudaSuccess && c >= h.slots) e = cudaStreamWaitEvent(P->comp, P->out[sl], 0);
     if (e != cudaSuccess) break;
-    mec_shape_t sc = *s;
-    sc.i_n = nb;
-    st = mec_conv_forward_ex(Id, base, Od, &sc, s_h, s_w, dt, P->comp, &co);
-    if (st != MEC_OK) break;
-    kernels += mec::g_launches;
-    e = cudaEventRecord(P->done[sl], P->comp);
+    mec::Resolved rk = rc;
+    if (nb != h.per_chunk) {
+      mec_shape_t sc = *s;
+      sc.i_n = nb;
+      if ((st = mec::resolve(&sc, s_h, s_w, dt, &co, &rk)) != MEC_OK) break;
+    }
+    int launches = 0;
+    e = mec::run_conv(rk, Id, base, Od, ws, Kt, true, P->comp, &co, &launches);
+    kernels += launches;
+    if (e == cudaSuccess) e = cudaEventRecord(P->done[sl], P->comp);
     // copy out
     if (e == cudaSuccess) e = cudaStreamWaitEvent(P->d2h, P->done[sl], 0);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(Oh + n0 * h.o_img, Od, nb * h.o_img, cudaMemcpyDeviceToHost, P->d2h);
     if (e == cudaSuccess) e = cudaEventRecord(P->out[sl], P->d2h);
   }
-  // the caller's stream waits for the last copy out (the D2H stream is in order)
-  if (e == cudaSuccess) e = cudaEventRecord(P->start, P->d2h);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(user, P->start, 0);
+  if (e == cudaSuccess && st == MEC_OK) {
+    // the caller's stream waits for the last copy out (the D2H stream is in order)
+    e = cudaEventRecord(P->start, P->d2h);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(user, P->start, 0);
+  }
+  if (e != cudaSuccess || st != MEC_OK) {
+    // a failure after the first enqueue: the caller's stream joins all three
+    // pipeline streams, so the scratch is not released (nor the call returned
+    // to a caller who may free the host buffers) while copies or kernels that
+    // were already enqueued can still touch it
+    const cudaError_t first = e;
+    cudaGetLastError();
+    for (cudaStream_t x : {P->h2d, P->comp, P->d2h}) {
+      if (cudaEventRecord(P->start, x) == cudaSuccess) cudaStreamWaitEvent(user, P->start, 0);
+    }
+    cudaStreamSynchronize(user);
+    e = first;
+  }
   if (pooled) cudaFreeAsync(scratch, user);
   if (st != MEC_OK) return st;
   if (e != cudaSuccess) return mec::cuda_fail(e, "mec_conv_forward_host");

@@ -134,4 +134,13 @@ cudaError_t launch_sola_transpose(const Plan& p, const void* Laux, void* O, cuda
 
 int num_sms();
 
+// Per-device library state (pools, host pipelines, kernel attributes) is kept
+// in arrays of kMaxDevices; current_device() clamps the ordinal into them.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
+
 }  // namespace mec

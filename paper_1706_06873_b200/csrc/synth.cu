@@ -5,7 +5,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 
 #include "../../include/mec_synth.h"
 #include "mec_internal.h"
@@ -84,7 +86,7 @@ extern "C" mec_status_t mec_synth_fill(void* dst, int64_t count, uint64_t seed, 
 }
 
 extern "C" mec_status_t mec_l2_flush(void* scratch, size_t bytes, void* stream) {
-  static uint32_t salt = 1;
+  static std::atomic<uint32_t> salt{1};
   if (scratch == nullptr) return MEC_ERR_INVALID_ARG;
   const int64_t half16 = static_cast<int64_t>(bytes / 32);
   if (half16 == 0) return MEC_OK;
@@ -93,18 +95,17 @@ extern "C" mec_status_t mec_l2_flush(void* scratch, size_t bytes, void* stream) 
   uint4* base = static_cast<uint4*>(scratch);
   // the same all-shared carveout as the MEC kernels, so the timed step after a
   // flush does not include an SM shared-memory reconfiguration the flush caused
-  static bool carveout = false;
-  if (!carveout) {
+  static std::once_flag carveout[mec::kMaxDevices];  // function attributes are per device
+  std::call_once(carveout[mec::current_device()], [] {
     cudaFuncSetAttribute(mec::flush_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(mec::flush_read_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     cudaGetLastError();
-    carveout = true;
-  }
-  mec::flush_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(base, half16, salt);
+  });
+  const uint32_t sl = salt.fetch_add(1);
+  mec::flush_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(base, half16, sl);
   mec::flush_read_kernel<<<static_cast<unsigned>(grid), 256, 0, st>>>(
-      base + half16, half16, salt, reinterpret_cast<uint32_t*>(base));
-  ++salt;
+      base + half16, half16, sl, reinterpret_cast<uint32_t*>(base));
   return cudaGetLastError() == cudaSuccess ? MEC_OK : MEC_ERR_CUDA;
 }

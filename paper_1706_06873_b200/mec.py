@@ -213,7 +213,24 @@ def conv_forward_host(I_h: torch.Tensor, K_h: torch.Tensor, s_h: int, s_w: int, 
                                               s_h, s_w, dtype_code(I_h.dtype), stream, ctypes.byref(opt),
                                               int(n_chunks), sp, sb)
     _lib.check(st, "mec_conv_forward_host")
+    # The copies read I_h / K_h and write out asynchronously: keep the tensors
+    # (and the scratch) alive until the stream passes an event recorded after
+    # the call, so a temporary argument (x.pin_memory()) is not freed -- and
+    # its pinned block reused -- while a copy still reads it.
+    with torch.cuda.device(dev):
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(dev))
+    _keep_alive(ev, (I_h, K_h, out, scratch))
     return (out, opt.selected_path) if return_path else out
+
+
+_PENDING: list = []  # (event, tensors) of host-buffer calls still in flight
+
+
+def _keep_alive(ev, refs) -> None:
+    """Hold `refs` until `ev` has completed; completed entries are dropped here."""
+    _PENDING[:] = [(e, r) for e, r in _PENDING if not e.query()]
+    _PENDING.append((ev, refs))
 
 
 def maxpool(X: torch.Tensor, p_h: int, p_w: int, s_h: int, s_w: int, hnwc: bool = False,

@@ -79,4 +79,4 @@ def kernel_tensor(cfg: dict, kind: int, seed: int) -> np.ndarray:
     return tensor((cfg["k_h"], cfg["k_w"], cfg["i_c"], cfg["k_c"]), seed, TENSOR_K, kind)
 
 
-from .configs import CONFIGS, TABLE2, config  # noqa: E402,F401
+from .configs import CONFIGS, ONE_BY_ONE, TABLE2, config  # noqa: E402,F401

@@ -51,11 +51,15 @@ CONFIGS = {
     "C3": _mk("C3_resnet50_stage2_3x3", 256, TABLE2["cv9"], "bf16", index=3),
 }
 for _n, _t in list(TABLE2.items()) + list(ONE_BY_ONE.items()):
-    CONFIGS[f"C4_{_n}"] = _mk(f"C4_{_n}_b1024", 1024, _t, "bf16", index=4)
+    CONFIGS[f"C4_{_n}"] = _mk(f"C4_{_n}_b1024", 1024, _t, "bf16", index=4, layer=_n)
 
 
 def config(name: str, i_n: int | None = None) -> dict:
+    """A copy of CONFIGS[name]; i_n overrides the batch.  The C4 sweep's names
+    carry the batch actually used (C4_cv4_b128 when i_n = 128)."""
     c = dict(CONFIGS[name])
     if i_n is not None:
         c["i_n"] = i_n
+    if "layer" in c:
+        c["name"] = f"C4_{c['layer']}_b{c['i_n']}"
     return c

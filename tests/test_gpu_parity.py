@@ -346,8 +346,11 @@ def test_lowering_full_C1_batch_bit_exact(cuda_ok):
 
 # -------------------------------------------- BASELINE configs at full size
 
-def sampled_parity(cfg_name, dtype, images, path=0):
-    c = synth.config(cfg_name)
+def sampled_parity(cfg_name, dtype, images, path=0, batch=None):
+    """The whole batch at the bench's size (bench.py's launch configuration:
+    inputs generated on the device, one mec_conv_forward_ex call on the full
+    batch), then the sampled images recomputed by the oracle one by one."""
+    c = synth.config(cfg_name, batch)
     shape = (c["i_n"], c["i_h"], c["i_w"], c["i_c"], c["k_h"], c["k_w"], c["k_c"])
     seed = synth.SEED_BASE + c["index"]
     kind = synth.KIND_GRID8 if dtype == "bf16" else synth.KIND_GRID11
@@ -358,13 +361,44 @@ def sampled_parity(cfg_name, dtype, images, path=0):
     mec.synth_fill(Kd, seed, synth.TENSOR_K, kind)
     O = mec.conv_forward(Id, Kd, c["s_h"], c["s_w"], path=path)
     torch.cuda.synchronize()
+    del Id
     # ... and the sampled images regenerated on the host for the oracle
     K = synth.kernel_tensor(c, kind, seed)
     np.testing.assert_array_equal(Kd.float().cpu().numpy(), K)
     for n in images:
+        n = n % c["i_n"]
         I = synth.input_images(c, n, 1, kind, seed)
         ref = oracle.direct_conv(I, K, c["s_h"], c["s_w"], n_threads=8)
         check_O(O[n:n + 1], ref, dtype, c["k_h"] * c["k_w"] * c["i_c"])
+    del O
+    torch.cuda.empty_cache()
+
+
+C4_LAYERS = list(synth.TABLE2) + list(synth.ONE_BY_ONE)
+
+
+@pytest.mark.parametrize("layer", C4_LAYERS)
+def test_C4_sweep_b128_sampled(cuda_ok, layer):
+    """C4 at b128 (the per-GPU shard of b1024 at g = 8, the size bench.py times
+    for the sweep lines): the first, a middle and the last image."""
+    sampled_parity(f"C4_{layer}", "bf16", [0, 77, -1], batch=128)
+
+
+@pytest.mark.parametrize("layer", ["cv4", "cv5", "cv12"])
+def test_C4_sweep_b1024_sampled(cuda_ok, layer):
+    """C4 at its stated batch 1024 (cv4: a 22.4 GB L, index math past 2^32 bytes)."""
+    sampled_parity(f"C4_{layer}", "bf16", [0, 513, -1], batch=1024)
+
+
+@pytest.mark.parametrize("layer", ["cv4", "cv5"])
+def test_C4_tf32_b128_sampled(cuda_ok, layer):
+    """C4's tf32 rows (+tf32 on cv4, cv5)."""
+    c = synth.config(f"C4_{layer}", 128)
+    synth.CONFIGS[f"_tmp_{layer}_tf32"] = dict(c, dtype="tf32")
+    try:
+        sampled_parity(f"_tmp_{layer}_tf32", "tf32", [0, -1])
+    finally:
+        del synth.CONFIGS[f"_tmp_{layer}_tf32"]
 
 
 def test_C1_alexnet_conv1_full_batch_sampled(cuda_ok):
@@ -686,3 +720,55 @@ def test_conv_forward_host_padded_and_forced_paths(cuda_ok, path, dtype):
     torch.cuda.synchronize()
     assert ran == p
     check_O(O, ref, dtype, shape[3] * shape[4] * shape[5])
+
+
+# ------------------------------------------- the C ABI's named entry points
+
+def test_abi_named_calls_conv_forward_and_lower(cuda_ok):
+    """north_star's two named calls, mec_conv_forward and mec_lower, called by
+    name through ctypes (not the _ex / _padded variants the binding uses)."""
+    import ctypes
+
+    from paper_1706_06873_b200 import _lib
+
+    L_ = _lib.lib()
+    shape, s = (3, 19, 23, 16, 3, 3, 32), 2
+    I, K = make_inputs(shape, "bf16", seed=4242)
+    Id, Kd = to_dev(I, "bf16"), to_dev(K, "bf16")
+    ref = oracle.direct_conv(I, K, s, s)
+    O = torch.empty(ref.shape, dtype=torch.bfloat16, device="cuda")
+    sh = _lib.MecShape(*shape)
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert L_.mec_conv_forward(Id.data_ptr(), Kd.data_ptr(), O.data_ptr(), ctypes.byref(sh), s, s,
+                               _lib.MEC_DTYPE_BF16, stream) == 0
+    torch.cuda.synchronize()
+    check_O(O, ref, "bf16", 3 * 3 * 16)
+    o_w = (23 - 3) // s + 1
+    Ld = torch.empty((3, o_w, 19, 3, 16), dtype=torch.bfloat16, device="cuda")
+    assert L_.mec_lower(Id.data_ptr(), Ld.data_ptr(), ctypes.byref(sh), s, s, _lib.MEC_DTYPE_BF16, stream) == 0
+    torch.cuda.synchronize()
+    bits = Id.view(torch.int16).cpu().numpy()
+    np.testing.assert_array_equal(Ld.view(torch.int16).cpu().numpy(), oracle.lower(bits, 3, 3, s, s))
+
+
+@pytest.mark.parametrize("path", [MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B])
+def test_non_finite_input_documented_behaviour(cuda_ok, path):
+    """include/mec.h: inputs must be finite.  Pinned behaviour with one NaN
+    pixel in I: every output whose window holds it (the definition) is
+    NaN; the K-tail of a window box may also reach it from a neighbouring
+    window (zero weights times NaN), so further outputs MAY be NaN; every
+    output that is finite equals the oracle within the tolerance."""
+    shape, s = (2, 12, 13, 8, 3, 3, 16), 1
+    I, K = make_inputs(shape, "tf32", seed=99)
+    I[1, 5, 6, 3] = np.nan
+    ref = oracle.direct_conv(I, K, s, s)
+    O = mec.conv_forward(to_dev(I, "tf32"), to_dev(K, "tf32"), s, s, path=path)
+    torch.cuda.synchronize()
+    got = O.cpu().numpy().astype(np.float64)
+    nan_ref, nan_got = np.isnan(ref), np.isnan(got)
+    assert nan_ref.sum() == 3 * 3 * 16  # the 3x3 outputs (x 16 channels) whose windows hold the pixel
+    assert np.all(nan_got[nan_ref])
+    fin = ~nan_got
+    bar = tol("tf32", 72, np.where(nan_ref, 0.0, ref))
+    assert np.abs(got[fin] - ref[fin]).max() <= bar
+    assert not np.any(nan_got[0])  # the other image is untouched
