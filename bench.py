@@ -61,6 +61,9 @@ def parse(argv=None):
     ap.add_argument("--T", type=int, default=100)
     ap.add_argument("--rows-per-tile", type=int, default=0,
                     help="window GEMM output rows per tile (multi-row schedule; 0 = library default)")
+    ap.add_argument("--gemm-kernel", type=int, default=0,
+                    help="window-GEMM kernel: 0 auto, 1 one window per tile, 2 h-sweep, 3 CTA pair")
+    ap.add_argument("--split-k", type=int, default=0, help="CTA-pair kernel K ranges (0 = automatic)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tf32", action="store_true", help="skip the tf32 variant of the config")
@@ -346,7 +349,9 @@ def measure(args, cfg, rw, rank, ws, dev, peaks, peak_src, tf32_peak, primary=Tr
     k_bcast_ok = bool(torch.equal(K, K_local))
     del K_local
     O = torch.empty((i_n, w["o_h"], w["o_w"], k_c), dtype=tdt, device=dev)
-    ws_bytes = mec.workspace_bytes(w["shape"], s_h, s_w, tdt)
+    ws_bytes = mec.workspace_bytes(w["shape"], s_h, s_w, tdt, path=path, T=args.T, sola_fix=fix,
+                                   rows_per_tile=args.rows_per_tile, gemm_kernel=args.gemm_kernel,
+                                   split_k=args.split_k)
     workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(4 * l2, 128 << 20), dtype=torch.uint8, device=dev)
@@ -355,13 +360,15 @@ def measure(args, cfg, rw, rank, ws, dev, peaks, peak_src, tf32_peak, primary=Tr
     def step(evs=None):
         return mec.conv_forward(I, K, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix,
                                 rows_per_tile=args.rows_per_tile, workspace=workspace, stage_events=evs,
-                                return_path=True, return_gemm=True)
+                                return_path=True, return_gemm=True, gemm_kernel=args.gemm_kernel,
+                                split_k=args.split_k)
 
     # ---- memory: device-memory delta of one pooled call (the library allocates L itself)
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats(dev)
     free0 = torch.cuda.mem_get_info(dev)[0]
-    mec.conv_forward(I, K, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, rows_per_tile=args.rows_per_tile)
+    mec.conv_forward(I, K, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix, rows_per_tile=args.rows_per_tile,
+                     gemm_kernel=args.gemm_kernel, split_k=args.split_k)
     torch.cuda.synchronize()
     free1 = torch.cuda.mem_get_info(dev)[0]
     pooled_delta = max(0, free0 - free1)
@@ -371,6 +378,9 @@ def measure(args, cfg, rw, rank, ws, dev, peaks, peak_src, tf32_peak, primary=Tr
         if not args.no_flush:
             mec.l2_flush(flush)
         _, chosen, gemm_kernel = step()
+    split_used = mec.conv_forward(I, K, s_h, s_w, out=O, path=path, T=args.T, sola_fix=fix,
+                                  rows_per_tile=args.rows_per_tile, workspace=workspace, gemm_kernel=args.gemm_kernel,
+                                  split_k=args.split_k, return_split=True)[1]
     torch.cuda.synchronize()
     launches_per_step = mec.last_launch_count()
 
@@ -590,8 +600,9 @@ def measure(args, cfg, rw, rank, ws, dev, peaks, peak_src, tf32_peak, primary=Tr
             else "forced",
             "north_star_letter": "B" if chosen == MEC_PATH_SOLUTION_A else "A",
             "sola_fix": args.sola_fix if chosen == MEC_PATH_SOLUTION_A else None,
-            "window_gemm_kernel": {1: "one_window_per_tile", 2: "h_sweep", 3: "wide_2sm"}.get(gemm_kernel,
-                                                                                              str(gemm_kernel)),
+            "window_gemm_kernel": {1: "one_window_per_tile", 2: "h_sweep", 3: "cta_pair_split_k"}.get(
+                gemm_kernel, str(gemm_kernel)),
+            "split_k": split_used if gemm_kernel == 3 else None,
             "l2": "flushed before every timed step: a 2x L2 write, then a 2x L2 read that writes its dirty "
                   "lines back (outside the timed region)" if not args.no_flush else "warm (not flushed)",
             "parallelism": f"dp{ws} ({args.scaling} scaling: images sharded per GPU, K broadcast once by NCCL)",

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define MEC_ABI_VERSION 4
+#define MEC_ABI_VERSION 5
 
 typedef enum {
   MEC_OK = 0,
@@ -111,7 +111,19 @@ typedef struct {
    * Not supported by the fused gather variant (MEC_ERR_UNSUPPORTED). */
   int pad_h, pad_w;
   int selected_gemm; /* OUT: the window-GEMM kernel that ran: 1 = one window per tile
-                        (DESIGN.md 6.2), 2 = h-sweep with A in TMEM (6.2b), 0 = none */
+                        (DESIGN.md 6.2), 2 = h-sweep with A in TMEM (6.2b), 3 = CTA-pair
+                        (cta_group::2) kernel with split-K (6.7), 0 = none */
+  /* ABI version 5.  gemm_kernel (IN) forces the window-GEMM kernel: 0 = automatic
+   * (the CTA-pair kernel for tensor-bound Solution A layers with o_w < 32, else
+   * the h-sweep where it applies, else one window per tile), 1 = one window per
+   * tile, 2 = h-sweep, 3 = CTA pair.  A forced kernel that cannot run the
+   * problem returns MEC_ERR_UNSUPPORTED.  split_k (IN): K ranges of the CTA-pair
+   * kernel, 0 = automatic (1..8 by a wave model); the ranges' fp32 partials are
+   * summed in range order, so the result depends on split_k but not on timing.
+   * selected_split (OUT): the split the CTA-pair kernel used (0 otherwise). */
+  int gemm_kernel;
+  int split_k;
+  int selected_split;
 } mec_options_t;
 
 /* Fills *opt with defaults (AUTO path, T = 100, epilogue fix, pool workspace). */

@@ -67,6 +67,9 @@ class MecOptions(ctypes.Structure):
         ("pad_h", ctypes.c_int),
         ("pad_w", ctypes.c_int),
         ("selected_gemm", ctypes.c_int),
+        ("gemm_kernel", ctypes.c_int),
+        ("split_k", ctypes.c_int),
+        ("selected_split", ctypes.c_int),
     ]
 
 

@@ -128,6 +128,10 @@ struct LowerParams {
   bool prep64;          // weight prep in 64 x 64 tiles with 16-byte vectors (bf16, k_c % 8 == 0)
   bool direct;          // aligned-copies path without the copies: every output granule is
                         // extracted from the raw band (two aligned LDS.128 per part)
+  // words the next kernel needs zeroed (the wide window GEMM's split-K
+  // counters), cleared by the last CTA of this launch
+  uint32_t* zero_words;
+  uint32_t n_zero;
 };
 
 template <typename T>
@@ -489,6 +493,8 @@ __global__ void __launch_bounds__(512) lower_kernel(const LowerParams p) {
   // the window GEMM that follows is launched as a programmatic dependent: let
   // its prologue start now (its loads of L / Kt wait for this grid to finish)
   ptx::griddep_launch_dependents();
+  if (p.zero_words != nullptr && blockIdx.x == gridDim.x - 1)
+    for (uint32_t i = threadIdx.x; i < p.n_zero; i += blockDim.x) p.zero_words[i] = 0u;
 
   if (p.ncls > 0) {
     // persistent lowering CTAs after the weight-prep CTAs, which are thus
@@ -777,9 +783,12 @@ void set_lower_attributes() {
 }
 
 cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, const void* K,
-                         void* Kt, cudaStream_t st, int* launches, bool gather_kt) {
+                         void* Kt, cudaStream_t st, int* launches, bool gather_kt, uint32_t* zero_words,
+                         uint32_t n_zero) {
   const mec_shape_t& s = pl.s;
   LowerParams p{};
+  p.zero_words = n_zero > 0 ? zero_words : nullptr;
+  p.n_zero = n_zero;
   p.I = static_cast<const unsigned char*>(I);
   p.I_end = p.I + static_cast<size_t>(s.i_n * pl.src_h * pl.src_w * s.i_c) * pl.elt;
   p.padded = pl.pad_h > 0 || pl.pad_w > 0;
@@ -840,7 +849,10 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   }
   const size_t prep_smem = p.prep64 ? kPrep64Smem : 64;
   if (L == nullptr) {  // weight operand only (fused path)
-    if (prep_blocks == 0) return cudaSuccess;
+    if (prep_blocks == 0) {
+      if (p.zero_words != nullptr) return cudaMemsetAsync(p.zero_words, 0, p.n_zero * sizeof(uint32_t), st);
+      return cudaSuccess;
+    }
     LowerParams q = p;
     q.n_lower_blocks = 0;
     if (pl.elt == 2)
@@ -858,6 +870,10 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
   // by the direct kernel: see below, after the band height is known)
   auto launch_direct = [&]() -> cudaError_t {
     // weight prep still needs the main kernel's prep blocks: run them with a 1-band grid
+    if (Kt == nullptr && p.zero_words != nullptr) {
+      const cudaError_t ez = cudaMemsetAsync(p.zero_words, 0, p.n_zero * sizeof(uint32_t), st);
+      if (ez != cudaSuccess) return ez;
+    }
     if (Kt != nullptr) {
       LowerParams q = p;
       q.n_lower_blocks = 0;

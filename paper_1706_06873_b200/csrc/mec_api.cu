@@ -16,6 +16,7 @@
 #include "tma_host.h"
 
 namespace mec {
+size_t workspace_need(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, const mec_options_t* opt);
 namespace {
 
 thread_local char g_err[512] = "";
@@ -166,6 +167,7 @@ void set_window_geometry(Plan* p, int64_t kw_s) {
   p->bytes_L_pitched = static_cast<size_t>(s->i_n * p->o_w * p->pitch) * p->elt;
   p->off_kt = static_cast<size_t>(round_up(static_cast<int64_t>(p->bytes_L_pitched), 1024));
   p->bytes_kt = static_cast<size_t>(std::max(p->n_var * p->kdim_pad, p->kdim_g) * p->kc_pad) * p->elt;
+  p->off_wide = static_cast<size_t>(round_up(static_cast<int64_t>(p->off_kt + p->bytes_kt), 1024));
   p->ws_bytes = p->off_kt + p->bytes_kt + 1024;
 }
 
@@ -230,6 +232,11 @@ mec_status_t make_plan(const mec_shape_t* s_in, int s_h, int s_w, mec_dtype_t dt
       p->ws_bytes = std::max(p->ws_bytes, q.ws_bytes);
     }
   }
+  // the CTA-pair kernel's scratch (split-K counters and partials) where Alg.2
+  // l.8's Solution A would run it automatically (mec_workspace_bytes has no
+  // options; resolve() sizes forced cases)
+  if (p->kwc_s == 0 && wide_eligible(*p, true, false) && wide_preferred(*p))
+    p->ws_bytes = std::max(p->ws_bytes, p->off_wide + wide_scratch_bytes(*p, 0) + 1024);
   // TMA coordinate / extent limits (int32 coordinates, dims <= 2^32)
   if (p->l_cols + p->kdim_pad >= (1LL << 31) || s->i_n * p->o_w >= (1LL << 31) ||
       p->kdim_pad >= (1LL << 31))
@@ -311,10 +318,8 @@ size_t mec_workspace_bytes(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t d
 
 size_t mec_workspace_bytes_ex(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt,
                               const mec_options_t* opt) {
-  Plan p;
-  if (mec::make_plan(s, s_h, s_w, dt, &p, opt ? opt->pad_h : 0, opt ? opt->pad_w : 0) != MEC_OK)
-    return 0;
-  return p.ws_bytes;
+  if (!opt) return mec_workspace_bytes(s, s_h, s_w, dt);
+  return mec::workspace_need(s, s_h, s_w, dt, opt);
 }
 
 mec_status_t mec_lower(const void* I, void* L, const mec_shape_t* s, int s_h, int s_w,
@@ -365,6 +370,9 @@ struct Resolved {
   Plan pc;         // the conv path's plan (strip-padded L where used)
   int path;        // MEC_PATH_SOLUTION_A / _B / _FUSED
   bool gather_kt;  // the fused gather variant's weight-operand layout
+  int gemm;        // window-GEMM kernel: 0 = h-sweep if it applies else one window, 1 = one window,
+                   // 2 = h-sweep (forced), 3 = CTA pair
+  size_t ws_need;  // workspace bytes this call needs
 };
 
 mec_status_t resolve(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, const mec_options_t* opt,
@@ -389,7 +397,30 @@ mec_status_t resolve(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, con
   const bool spad = p.kwc_s > 0 && path != MEC_PATH_FUSED && opt->rows_per_tile != 1;
   r->pc = spad ? strip_padded_plan(p) : p;
   r->gather_kt = path == MEC_PATH_FUSED && !fused_eligible(p);
+  if (opt->gemm_kernel < 0 || opt->gemm_kernel > 3 || opt->split_k < 0 || opt->split_k > 64)
+    return MEC_ERR_INVALID_ARG;
+  const bool batch_folded = path != MEC_PATH_SOLUTION_B;
+  const bool wide_ok = !spad && wide_eligible(r->pc, batch_folded, path == MEC_PATH_FUSED) &&
+                       opt->sola_fix == MEC_SOLA_FIX_EPILOGUE;
+  if (opt->gemm_kernel == 3) {
+    if (!wide_ok) return MEC_ERR_UNSUPPORTED;
+    r->gemm = 3;
+  } else if (opt->gemm_kernel == 0 && opt->rows_per_tile == 0 && wide_ok && wide_preferred(r->pc)) {
+    r->gemm = 3;
+  } else {
+    r->gemm = opt->gemm_kernel == 0 ? (opt->rows_per_tile == 0 ? 0 : 1) : opt->gemm_kernel;
+  }
+  if (r->gemm == 2 && opt->rows_per_tile != 0) return MEC_ERR_INVALID_ARG;
+  r->ws_need = p.ws_bytes;
+  if (r->gemm == 3)
+    r->ws_need = std::max(r->ws_need, r->pc.off_wide + wide_scratch_bytes(r->pc, opt->split_k) + 1024);
   return MEC_OK;
+}
+
+size_t workspace_need(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, const mec_options_t* opt) {
+  Resolved r;
+  if (resolve(s, s_h, s_w, dt, opt, &r) != MEC_OK) return 0;
+  return r.ws_need;
 }
 
 // Prepare the weight operand (Alg.2 l.7: K as a (k_h k_w i_c) x k_c matrix,
@@ -411,8 +442,12 @@ cudaError_t run_conv(const Resolved& r, const void* I, const void* K, void* O, v
   rec(0);
   // Alg.2 l.2-7: lowering into the pitch-padded L, and K as a (k_h k_w i_c) x k_c matrix
   // (the fused path skips L: only the weight operand is prepared)
+  unsigned char* wide_scratch = static_cast<unsigned char*>(L) + pc.off_wide;
+  const size_t wide_bytes = r.ws_need - pc.off_wide - 1024;
   cudaError_t e = launch_lower(pc, I, path == MEC_PATH_FUSED ? nullptr : L, pc.pitch, kt_ready ? nullptr : K,
-                               kt_ready ? nullptr : Kt, st, launches, r.gather_kt);
+                               kt_ready ? nullptr : Kt, st, launches, r.gather_kt,
+                               r.gemm == 3 ? reinterpret_cast<uint32_t*>(wide_scratch) : nullptr,
+                               r.gemm == 3 ? wide_zero_words(pc) : 0u);
   if (e != cudaSuccess) return e;
   rec(1);
   GemmArgs ga{};
@@ -431,14 +466,21 @@ cudaError_t run_conv(const Resolved& r, const void* I, const void* K, void* O, v
     ga.batch_folded = false;
     ga.out_hnwc = false;
   }
-  // rows_per_tile 0 (auto): the h-sweep where it applies; 1 or more: the
-  // one-window-per-tile kernel (R output rows per tile)
-  e = cudaErrorNotSupported;
-  opt->selected_gemm = 2;
-  if (opt->rows_per_tile == 0) e = launch_sweep_gemm(pc, ga, st, launches);
-  if (e == cudaErrorNotSupported) {
-    opt->selected_gemm = 1;
-    e = launch_window_gemm(pc, ga, st, launches);
+  // r.gemm (resolve): 3 = the CTA-pair kernel; 0 = the h-sweep where it
+  // applies, else one window per tile; 1 = one window per tile (R output rows
+  // per tile, rows_per_tile); 2 = the h-sweep, forced
+  opt->selected_split = 0;
+  if (r.gemm == 3) {
+    opt->selected_gemm = 3;
+    e = launch_wide_gemm(pc, ga, wide_scratch, wide_bytes, opt->split_k, st, launches, &opt->selected_split);
+  } else {
+    e = cudaErrorNotSupported;
+    opt->selected_gemm = 2;
+    if (r.gemm == 0 || r.gemm == 2) e = launch_sweep_gemm(pc, ga, st, launches);
+    if (e == cudaErrorNotSupported && r.gemm != 2) {
+      opt->selected_gemm = 1;
+      e = launch_window_gemm(pc, ga, st, launches);
+    }
   }
   if (e != cudaSuccess) return e;
   rec(2);
@@ -476,16 +518,16 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
   bool pooled = false;
   if (ws) {
     if (!mec::aligned16(ws)) return MEC_ERR_MISALIGNED;
-    if (opt->workspace_bytes < p.ws_bytes) return MEC_ERR_NO_MEMORY;
+    if (opt->workspace_bytes < r.ws_need) return MEC_ERR_NO_MEMORY;
   } else {
     cudaMemPool_t pool;
     cudaError_t e = mec::get_pool(&pool);
     if (e != cudaSuccess) return mec::cuda_fail(e, "mec pool");
-    e = cudaMallocFromPoolAsync(&ws, p.ws_bytes, pool, stream_);
+    e = cudaMallocFromPoolAsync(&ws, r.ws_need, pool, stream_);
     if (e != cudaSuccess) {
       cudaGetLastError();
       snprintf(mec::g_err, sizeof(mec::g_err), "workspace allocation of %zu bytes failed",
-               p.ws_bytes);
+               r.ws_need);
       return MEC_ERR_NO_MEMORY;
     }
     pooled = true;
@@ -495,6 +537,10 @@ mec_status_t mec_conv_forward_ex(const void* I, const void* K, void* O, const me
   int launches = 0;
   const cudaError_t e = mec::run_conv(r, I, K, O, base, base + r.pc.off_kt, false, stream_, opt, &launches);
   if (pooled) cudaFreeAsync(ws, stream_);
+  if (e == cudaErrorNotSupported) {  // a forced window-GEMM kernel that cannot run this problem
+    snprintf(mec::g_err, sizeof(mec::g_err), "the forced window-GEMM kernel %d does not apply", r.gemm);
+    return MEC_ERR_UNSUPPORTED;
+  }
   if (e != cudaSuccess) {
     if (getenv("MEC_DEBUG_ERRORS"))
       fprintf(stderr, "mec_conv_forward: failed after %d launches (path %d): %s\n", launches, r.path,
@@ -619,7 +665,12 @@ mec_status_t host_layout(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt,
   h->off_o = round_up(h->i_img * h->per_chunk, 1024);
   h->slot_bytes = h->off_o + round_up(h->o_img * h->per_chunk, 1024);
   h->off_ws = h->off_slot0 + h->slots * h->slot_bytes;
-  h->ws_bytes = pc.ws_bytes;
+  {
+    mec_options_t d;
+    mec_options_init(&d);
+    h->ws_bytes = workspace_need(&sc, s_h, s_w, dt, opt ? opt : &d);
+    if (h->ws_bytes == 0) return MEC_ERR_INVALID_ARG;
+  }
   h->total = h->off_ws + h->ws_bytes + 1024;  // + alignment slack of the base
   return MEC_OK;
 }

@@ -62,6 +62,7 @@ struct Plan {
   size_t bytes_L_pitched;  // i_n o_w pitch elt
   size_t off_kt;           // workspace offset of the prepared weight operand
   size_t bytes_kt;         // max(n_var kc_pad kdim_pad, kc_pad kdim_g) elt
+  size_t off_wide;         // workspace offset of the CTA-pair kernel's scratch (after Kt)
   size_t ws_bytes;         // total workspace (incl. alignment slack)
 };
 
@@ -86,8 +87,11 @@ int select_path_plan(const Plan& p, int T);
 // Kt may be null (mec_lower); L may be null (weight prep only, fused path).
 // gather_kt: build the gather path's operand instead (one copy, n_var = 1):
 //   Kt[c][a kwc_p + j] = K_mat[a k_w i_c + j][c] for j < k_w i_c, 0 otherwise.
+// zero_words / n_zero: words the following GEMM needs zeroed (split-K
+// counters of the wide kernel), cleared inside the same launch.
 cudaError_t launch_lower(const Plan& p, const void* I, void* L, int64_t pitch, const void* K,
-                         void* Kt, cudaStream_t st, int* launches, bool gather_kt = false);
+                         void* Kt, cudaStream_t st, int* launches, bool gather_kt = false,
+                         uint32_t* zero_words = nullptr, uint32_t n_zero = 0);
 
 // Window GEMMs (Alg.2 l.10-12 or l.23-25) on tcgen05.  batch_folded:
 // Solution A (rows of several images share one 128-row tile); otherwise
@@ -124,6 +128,18 @@ cudaError_t launch_window_gemm(const Plan& p, const GemmArgs& a, cudaStream_t st
 // launch_window_gemm.
 bool sweep_config(const Plan& p, bool batch_folded, int* n_vres, int* n_acc, int* ns, int* stages);
 cudaError_t launch_sweep_gemm(const Plan& p, const GemmArgs& a, cudaStream_t st, int* launches);
+
+// Window GEMMs of the tensor-bound layers on CTA pairs (wide_gemm.cu):
+// tcgen05 cta_group::2 (M = 256), split-K across pairs with an in-order
+// reduction.  Solution A with flat rows (o_w < 32) only.
+bool wide_eligible(const Plan& p, bool batch_folded, bool fused);
+bool wide_preferred(const Plan& p);  // tensor-bound (AI >= 0.8 ridge) or MEC_WIDE
+// scratch (counters + fp32 partials) for split `split` (0 = automatic)
+size_t wide_scratch_bytes(const Plan& p, int split);
+// words of the scratch that must be zero when the kernel starts
+uint32_t wide_zero_words(const Plan& p);
+cudaError_t launch_wide_gemm(const Plan& p, const GemmArgs& a, void* scratch, size_t scratch_bytes, int split,
+                             cudaStream_t st, int* launches, int* split_used);
 
 // Solution A format fix, paper-literal (Alg.2 l.13-19): "Copy L = O" and the
 // block transpose O[n,h,:] = L[h,n,:].

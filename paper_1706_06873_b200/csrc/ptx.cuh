@@ -686,6 +686,112 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+
+// ------------------------------------------------ CTA pairs (cta_group::2)
+// A cluster of 2 CTAs on the two SMs of a TPC issues tcgen05 work as one
+// "CTA pair": the leader (rank 0) issues the MMAs, whose M =
+// 256 rows come 128 from each CTA's shared memory (A) and whose N columns of B
+// are split N/2 per CTA; each CTA's TMEM receives its 128 rows of D.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on an mbarrier given by its shared::cluster address (possibly the peer CTA's)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA load into this CTA's shared memory whose completion (complete_tx) is
+// signalled on the mbarrier at shared::cluster address `bar_cluster` -- the
+// pair leader's barrier, so one expect_tx there covers both CTAs' loads.
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* desc, uint32_t bar_cluster, int32_t x,
+                                                 int32_t y, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar_cluster), "r"(x), "r"(y), "l"(cache_hint)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const void* desc, uint32_t bar_cluster, int32_t x,
+                                                 int32_t y, int32_t z, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar_cluster), "r"(x), "r"(y), "r"(z), "l"(cache_hint)
+      : "memory");
+}
+// TMEM allocation for a CTA pair: executed by the same warp in both CTAs.
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_result, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_result)),
+               "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols) : "memory");
+}
+// Whole-warp call (pair leader): one elected lane issues the 4 SS MMAs of a
+// 128-byte K atom with cta_group::2 (M = 256 across the pair).
+template <bool kTF32>
+__device__ __forceinline__ void mma_ss_atom_pair_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                       uint32_t idesc, uint32_t accumulate) {
+#define MEC_PAIR_ATOM(KIND)                                                                             \
+  asm volatile(                                                                                         \
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"                                    \
+      "setp.ne.b32 p, %4, 0;\n\t"                                                                       \
+      "add.u64 a1, %1, 2;\n\tadd.u64 a2, %1, 4;\n\tadd.u64 a3, %1, 6;\n\t"                                 \
+      "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t"                                 \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                                 \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], %1, %2, %3, p;\n\t"                              \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], a1, b1, %3, 1;\n\t"                              \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], a2, b2, %3, 1;\n\t"                              \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], a3, b3, %3, 1;\n\t}" ::"r"(tmem_d),              \
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)                                               \
+      : "memory")
+  if constexpr (kTF32) {
+    MEC_PAIR_ATOM("tf32");
+  } else {
+    MEC_PAIR_ATOM("f16");
+  }
+#undef MEC_PAIR_ATOM
+}
+// Whole-warp call (pair leader): commit the pair's prior MMAs to the mbarrier
+// at the same shared offset in every CTA of `cta_mask` (multicast arrive).
+__device__ __forceinline__ void mma_commit_pair_elect(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
+// 16-byte global load that bypasses L1 (data written by other SMs in this launch)
+__device__ __forceinline__ uint4 ld_global_cg_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
 // ----------------------------------------------------------- descriptors
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"), K-major
 // operand stored in the canonical 128-byte-swizzle layout that a TMA load with

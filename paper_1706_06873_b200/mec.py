@@ -71,12 +71,15 @@ def im2col_elems(shape, s_h, s_w) -> int:
     return _lib.lib().mec_im2col_elems(ctypes.byref(_shape(*shape)), s_h, s_w)
 
 
-def workspace_bytes(shape, s_h, s_w, dtype: torch.dtype, pad_h: int = 0, pad_w: int = 0) -> int:
-    if pad_h == 0 and pad_w == 0:
+def workspace_bytes(shape, s_h, s_w, dtype: torch.dtype, pad_h: int = 0, pad_w: int = 0, **opts) -> int:
+    """mec_workspace_bytes (or _ex with pads / options such as path, gemm_kernel, split_k)."""
+    if pad_h == 0 and pad_w == 0 and not opts:
         return _lib.lib().mec_workspace_bytes(ctypes.byref(_shape(*shape)), s_h, s_w, dtype_code(dtype))
     opt = _lib.MecOptions()
     _lib.lib().mec_options_init(ctypes.byref(opt))
     opt.pad_h, opt.pad_w = int(pad_h), int(pad_w)
+    for k, v in opts.items():
+        setattr(opt, k, int(v))
     return _lib.lib().mec_workspace_bytes_ex(ctypes.byref(_shape(*shape)), s_h, s_w, dtype_code(dtype),
                                              ctypes.byref(opt))
 
@@ -123,12 +126,15 @@ def lower_pitched(I: torch.Tensor, k_h: int, k_w: int, s_h: int, s_w: int, pitch
 def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torch.Tensor | None = None,
                  path: int = MEC_PATH_AUTO, T: int = MEC_DEFAULT_T, sola_fix: int = MEC_SOLA_FIX_EPILOGUE,
                  workspace: torch.Tensor | None = None, stage_events=None, return_path: bool = False,
-                 rows_per_tile: int = 0, pad_h: int = 0, pad_w: int = 0, return_gemm: bool = False):
+                 rows_per_tile: int = 0, pad_h: int = 0, pad_w: int = 0, return_gemm: bool = False,
+                 gemm_kernel: int = 0, split_k: int = 0, return_split: bool = False):
     """mec_conv_forward_ex: O = MEC(I, K, s) (Algorithm 2), O in n-h-w-c
     (or h-n-w-c with sola_fix=MEC_SOLA_FIX_NONE when Solution A runs).  pad_h / pad_w:
     zero padding applied virtually inside the lowering (never materialised).
-    return_path / return_gemm: also return the path that ran (1 = A, 2 = B, 3 = fused)
-    / the window-GEMM kernel that ran (1 = one window per tile, 2 = h-sweep)."""
+    return_path / return_gemm / return_split: also return the path that ran (1 = A, 2 = B,
+    3 = fused) / the window-GEMM kernel that ran (1 = one window per tile, 2 = h-sweep,
+    3 = CTA pair) / the CTA-pair kernel's split-K count.  gemm_kernel forces the kernel
+    (0 = automatic), split_k the CTA-pair kernel's K ranges (0 = automatic)."""
     _cuda(I, "I")
     _cuda(K, "K")
     if K.dtype != I.dtype:
@@ -147,6 +153,7 @@ def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torc
     opt.path, opt.T, opt.sola_fix = int(path), int(T), int(sola_fix)
     opt.rows_per_tile = int(rows_per_tile)
     opt.pad_h, opt.pad_w = int(pad_h), int(pad_w)
+    opt.gemm_kernel, opt.split_k = int(gemm_kernel), int(split_k)
     if workspace is not None:
         _cuda(workspace, "workspace")
         opt.workspace = workspace.data_ptr()
@@ -158,7 +165,8 @@ def conv_forward(I: torch.Tensor, K: torch.Tensor, s_h: int, s_w: int, out: torc
                                         ctypes.byref(_shape(i_n, i_h, i_w, i_c, k_h, k_w, k_c)),
                                         s_h, s_w, dtype_code(I.dtype), _stream(I), ctypes.byref(opt))
     _lib.check(st, "mec_conv_forward")
-    extra = ([opt.selected_path] if return_path else []) + ([opt.selected_gemm] if return_gemm else [])
+    extra = (([opt.selected_path] if return_path else []) + ([opt.selected_gemm] if return_gemm else [])
+             + ([opt.selected_split] if return_split else []))
     return (out, *extra) if extra else out
 
 

@@ -135,13 +135,15 @@ def test_table2_layers_small_batch(cuda_ok, name, dtype):
     I, K = make_inputs(shape, dtype, seed=2000 + int(name[2:]))
     ref = oracle.direct_conv(I, K, s, s, n_threads=8)
     Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
-    O_auto = mec.conv_forward(Id, Kd, s, s)
+    O_auto, g_auto = mec.conv_forward(Id, Kd, s, s, return_gemm=True)
     other = (MEC_PATH_SOLUTION_B if mec.select_path(shape, s, s) == MEC_PATH_SOLUTION_A
              else MEC_PATH_SOLUTION_A)
-    O_other = mec.conv_forward(Id, Kd, s, s, path=other)
+    O_other, g_other = mec.conv_forward(Id, Kd, s, s, path=other, return_gemm=True)
     torch.cuda.synchronize()
     check_O(O_auto, ref, dtype, k_h * k_w * i_c)
-    assert torch.equal(O_auto, O_other)
+    check_O(O_other, ref, dtype, k_h * k_w * i_c)
+    if 3 not in (g_auto, g_other):  # same MMA sequence per element unless split-K regrouped it
+        assert torch.equal(O_auto, O_other)
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "tf32"])
@@ -772,3 +774,45 @@ def test_non_finite_input_documented_behaviour(cuda_ok, path):
     bar = tol("tf32", 72, np.where(nan_ref, 0.0, ref))
     assert np.abs(got[fin] - ref[fin]).max() <= bar
     assert not np.any(nan_got[0])  # the other image is untouched
+
+
+# ------------------------------- the CTA-pair (cta_group::2) split-K kernel
+
+WIDE_CASES = [("cv12", 2), ("cv12", 9), ("cv6", 3), ("cv5", 2), ("cv11", 4), ("cv10", 3)]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("split", [0, 1, 2, 3, 5])
+@pytest.mark.parametrize("name,batch", WIDE_CASES)
+def test_wide_pair_kernel(cuda_ok, name, batch, split, dtype):
+    """Solution A on CTA pairs (M = 256 across two SMs) with K split
+    into `split` ranges whose fp32 partials are summed in range order: within the
+    north_star tolerance of the oracle, deterministic run to run, and with one
+    range the same MMA sequence per element as the one-window kernel."""
+    i_h, i_w, i_c, k_h, k_w, k_c, s = synth.TABLE2[name]
+    shape = (batch, i_h, i_w, i_c, k_h, k_w, k_c)
+    I, K = make_inputs(shape, dtype, seed=6000 + int(name[2:]) + batch)
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    O, g, used = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_SOLUTION_A, gemm_kernel=3, split_k=split,
+                                  return_gemm=True, return_split=True)
+    O2 = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_SOLUTION_A, gemm_kernel=3, split_k=split)
+    torch.cuda.synchronize()
+    assert g == 3 and used >= 1 and (split == 0 or used <= split)
+    check_O(O, ref, dtype, k_h * k_w * i_c)
+    assert torch.equal(O, O2)
+    if used == 1:
+        O1 = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_SOLUTION_A, gemm_kernel=1)
+        torch.cuda.synchronize()
+        assert torch.equal(O, O1)
+
+
+def test_wide_pair_kernel_refuses_other_layouts(cuda_ok):
+    """Forced CTA-pair kernel where it does not apply (per-image tiles, o_w >= 32):
+    MEC_ERR_UNSUPPORTED, not a silent fallback."""
+    shape, s = (2, 30, 40, 64, 3, 3, 128), 1
+    I, K = make_inputs(shape, "bf16", seed=1)
+    with pytest.raises(MecError):
+        mec.conv_forward(to_dev(I, "bf16"), to_dev(K, "bf16"), s, s, path=MEC_PATH_SOLUTION_B, gemm_kernel=3)
+    with pytest.raises(MecError):
+        mec.conv_forward(to_dev(I, "bf16"), to_dev(K, "bf16"), s, s, path=MEC_PATH_SOLUTION_A, gemm_kernel=3)
