@@ -112,11 +112,13 @@ typedef struct {
   int pad_h, pad_w;
   int selected_gemm; /* OUT: the window-GEMM kernel that ran: 1 = one window per tile
                         (DESIGN.md 6.2), 2 = h-sweep with A in TMEM (6.2b), 3 = CTA-pair
-                        (cta_group::2) kernel with split-K (6.7), 0 = none */
+                        (cta_group::2) kernel with split-K (6.7), 4 = CTA-pair atom-major
+                        sweep (6.8), 0 = none */
   /* ABI version 5.  gemm_kernel (IN) forces the window-GEMM kernel: 0 = automatic
    * (the CTA-pair kernel for tensor-bound Solution A layers with o_w < 32, else
-   * the h-sweep where it applies, else one window per tile), 1 = one window per
-   * tile, 2 = h-sweep, 3 = CTA pair.  A forced kernel that cannot run the
+   * the h-sweep where it applies, else the CTA-pair atom-major sweep where it
+   * applies, else one window per tile), 1 = one window per tile, 2 = h-sweep,
+   * 3 = CTA pair with split-K, 4 = CTA-pair atom-major sweep.  A forced kernel that cannot run the
    * problem returns MEC_ERR_UNSUPPORTED.  split_k (IN): K ranges of the CTA-pair
    * kernel, 0 = automatic (1..8 by a wave model); the ranges' fp32 partials are
    * summed in range order, so the result depends on split_k but not on timing.

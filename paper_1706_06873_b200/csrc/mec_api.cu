@@ -171,6 +171,18 @@ void set_window_geometry(Plan* p, int64_t kw_s) {
   p->ws_bytes = p->off_kt + p->bytes_kt + 1024;
 }
 
+// The atom-major pair sweep where the h-sweep does not apply (its TMEM ring
+// cannot hold the window: VGG conv1_2 in tf32) or runs with a single
+// accumulator (rows serialised on it: cv8, k_c = 128).  Measured on B200:
+// C2 tf32 GEMM 1306 -> 695 us (the one-window kernel before), cv8 b128 337 ->
+// 298 us; where the h-sweep has two accumulators it stays faster (C2 bf16 311
+// vs 379 us, C3 91 vs 112 us).  MEC_PAIR_SWEEP=1 / 0 forces the choice.
+bool pair_sweep_preferred(const Plan& p, bool batch_folded) {
+  if (const char* e = getenv("MEC_PAIR_SWEEP")) return atoi(e) != 0;
+  int a, n_acc, c, d;
+  return !sweep_config(p, batch_folded, &a, &n_acc, &c, &d) || n_acc == 1;
+}
+
 Plan strip_padded_plan(const Plan& p) {
   Plan q = p;
   if (p.kwc_s > 0) set_window_geometry(&q, p.kwc_s);
@@ -371,7 +383,7 @@ struct Resolved {
   int path;        // MEC_PATH_SOLUTION_A / _B / _FUSED
   bool gather_kt;  // the fused gather variant's weight-operand layout
   int gemm;        // window-GEMM kernel: 0 = h-sweep if it applies else one window, 1 = one window,
-                   // 2 = h-sweep (forced), 3 = CTA pair
+                   // 2 = h-sweep (forced), 3 = CTA pair (split-K), 4 = CTA-pair atom-major sweep
   size_t ws_need;  // workspace bytes this call needs
 };
 
@@ -397,16 +409,22 @@ mec_status_t resolve(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, con
   const bool spad = p.kwc_s > 0 && path != MEC_PATH_FUSED && opt->rows_per_tile != 1;
   r->pc = spad ? strip_padded_plan(p) : p;
   r->gather_kt = path == MEC_PATH_FUSED && !fused_eligible(p);
-  if (opt->gemm_kernel < 0 || opt->gemm_kernel > 3 || opt->split_k < 0 || opt->split_k > 64)
+  if (opt->gemm_kernel < 0 || opt->gemm_kernel > 4 || opt->split_k < 0 || opt->split_k > 64)
     return MEC_ERR_INVALID_ARG;
   const bool batch_folded = path != MEC_PATH_SOLUTION_B;
   const bool wide_ok = !spad && wide_eligible(r->pc, batch_folded, path == MEC_PATH_FUSED) &&
                        opt->sola_fix == MEC_SOLA_FIX_EPILOGUE;
+  const bool ps_ok = !spad && pair_sweep_eligible(r->pc, batch_folded, path == MEC_PATH_FUSED);
   if (opt->gemm_kernel == 3) {
     if (!wide_ok) return MEC_ERR_UNSUPPORTED;
     r->gemm = 3;
+  } else if (opt->gemm_kernel == 4) {
+    if (!ps_ok) return MEC_ERR_UNSUPPORTED;
+    r->gemm = 4;
   } else if (opt->gemm_kernel == 0 && opt->rows_per_tile == 0 && wide_ok && wide_preferred(r->pc)) {
     r->gemm = 3;
+  } else if (opt->gemm_kernel == 0 && opt->rows_per_tile == 0 && ps_ok && pair_sweep_preferred(r->pc, batch_folded)) {
+    r->gemm = 4;
   } else {
     r->gemm = opt->gemm_kernel == 0 ? (opt->rows_per_tile == 0 ? 0 : 1) : opt->gemm_kernel;
   }
@@ -473,6 +491,9 @@ cudaError_t run_conv(const Resolved& r, const void* I, const void* K, void* O, v
   if (r.gemm == 3) {
     opt->selected_gemm = 3;
     e = launch_wide_gemm(pc, ga, wide_scratch, wide_bytes, opt->split_k, st, launches, &opt->selected_split);
+  } else if (r.gemm == 4) {
+    opt->selected_gemm = 4;
+    e = launch_pair_sweep(pc, ga, st, launches);
   } else {
     e = cudaErrorNotSupported;
     opt->selected_gemm = 2;

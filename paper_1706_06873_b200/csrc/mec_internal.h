@@ -141,6 +141,12 @@ uint32_t wide_zero_words(const Plan& p);
 cudaError_t launch_wide_gemm(const Plan& p, const GemmArgs& a, void* scratch, size_t scratch_bytes, int split,
                              cudaStream_t st, int* launches, int* split_used);
 
+// Window GEMMs as an atom-major sweep along h on CTA pairs (pair_sweep.cu):
+// windows starting on 128-byte atom boundaries (shift a whole number of
+// atoms), any window width, weights resident (k_c / 2 rows per CTA).
+bool pair_sweep_eligible(const Plan& p, bool batch_folded, bool fused);
+cudaError_t launch_pair_sweep(const Plan& p, const GemmArgs& a, cudaStream_t st, int* launches);
+
 // Solution A format fix, paper-literal (Alg.2 l.13-19): "Copy L = O" and the
 // block transpose O[n,h,:] = L[h,n,:].
 cudaError_t launch_sola_copy(const Plan& p, const void* O, void* Laux, cudaStream_t st,

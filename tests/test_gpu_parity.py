@@ -816,3 +816,68 @@ def test_wide_pair_kernel_refuses_other_layouts(cuda_ok):
         mec.conv_forward(to_dev(I, "bf16"), to_dev(K, "bf16"), s, s, path=MEC_PATH_SOLUTION_B, gemm_kernel=3)
     with pytest.raises(MecError):
         mec.conv_forward(to_dev(I, "bf16"), to_dev(K, "bf16"), s, s, path=MEC_PATH_SOLUTION_A, gemm_kernel=3)
+
+
+# ---------------------------- the CTA-pair atom-major sweep (gemm_kernel 4)
+
+PS_CASES = [
+    # shape, s, path
+    ((3, 30, 230, 64, 3, 3, 64), 1, MEC_PATH_SOLUTION_B),   # VGG conv1_2-like rows (o_w 228: 2 CTA tiles per image)
+    ((1, 20, 140, 64, 3, 3, 64), 1, MEC_PATH_SOLUTION_B),   # odd CTA-tile count: the last pair's second CTA is empty
+    ((2, 40, 112, 64, 3, 3, 128), 1, MEC_PATH_SOLUTION_B),  # cv8-like (k_c 128: 4 accumulators)
+    ((5, 56, 56, 64, 3, 3, 64), 1, MEC_PATH_SOLUTION_A),    # cv9 / C3 (2 image slots per CTA tile)
+    ((3, 21, 80, 32, 5, 3, 48), 2, MEC_PATH_SOLUTION_A),    # s_h = 2, k_c 48, o_w 39 (64-row slots)
+    ((2, 17, 70, 128, 2, 2, 32), 1, MEC_PATH_SOLUTION_B),   # shift = 2 atoms, window 4 atoms
+]
+
+
+PS_TOO_WIDE = {(2, "tf32")}
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("case", range(len(PS_CASES)))
+def test_pair_sweep_kernel(cuda_ok, case, dtype):
+    """Atom-major sweep on CTA pairs: every L column read once per
+    work item, each atom's MMAs into every open row's accumulator."""
+    shape, s, path = PS_CASES[case]
+    I, K = make_inputs(shape, dtype, seed=8000 + case)
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    if (case, dtype) in PS_TOO_WIDE:
+        # fp32 weights of k_c 128 x kdim 576 (147 KB per CTA) do not fit resident: refused
+        with pytest.raises(MecError):
+            mec.conv_forward(Id, Kd, s, s, path=path, gemm_kernel=4)
+        return
+    O, g = mec.conv_forward(Id, Kd, s, s, path=path, gemm_kernel=4, return_gemm=True)
+    torch.cuda.synchronize()
+    assert g == 4
+    check_O(O, ref, dtype, shape[3] * shape[4] * shape[5])
+    # same K steps per row as the one-window kernel
+    O1 = mec.conv_forward(Id, Kd, s, s, path=path, gemm_kernel=1)
+    torch.cuda.synchronize()
+    assert torch.equal(O, O1)
+    if path == MEC_PATH_SOLUTION_A:  # the paper-literal format fix stores h-n-w-c first
+        OL = mec.conv_forward(Id, Kd, s, s, path=path, gemm_kernel=4, sola_fix=MEC_SOLA_FIX_LITERAL)
+        torch.cuda.synchronize()
+        assert torch.equal(O, OL)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_C2_pair_sweep_full_batch_sampled(cuda_ok, dtype):
+    """C2 at b64 through the pair sweep (tf32: the automatic choice)."""
+    c = "C2" if dtype == "bf16" else "C2_tf32"
+    cfg = synth.config(c)
+    shape = (cfg["i_n"], cfg["i_h"], cfg["i_w"], cfg["i_c"], cfg["k_h"], cfg["k_w"], cfg["k_c"])
+    seed = synth.SEED_BASE + cfg["index"]
+    kind = synth.KIND_GRID8 if dtype == "bf16" else synth.KIND_GRID11
+    Id = torch.empty(shape[:4], dtype=TDT[dtype], device="cuda")
+    Kd = torch.empty((cfg["k_h"], cfg["k_w"], cfg["i_c"], cfg["k_c"]), dtype=TDT[dtype], device="cuda")
+    mec.synth_fill(Id, seed, synth.TENSOR_I, kind)
+    mec.synth_fill(Kd, seed, synth.TENSOR_K, kind)
+    O, g = mec.conv_forward(Id, Kd, 1, 1, gemm_kernel=4, return_gemm=True)
+    torch.cuda.synchronize()
+    assert g == 4
+    K = synth.kernel_tensor(cfg, kind, seed)
+    for n in (0, 37, 63):
+        I = synth.input_images(cfg, n, 1, kind, seed)
+        check_O(O[n:n + 1], oracle.direct_conv(I, K, 1, 1, n_threads=8), dtype, 576)
