@@ -28,15 +28,18 @@ KEYS = [
     "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
     "launch__shared_mem_per_block_dynamic", "sm__cycles_elapsed.avg", "smsp__cycles_active.avg",
+    "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum",
 ]
 
 
 def short(name):
-    for k in ("lower_kernel", "window_gemm_kernel", "sweep_gemm_kernel", "copy16_kernel", "block_permute_kernel", "flush_kernel",
-              "synth_kernel", "fused"):
+    for k in ("lower_kernel", "window_gemm_kernel", "sweep_gemm_kernel", "wide_gemm_kernel", "pair_sweep_kernel",
+              "copy16_kernel", "block_permute_kernel", "flush_kernel", "synth_kernel", "fused"):
         if k in name:
+            # every window-GEMM kernel is the "window_gemm" stage of bench.py
             return {"lower_kernel": "mec_lower", "window_gemm_kernel": "window_gemm",
-                    "sweep_gemm_kernel": "window_gemm",  # the window GEMM stage (h-sweep kernel)
+                    "sweep_gemm_kernel": "window_gemm", "wide_gemm_kernel": "window_gemm",
+                    "pair_sweep_kernel": "window_gemm",
                     "copy16_kernel": "sola_copy", "block_permute_kernel": "sola_transpose"}.get(k, k)
     return name[:40]
 
@@ -107,14 +110,38 @@ def main():
                 v = float(r[h.index(k)].replace(",", ""))
                 u = units[h.index(k)]
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-            acc[name].append(val("dram__bytes_read.sum") + val("dram__bytes_write.sum"))
+            def num(k):
+                try:
+                    return float(r[h.index(k)].replace(",", ""))
+                except (ValueError, IndexError):
+                    return None
+            acc[name].append({
+                "dram_bytes": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
+                "dram_read": val("dram__bytes_read.sum"), "dram_write": val("dram__bytes_write.sum"),
+                "tensor_pipe_pct": num("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+                "l2_to_sm_tma_bytes": val("l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum")
+                if "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum" in h else None,
+                "duration_us": val("gpu__time_duration.sum") / 1e3 if units[h.index("gpu__time_duration.sum")] == "ns"
+                else val("gpu__time_duration.sum"),
+                "kernel_name": r[h.index("Kernel Name")][:120],
+            })
         with open(base + "_ncu.txt", "w") as f:
             f.write("\n".join(lines) + "\n")
         traffic.setdefault(args.config, {})
+        metrics_path = os.path.join(ROOT, "profiles", "ncu_metrics.json")
+        metrics = json.load(open(metrics_path)) if os.path.exists(metrics_path) else {}
+        metrics.setdefault(args.config, {})
         for k, v in acc.items():
-            traffic[args.config][k] = sum(v) / len(v)
+            traffic[args.config][k] = sum(x["dram_bytes"] for x in v) / len(v)
+            m = {key: (sum(x[key] for x in v) / len(v) if all(isinstance(x[key], float) for x in v) else v[-1][key])
+                 for key in v[-1]}
+            m["launches_averaged"] = len(v)
+            m["source"] = os.path.relpath(base + "_ncu.txt", ROOT)
+            metrics[args.config][k] = m
         with open(traffic_path, "w") as f:
             json.dump(traffic, f, indent=1, sort_keys=True)
+        with open(metrics_path, "w") as f:
+            json.dump(metrics, f, indent=1, sort_keys=True)
     print("wrote", base + "*")
 
 
