@@ -50,7 +50,7 @@ namespace {
 constexpr int kPsThreads = 64 + 2 * 128;
 constexpr uint32_t kPsStageOut = 32 * 128;        // epilogue staging per warp
 constexpr size_t kPsSmemBudget = 227 * 1024;
-constexpr size_t kPsMaxResident = 112 * 1024;     // per CTA: k_c/2 weight rows x kdim
+constexpr size_t kPsMaxResident = 112 * 1024;     // per CTA: k_c/2 weight rows x kdim (else streamed)
 
 struct PsParams {
   void* O;
@@ -68,8 +68,14 @@ struct PsParams {
   int n_acc;             // TMEM accumulators (bn columns each)
   int stages;
   uint32_t a_bytes;      // this CTA's A bytes per atom (TMA boxes)
-  uint32_t b_half_bytes; // bn/2 rows x 128 bytes: one resident weight atom per CTA
+  uint32_t b_half_bytes; // bn/2 rows x 128 bytes: one weight atom per CTA
+  // weights resident (b_stream = false), or streamed with A: stage s holds
+  // the A atom and, for each open row, that row's weight atom (b_open slots)
+  bool b_stream;
+  int b_open;
+  uint32_t stage_bytes;  // A (16 KB) [+ b_open x b_half_bytes]
   uint32_t idesc;
+  bool a_evict_first;    // (experiments: MEC_PS_EVICT_FIRST=1) L2 evict-first hint on the L stream
 };
 
 // CTA tile c -> the image and first row (w) of each of its rows' slots
@@ -103,8 +109,8 @@ __global__ void __launch_bounds__(kPsThreads, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + kSmemAlign - 1) & ~uintptr_t(kSmemAlign - 1));
   const int S = p.stages;
-  unsigned char* smemB = smem + static_cast<size_t>(S) * kBM * kTileKBytes;  // resident weights
-  unsigned char* stg_base = smemB + static_cast<size_t>(p.na) * p.b_half_bytes;
+  unsigned char* smemB = smem + static_cast<size_t>(S) * p.stage_bytes;  // resident weights (if any)
+  unsigned char* stg_base = smemB + (p.b_stream ? 0 : static_cast<size_t>(p.na) * p.b_half_bytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + 8 * kPsStageOut);
   uint64_t* full = bars;                  // [S] leader
   uint64_t* empty = bars + S;             // [S] each CTA
@@ -136,6 +142,7 @@ __global__ void __launch_bounds__(kPsThreads, 1)
   }
   if (warp == 1) ptx::tmem_alloc_pair(tmem_slot, 512);
   ptx::tc_fence_before();
+  __syncthreads();      // the allocator's write of tmem_slot before any read (a CTA barrier racecheck models)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -143,19 +150,20 @@ __global__ void __launch_bounds__(kPsThreads, 1)
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
-      const uint64_t hintA = ptx::policy_evict_first();  // L is streamed once
+      // L columns are streamed once per item; adjacent chunks of the same tile
+      // (run at the same time by neighbouring pairs) share na - sa atoms in L2
+      const uint64_t hintA = p.a_evict_first ? ptx::policy_evict_first() : ptx::policy_evict_normal();
       const uint64_t hintB = ptx::policy_evict_last();
       ptx::griddep_wait();  // L and Kt come from the preceding (lowering) kernel
       const uint32_t full0 = ptx::mapa_shared(ptx::smem_u32(full), 0);
       const uint32_t bfull0 = ptx::mapa_shared(ptx::smem_u32(bfull), 0);
-      if (pair < p.n_items) {
+      if (pair < p.n_items && !p.b_stream) {
         // this CTA's half of the weights (k_c/2 rows of every window atom), resident
         if (leader) ptx::mbar_arrive_expect_tx(bfull, 2u * static_cast<uint32_t>(p.na) * p.b_half_bytes);
         for (int a = 0; a < p.na; ++a)
           ptx::tma_load_2d_pair(smemB + static_cast<size_t>(a) * p.b_half_bytes, &tmB, bfull0, a * p.bk,
                                 static_cast<int32_t>(rank * (p.bn / 2)), hintB);
       }
-      const uint32_t tx = 2u * p.a_bytes;
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t it = pair; it < p.n_items; it += n_pairs) {
@@ -166,10 +174,18 @@ __global__ void __launch_bounds__(kPsThreads, 1)
         const CTile t = ctile(p, 2 * pt + rank);
         const int32_t x0 = static_cast<int32_t>(h0 * p.shift);
         for (int j = 0; j < n_stream; ++j) {
+          // streamed weights: the open rows r_lo..r_hi of this atom each need weight atom j - r sa
+          const int r_hi = min(rows - 1, j / p.sa);
+          const int r_lo = j >= p.na ? (j - p.na) / p.sa + 1 : 0;
+          const uint32_t nb = p.b_stream ? static_cast<uint32_t>(r_hi - r_lo + 1) : 0u;
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], tx);
-          unsigned char* dA = smem + static_cast<size_t>(stage) * kBM * kTileKBytes;
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2u * (p.a_bytes + nb * p.b_half_bytes));
+          unsigned char* dA = smem + static_cast<size_t>(stage) * p.stage_bytes;
           const uint32_t fb = full0 + static_cast<uint32_t>(stage) * 8u;
+          for (uint32_t k = 0; k < nb; ++k)
+            ptx::tma_load_2d_pair(dA + kBM * kTileKBytes + k * p.b_half_bytes, &tmB, fb,
+                                  (j - (r_lo + static_cast<int>(k)) * p.sa) * p.bk,
+                                  static_cast<int32_t>(rank * (p.bn / 2)), hintB);
           const int32_t x = x0 + j * p.bk;
           if (p.ipt == 1) {
             ptx::tma_load_3d_pair(dA, &tmA, fb, x, static_cast<int32_t>(t.w0), static_cast<int32_t>(t.n0), hintA);
@@ -190,8 +206,9 @@ __global__ void __launch_bounds__(kPsThreads, 1)
     if (leader && pair < p.n_items) {
       const uint64_t adesc0 = ptx::smem_desc_sw128(ptx::smem_u32(smem));
       const uint64_t bdesc0 = ptx::smem_desc_sw128(ptx::smem_u32(smemB));
-      const uint32_t a_stage16 = (kBM * kTileKBytes) >> 4, b16 = p.b_half_bytes >> 4;
-      ptx::mbar_wait(bfull, 0);
+      const uint32_t a_stage16 = p.stage_bytes >> 4, b16 = p.b_half_bytes >> 4;
+      const uint32_t a_to_b16 = (kBM * kTileKBytes) >> 4;
+      if (!p.b_stream) ptx::mbar_wait(bfull, 0);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t row_seq = 0;  // rows started so far by this CTA pair (accumulator rotation)
@@ -214,8 +231,11 @@ __global__ void __launch_bounds__(kPsThreads, 1)
           for (int r = r_lo; r <= r_hi; ++r) {
             const int a = j - r * p.sa;  // the row's window atom
             const uint32_t q = row_seq + static_cast<uint32_t>(r);
-            ptx::mma_ss_atom_pair_elect<kTF32>(tmem_base + (q % p.n_acc) * static_cast<uint32_t>(p.bn), ad,
-                                               bdesc0 + static_cast<uint32_t>(a) * b16, p.idesc, a != 0 ? 1u : 0u);
+            // weights: resident atom a, or the stage's slot r - r_lo
+            const uint64_t bd = p.b_stream ? ad + a_to_b16 + static_cast<uint32_t>(r - r_lo) * b16
+                                           : bdesc0 + static_cast<uint32_t>(a) * b16;
+            ptx::mma_ss_atom_pair_elect<kTF32>(tmem_base + (q % p.n_acc) * static_cast<uint32_t>(p.bn), ad, bd,
+                                               p.idesc, a != 0 ? 1u : 0u);
           }
           ptx::mma_commit_pair_elect(&empty[stage], 0x3);
           if (j - r_lo * p.sa == p.na - 1)  // the oldest open row is complete
@@ -335,7 +355,9 @@ struct PsGeo {
   int ipt, slot;
   int64_t mt_per_img, n_ctile, n_pt;
   int sa, na, n_acc, stages;
-  uint32_t a_bytes, b_half_bytes;
+  uint32_t a_bytes, b_half_bytes, stage_bytes;
+  bool b_stream;
+  int b_open;
   size_t smem;
 };
 
@@ -361,11 +383,16 @@ bool ps_geo(const Plan& pl, bool batch_folded, PsGeo* g) {
   g->n_acc = std::min(8, 512 / pl.bn);
   if (g->n_acc < open + 1) return false;
   g->b_half_bytes = static_cast<uint32_t>(pl.bn / 2 * kTileKBytes);
-  const size_t b_res = static_cast<size_t>(g->na) * g->b_half_bytes;
-  if (b_res > kPsMaxResident) return false;
+  size_t b_res = static_cast<size_t>(g->na) * g->b_half_bytes;
+  // weights that do not fit resident (cv4: 49 atoms) are streamed with A: the
+  // open rows' weight atoms ride in the stage (<= `open` x k_c/2 rows)
+  g->b_stream = b_res > kPsMaxResident || (getenv("MEC_PS_BSTREAM") && atoi(getenv("MEC_PS_BSTREAM")) != 0);
+  g->b_open = open;
+  if (g->b_stream) b_res = 0;
   g->a_bytes = static_cast<uint32_t>(g->ipt == 1 ? kBM * kTileKBytes : g->ipt * g->slot * kTileKBytes);
+  g->stage_bytes = static_cast<uint32_t>(kBM * kTileKBytes + (g->b_stream ? open * g->b_half_bytes : 0));
   const size_t fixed = kSmemAlign + b_res + 8 * kPsStageOut + 32 * 8 + 64;
-  const size_t stage = static_cast<size_t>(kBM) * kTileKBytes;
+  const size_t stage = g->stage_bytes;
   if (fixed + 2 * stage > kPsSmemBudget) return false;
   g->stages = static_cast<int>(std::min<size_t>(12, (kPsSmemBudget - fixed) / stage));
   g->smem = fixed + g->stages * stage;
@@ -405,6 +432,10 @@ cudaError_t launch_pair_sweep(const Plan& pl, const GemmArgs& a, cudaStream_t st
   p.stages = g.stages;
   p.a_bytes = g.a_bytes;
   p.b_half_bytes = g.b_half_bytes;
+  p.b_stream = g.b_stream;
+  p.b_open = g.b_open;
+  p.stage_bytes = g.stage_bytes;
+  p.a_evict_first = getenv("MEC_PS_EVICT_FIRST") && atoi(getenv("MEC_PS_EVICT_FIRST")) != 0;
   p.idesc = ptx::instr_desc(tf32, 2 * kBM, pl.bn);
   auto kern = tf32 ? pair_sweep_kernel<true> : pair_sweep_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));

@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
   }
   if (warp == 1) ptx::tmem_alloc_pair(tmem_slot, 512);
   ptx::tc_fence_before();
+  __syncthreads();      // the allocator's write of tmem_slot before any read (a CTA barrier racecheck models)
   ptx::cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
@@ -445,10 +446,13 @@ WideGeo wide_geo(const Plan& pl, int split) {
 }  // namespace
 
 bool wide_eligible(const Plan& pl, bool batch_folded, bool fused) {
-  if (fused || !batch_folded || pl.o_w >= 32) return false;  // Solution A, flat rows
+  // Solution A: the batch-folded rows n o_w + w of Alg.2 l.9's L matrix, 256
+  // per pair tile (rows of several images share a tile; the epilogue computes
+  // each row's own output address)
+  if (fused || !batch_folded) return false;
   if (pl.bn < 64 || pl.bn % 32 != 0) return false;          // N/2 rows of B per CTA, 16-aligned
   if ((pl.s.k_c * pl.elt) % 16 != 0) return false;           // 16-byte output stores
-  if (pl.kdim_pad / pl.bk < 8) return false;
+  if (pl.kdim_pad / pl.bk < 2) return false;
   if (pl.s.i_n * pl.o_w >= (1LL << 31)) return false;
   return true;
 }
