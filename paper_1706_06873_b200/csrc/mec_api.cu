@@ -225,7 +225,7 @@ mec_status_t make_plan(const mec_shape_t* s_in, int s_h, int s_w, mec_dtype_t dt
   p->kdim_g = round_up(s->k_h * p->kwc_p, p->bk);
   p->kdim_src = s->k_h * s->k_w * s->i_c;
   set_window_geometry(p, s->k_w * s->i_c);
-  // Strip padding of the conv-path L (DESIGN.md 6.6): when the window shift
+  // Strip padding of the conv-path L (DESIGN.md 6.9): when the window shift
   // s_h k_w i_c is not a whole 32-byte MMA K step (AlexNet conv1: 132
   // elements), every strip of k_w i_c elements is stored with kwc_s - k_w i_c
   // zeros after it, kwc_s the smallest length making s_h kwc_s a multiple of
@@ -404,7 +404,7 @@ mec_status_t resolve(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, con
   if (path == MEC_PATH_SOLUTION_A && opt->sola_fix == MEC_SOLA_FIX_LITERAL && p.n_O > p.n_L)
     return MEC_ERR_UNSUPPORTED;
   r->path = path;
-  // the conv path's L: the strip-padded layout (DESIGN.md 6.6) where the plan
+  // the conv path's L: the strip-padded layout (DESIGN.md 6.9) where the plan
   // has one and multi-row tiles are not switched off; the fused path reads I
   const bool spad = p.kwc_s > 0 && path != MEC_PATH_FUSED && opt->rows_per_tile != 1;
   r->pc = spad ? strip_padded_plan(p) : p;

@@ -31,7 +31,7 @@ struct Plan {
   // its strip length: k_w i_c (the paper's dense L), or kwc_s in the
   // strip-padded plan (strip_padded_plan; the extra elements are zeros).
   int64_t strip;
-  int64_t kwc_s;         // strip-padded length for the conv path, 0 = not used (DESIGN.md 6.6)
+  int64_t kwc_s;         // strip-padded length for the conv path, 0 = not used (DESIGN.md 6.9)
   int64_t kdim_src;      // k_h k_w i_c (the paper's reduction length, whatever the strip)
   int64_t l_cols;        // i_h strip: one row of L (Alg.2 l.9 / l.21 "i_h k_w i_c")
   int64_t pitch;         // l_cols rounded up to 16 B (TMA stride rule), elements
@@ -126,7 +126,8 @@ cudaError_t launch_window_gemm(const Plan& p, const GemmArgs& a, cudaStream_t st
 // output rows instead of once per row.  Returns cudaErrorNotSupported (and
 // launches nothing) where it does not apply; the caller then runs
 // launch_window_gemm.
-bool sweep_config(const Plan& p, bool batch_folded, int* n_vres, int* n_acc, int* ns, int* stages);
+bool sweep_config(const Plan& p, bool batch_folded, int* n_vres, int* n_acc, int* ns, int* stages,
+                  bool pair = false);
 cudaError_t launch_sweep_gemm(const Plan& p, const GemmArgs& a, cudaStream_t st, int* launches);
 
 // Window GEMMs of the tensor-bound layers on CTA pairs (wide_gemm.cu):

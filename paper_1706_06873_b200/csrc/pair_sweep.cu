@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kPsThreads, 1)
           // a row starting here needs its accumulator drained (row r_hi starts iff j == r_hi sa)
           if (j == r_hi * p.sa) {
             const uint32_t q = row_seq + static_cast<uint32_t>(r_hi);
-            ptx::mbar_wait(&tempty[q % p.n_acc], ((q / p.n_acc) & 1u) ^ 1u);
+            ptx::mbar_wait_cluster(&tempty[q % p.n_acc], ((q / p.n_acc) & 1u) ^ 1u);
           }
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();

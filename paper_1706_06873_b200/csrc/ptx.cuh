@@ -65,6 +65,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// As mbar_wait, with cluster-scope acquire: for barriers that a peer CTA of
+// the cluster arrives on (remote mbarrier.arrive.release.cluster).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
 // try_wait with a nanosleep backoff between failed probes: for waits that are
 // usually long (epilogue waiting for an accumulator, producer waiting for a
 // slot), so idle warps do not keep the mbarrier unit busy.
@@ -535,10 +548,10 @@ __device__ __forceinline__ void mma_ts_groups_elect(uint32_t tmem_d, uint32_t a_
       "add.u32 a1, c, 8;\n\tadd.u32 a2, c, 16;\n\tadd.u32 a3, c, 24;\n\t"                                \
       "add.u32 l1, b, 2;\n\tadd.u32 l2, b, 4;\n\tadd.u32 l3, b, 6;\n\t"                                  \
       "mov.b64 b0, {b, hi};\n\tmov.b64 b1, {l1, hi};\n\tmov.b64 b2, {l2, hi};\n\tmov.b64 b3, {l3, hi};\n\t" \
-      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [c], b0, %6, p;\n\t"                                \
-      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a1], b1, %6, 1;\n\t"                               \
-      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a2], b2, %6, 1;\n\t"                               \
-      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a3], b3, %6, 1;\n\t"                               \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [c], b0, %6, p;\n\t"                        \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a1], b1, %6, 1;\n\t"                       \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a2], b2, %6, 1;\n\t"                       \
+      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a3], b3, %6, 1;\n\t"                       \
       "setp.ne.b32 p, 1, 0;\n\t"                                                                       \
       "add.u32 c, c, 32;\n\tsetp.ge.u32 w, c, %2;\n\t@w sub.u32 c, c, %3;\n\t"                          \
       "add.u32 b, b, %5;\n\tadd.u32 g, g, 1;\n\t"                                                      \
@@ -564,13 +577,16 @@ __device__ __forceinline__ void mma_ts_groups_elect(uint32_t tmem_d, uint32_t a_
 // caller advances its own copy of (wslot, wphase, avail) past the last atom
 // the row needs (the elected lane's counters are not returned).  One call per
 // row: no per-group or per-run control code in the warp (latency-bound).
-template <bool kTF32>
+#ifndef MEC_PAIR_WAITSEM
+#define MEC_PAIR_WAITSEM ".acquire.cluster"
+#endif
+template <bool kTF32, bool kPair = false>
 __device__ __forceinline__ void mma_ts_row_elect(uint32_t tmem_d, uint32_t a_tmem, uint32_t ring_end,
                                                  uint32_t ring_cols, uint32_t b_lo, uint32_t b_step,
                                                  uint32_t idesc, int n_groups, int a, int grp_log2, int bkl,
                                                  uint32_t afull_base, int wslot, uint32_t wphase, int avail,
                                                  int ns) {
-#define MEC_TS_ROW_BODY(KIND)                                                                          \
+#define MEC_TS_ROW_BODY(KIND, GRP, WAITSEM)                                                            \
   asm volatile(                                                                                        \
       "{\n\t.reg .pred e, p, w, more, ok, fin;\n\t"                                                    \
       ".reg .b32 c, b, g, a1, a2, a3, l1, l2, l3, hi, need, t, ws, wp, av, bar;\n\t"                    \
@@ -588,7 +604,7 @@ __device__ __forceinline__ void mma_ts_row_elect(uint32_t tmem_d, uint32_t a_tme
       "setp.gt.s32 ok, av, need;\n\t@ok bra READY_%=;\n\t"                                              \
       "mad.lo.u32 bar, ws, 8, %15;\n"                                                                  \
       "SPIN_%=:\n\t"                                                                                   \
-      "mbarrier.try_wait.parity.shared::cta.b64 w, [bar], wp;\n\t"                                     \
+      "mbarrier.try_wait.parity" WAITSEM ".shared::cta.b64 w, [bar], wp;\n\t"                           \
       "@!w bra SPIN_%=;\n\t"                                                                           \
       "add.u32 ws, ws, 1;\n\tsetp.eq.u32 fin, ws, %16;\n\t@fin mov.b32 ws, 0;\n\t@fin xor.b32 wp, wp, 1;\n\t" \
       "add.u32 av, av, 1;\n\tbra WAIT_%=;\n"                                                            \
@@ -597,10 +613,10 @@ __device__ __forceinline__ void mma_ts_row_elect(uint32_t tmem_d, uint32_t a_tme
       "add.u32 a1, c, 8;\n\tadd.u32 a2, c, 16;\n\tadd.u32 a3, c, 24;\n\t"                                \
       "add.u32 l1, b, 2;\n\tadd.u32 l2, b, 4;\n\tadd.u32 l3, b, 6;\n\t"                                  \
       "mov.b64 b0, {b, hi};\n\tmov.b64 b1, {l1, hi};\n\tmov.b64 b2, {l2, hi};\n\tmov.b64 b3, {l3, hi};\n\t" \
-      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [c], b0, %6, p;\n\t"                                \
-      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a1], b1, %6, 1;\n\t"                               \
-      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a2], b2, %6, 1;\n\t"                               \
-      "tcgen05.mma.cta_group::1.kind::" KIND " [%0], [a3], b3, %6, 1;\n\t"                               \
+      "tcgen05.mma.cta_group::" GRP ".kind::" KIND " [%0], [c], b0, %6, p;\n\t"                        \
+      "tcgen05.mma.cta_group::" GRP ".kind::" KIND " [%0], [a1], b1, %6, 1;\n\t"                       \
+      "tcgen05.mma.cta_group::" GRP ".kind::" KIND " [%0], [a2], b2, %6, 1;\n\t"                       \
+      "tcgen05.mma.cta_group::" GRP ".kind::" KIND " [%0], [a3], b3, %6, 1;\n\t"                       \
       "setp.ne.b32 p, 1, 0;\n\t"                                                                       \
       "add.u32 c, c, 32;\n\tsetp.ge.u32 w, c, %2;\n\t@w sub.u32 c, c, %3;\n\t"                          \
       "add.u32 b, b, %5;\n\tadd.u32 g, g, 1;\n\t"                                                      \
@@ -610,10 +626,21 @@ __device__ __forceinline__ void mma_ts_row_elect(uint32_t tmem_d, uint32_t a_tme
       "r"(0), "r"(a), "r"(grp_log2), "r"(bkl), "r"(wslot), "r"(wphase), "r"(avail), "r"(afull_base),   \
       "r"(ns)                                                                                          \
       : "memory")
-  if constexpr (kTF32) {
-    MEC_TS_ROW_BODY("tf32");
+  // kPair: the CTA pair's MMA (cta_group::2, M = 256; A from both CTAs' TMEM
+  // at the same columns) and cluster-scope acquire on the ring barriers, which
+  // the peer CTA's copiers arrive on remotely
+  if constexpr (kPair) {
+    if constexpr (kTF32) {
+      MEC_TS_ROW_BODY("tf32", "2", MEC_PAIR_WAITSEM);
+    } else {
+      MEC_TS_ROW_BODY("f16", "2", MEC_PAIR_WAITSEM);
+    }
   } else {
-    MEC_TS_ROW_BODY("f16");
+    if constexpr (kTF32) {
+      MEC_TS_ROW_BODY("tf32", "1", "");
+    } else {
+      MEC_TS_ROW_BODY("f16", "1", "");
+    }
   }
 #undef MEC_TS_ROW_BODY
 }

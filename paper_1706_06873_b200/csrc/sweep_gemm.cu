@@ -129,6 +129,9 @@ struct SweepParams {
   uint32_t stage_out_bytes;
   uint32_t backoff_ns;  // copier / epilogue waits: nanosleep between probes (0: spin)
   int n_iss;  // MMA issuer warps (1 or 2)
+  // CTA-pair mode (kPair kernels): CTA tiles are dealt in
+  // pairs (CTA rank r takes tile 2 pt + r); n_tiles = n_mt groups
+  int64_t n_tiles;
   // fused (MEC_PATH_FUSED, i_c elt a multiple of 128 B): stream atoms are TMA
   // boxes of I -- column c = hh kwc + b i_c + ci of L row (n, w) is pixel
   // s_w w + b of input row hh, channels ci (Alg.2 l.4-6), so L is never written
@@ -139,16 +142,21 @@ struct SweepParams {
 
 struct SwItem {
   int64_t h0, mt, g;
+  bool valid;  // pair mode: an odd tile count leaves the last pair's second CTA without rows
   int nrows;
   int n_a;     // atoms streamed
   int x0;      // stream start column (multiple of avec)
   int off0;    // h0 shift - x0 (< avec)
 };
 
-__device__ __forceinline__ SwItem sw_decode(const SweepParams& p, int64_t t) {
+__device__ __forceinline__ SwItem sw_decode(const SweepParams& p, int64_t t, bool pair = false,
+                                           uint32_t rank = 0) {
   SwItem it;
   const int64_t hc = t % p.n_hc;
   t /= p.n_hc;
+  if (pair) t = 2 * t + rank;  // pair tile -> this CTA's tile
+  it.valid = t < p.n_tiles;
+  if (!it.valid) t = p.n_tiles - 1;  // (a real tile's coordinates; nothing is stored)
   it.mt = t % p.n_mt;
   it.g = t / p.n_mt;
   // chunk hc: rows [hc o_h / n_hc, (hc + 1) o_h / n_hc) (sizes differ by <= 1)
@@ -182,7 +190,8 @@ template <bool kTF32>
 // next row that uses it can start accumulating while this one is stored.
 __device__ __forceinline__ void sw_store_row(const SweepParams& p, const CUtensorMap* tmO, int64_t h, int64_t mt,
                                              int64_t g, int quarter, int lane, uint32_t taddr, uint32_t stg,
-                                             unsigned char* stg_gen, uint64_t* tempty_bar) {
+                                             unsigned char* stg_gen, uint64_t* tempty_bar, bool valid = true,
+                                             uint32_t tempty_cluster = 0) {
   constexpr int kOutElt = kTF32 ? 4 : 2;
   const int row_bytes = p.pw * kOutElt;
   const int swz_shift = row_bytes == 128 ? 0 : (row_bytes == 64 ? 1 : 2);
@@ -200,6 +209,7 @@ __device__ __forceinline__ void sw_store_row(const SweepParams& p, const CUtenso
     nvalid = (j < p.ipt && n_img < p.i_n) ? min(static_cast<int64_t>(32), p.o_w - w0) : 0;
     gr0 = n_img * p.o_w + w0;
   }
+  if (!valid) nvalid = 0;
   unsigned char* orow_own;
   {
     const int64_t gr = gr0 + lane;
@@ -222,7 +232,10 @@ __device__ __forceinline__ void sw_store_row(const SweepParams& p, const CUtenso
     if (pass == p.n_pass - 1) {
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(tempty_bar);
+      if (lane == 0) {
+        if (tempty_cluster != 0) ptx::mbar_arrive_cluster(tempty_cluster);  // the pair leader's barrier
+        else ptx::mbar_arrive(tempty_bar);
+      }
     }
     if (nvalid <= 0 || c0 >= p.k_c || (p.dbg & 1)) continue;  // warp-uniform
     if (p.tma_store) {
@@ -315,7 +328,7 @@ __device__ __forceinline__ void sw_store_row(const SweepParams& p, const CUtenso
   }
 }
 
-template <bool kTF32>
+template <bool kTF32, bool kPair>
 __global__ void __launch_bounds__(kSwThreads, 1)
     sweep_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmO, const SweepParams p) {
@@ -323,7 +336,9 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + kSmemAlign - 1) & ~uintptr_t(kSmemAlign - 1));
   const int S = p.stages;
-  const uint32_t b_tile_bytes = static_cast<uint32_t>(p.bn) * kTileKBytes;
+  // pair mode: each CTA holds bn / 2 rows of every weight atom (the pair's MMA
+  // reads N/2 columns of B from each CTA)
+  const uint32_t b_tile_bytes = static_cast<uint32_t>(kPair ? p.bn / 2 : p.bn) * kTileKBytes;
   const int n_btiles = p.n_vres * p.nb_atoms;
   unsigned char* smemA = smem;
   unsigned char* smemB = smem + static_cast<size_t>(S) * kSwAtomBytes;
@@ -344,7 +359,10 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  const int64_t t_begin = blockIdx.x, t_step = gridDim.x;
+  const uint32_t rank = kPair ? ptx::cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int64_t t_begin = kPair ? static_cast<int64_t>(ptx::cluster_id_x()) : static_cast<int64_t>(blockIdx.x);
+  const int64_t t_step = kPair ? static_cast<int64_t>(ptx::nclusters_x()) : static_cast<int64_t>(gridDim.x);
 #ifdef MEC_TRACE
   unsigned long long* const sw_tr = g_sweep_trace;
 #endif
@@ -358,19 +376,24 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], kSwCopyWarps);
     }
-    for (int i = 0; i < p.ns; ++i) ptx::mbar_init(&afull[i], kSwCopyWarps);
+    // (pair mode: the leader's ring barriers count both CTAs' copier warps)
+    for (int i = 0; i < p.ns; ++i) ptx::mbar_init(&afull[i], kSwCopyWarps * (kPair ? 2 : 1));
     rows_done[0] = 0;
     rows_done[1] = 0;
     for (int i = 0; i < p.n_acc; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 4);  // the 4 warps of one epilogue group
+      ptx::mbar_init(&tempty[i], kPair ? 8 : 4);  // the 4 warps of one epilogue group (x 2 CTAs)
     }
     ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc_dyn(tmem_slot, 512);
+  if (warp == 1) {
+    if constexpr (kPair) ptx::tmem_alloc_pair(tmem_slot, 512);
+    else ptx::tmem_alloc_dyn(tmem_slot, 512);
+  }
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) ptx::cluster_sync();  // both CTAs' barriers initialised (remote arrives follow)
   ptx::tc_fence_after();
   // broadcast from lane 0: provably warp-uniform, so the MMA warp keeps its
   // operand addresses in uniform registers (no per-MMA R2UR loops)
@@ -388,14 +411,14 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         for (int v = 0; v < p.n_vres; ++v)
           for (int a = 0; a < p.nb_atoms; ++a)
             ptx::tma_load_2d(smemB + static_cast<size_t>(v * p.nb_atoms + a) * b_tile_bytes, &tmB, bfull, a * p.bk,
-                             static_cast<int32_t>(v * p.kc_pad), hintB);
+                             static_cast<int32_t>(v * p.kc_pad + (kPair ? rank * (p.bn / 2) : 0)), hintB);
       }
       SW_TRACE(511u, 2);
       uint32_t pseq = 0;
       int stage = 0;
       uint32_t pphase = 0;
       for (int64_t t = t_begin; t < p.n_items; t += t_step) {
-        const SwItem it = sw_decode(p, t);
+        const SwItem it = sw_decode(p, t, kPair, rank);
         const int32_t y0 = static_cast<int32_t>(it.mt * kBM);
         const int32_t z0 = static_cast<int32_t>(it.g);
         for (int i = 0; i < it.n_a; ++i, ++pseq) {
@@ -432,7 +455,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         }
       }
     }
-  } else if (warp == 1 || (warp == kSwMma2Warp && p.n_iss > 1)) {
+  } else if ((warp == 1 || (warp == kSwMma2Warp && p.n_iss > 1)) && leader) {
     // ===================== MMA issuer(s) =====================
     // Issuer mi takes the rows with global sequence number g = mi (mod
     // p.n_iss); row g accumulates into accumulator g mod 2.  A row's K
@@ -463,7 +486,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     long long cyc_wait = 0, cyc_issue = 0, cyc_tempty = 0, cyc_row0 = 0;
 #endif
     for (int64_t t = t_begin; t < p.n_items; t += t_step) {
-      const SwItem it = sw_decode(p, t);
+      const SwItem it = sw_decode(p, t, kPair, rank);
       const int slot0 = wslot;  // ring slot of the item's atom 0
       int avail = 0;            // atoms of the item landed in TMEM
       int released = 0;         // atoms of the item released by this issuer
@@ -513,7 +536,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         cyc_issue = 0;
         cyc_row0 = clock64();
 #endif
-        ptx::mbar_wait(&tempty[acc], (acc_use & 1u) ^ 1u);
+        if constexpr (kPair) ptx::mbar_wait_cluster(&tempty[acc], (acc_use & 1u) ^ 1u);
+        else ptx::mbar_wait(&tempty[acc], (acc_use & 1u) ^ 1u);
 #ifdef MEC_TRACE
         cyc_tempty = clock64() - cyc_row0;
 #endif
@@ -544,7 +568,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           // inside the PTX loop; this warp's ring counters then skip past the
           // last atom the row's full groups need
           if (!no_mma)
-            ptx::mma_ts_row_elect<kTF32>(d_tmem, col, ring0 + ring_cols, ring_cols, b_lo0, b_tile16, p.idesc,
+            ptx::mma_ts_row_elect<kTF32, kPair>(d_tmem, col, ring0 + ring_cols, ring_cols, b_lo0, b_tile16, p.idesc,
                                          n_full, a, kcl + 2, bkl, ptx::smem_u32(afull), wslot, wphase, avail,
                                          ns);
           const int last = (a + (n_full << (kcl + 2)) - 1) >> bkl;
@@ -567,7 +591,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 #ifdef MEC_TRACE
         const long long cc0 = clock64();
 #endif
-        ptx::mma_commit_elect(&tfull[acc]);
+        if constexpr (kPair) ptx::mma_commit_pair_elect(&tfull[acc], 0x3);  // both CTAs' epilogues
+        else ptx::mma_commit_elect(&tfull[acc]);
 #ifdef MEC_TRACE
         const long long cyc_commit = clock64() - cc0;
 #endif
@@ -591,8 +616,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       skip_to(it.n_a);  // atoms no row of this issuer needs: never waited for
       q += static_cast<uint32_t>(it.nrows);
     }
-  } else if (warp == kSwMma2Warp) {
-    // (second issuer not used for this problem)
+  } else if (warp == 1 || warp == kSwMma2Warp) {
+    // (second issuer not used for this problem; pair mode: the peer CTA issues nothing)
   } else if (warp < kSwFirstEpiWarp) {
     // ===================== copiers: smem atom -> TMEM ring =====================
     const int quarter = warp & 3;
@@ -605,8 +630,9 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     // running ring positions (no divisions on this latency-critical path)
     int stage = 0, slot = 0;
     uint32_t sphase = 0;
+    const uint32_t afull0 = kPair ? ptx::mapa_shared(ptx::smem_u32(afull), 0) : 0u;  // the leader's ring barriers
     for (int64_t t = t_begin; t < p.n_items; t += t_step) {
-      const SwItem it = sw_decode(p, t);
+      const SwItem it = sw_decode(p, t, kPair, rank);
       const uint32_t jstart = cseq;  // the item's atom 0
       // last row whose window starts at or before atom jj (jj increasing):
       // fr, and fo = the first element of row fr + 1
@@ -670,7 +696,10 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&afull[slot]);
+        if (lane == 0) {
+          if constexpr (kPair) ptx::mbar_arrive_cluster(afull0 + static_cast<uint32_t>(slot) * 8u);
+          else ptx::mbar_arrive(&afull[slot]);
+        }
         if (warp == kSwFirstCopyWarp && lane == 0) SW_TRACE(cseq, 3);
         if (++stage == S) {
           stage = 0;
@@ -688,8 +717,9 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     const uint32_t stg = ptx::smem_u32(stg_gen);
     const uint32_t lane_base = static_cast<uint32_t>(32 * quarter) << 16;
     uint32_t q = 0;
+    const uint32_t tempty0 = kPair ? ptx::mapa_shared(ptx::smem_u32(tempty), 0) : 0u;
     for (int64_t t = t_begin; t < p.n_items; t += t_step) {
-      const SwItem it = sw_decode(p, t);
+      const SwItem it = sw_decode(p, t, kPair, rank);
       for (int r = 0; r < it.nrows; ++r) {
         const uint32_t qr = q + static_cast<uint32_t>(r);
         const uint32_t al = static_cast<uint32_t>(p.n_acc - 1);  // log2(n_acc), n_acc = 1 or 2
@@ -702,7 +732,8 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         if (lane == 0 && ((warp - kSwFirstEpiWarp) & 3) == 0)
           ptx::st_release_shared_u32(ptx::smem_u32(&rows_done[group]), (qr >> al) + 1u);
         sw_store_row<kTF32>(p, &tmO, it.h0 + r, it.mt, it.g, quarter, lane,
-                            tmem_base + lane_base + static_cast<uint32_t>(acc * p.bn), stg, stg_gen, &tempty[acc]);
+                            tmem_base + lane_base + static_cast<uint32_t>(acc * p.bn), stg, stg_gen, &tempty[acc],
+                            it.valid, kPair ? tempty0 + static_cast<uint32_t>(acc) * 8u : 0u);
       }
       q += static_cast<uint32_t>(it.nrows);
     }
@@ -712,14 +743,23 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) ptx::cluster_sync();  // no MMA, commit or remote arrive of the pair in flight
   if (threadIdx.x == 0) SW_TRACE(511u, 5);
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, 512);
+    if constexpr (kPair) ptx::tmem_dealloc_pair(tmem_base, 512);
+    else ptx::tmem_dealloc(tmem_base, 512);
   }
 }
 
 constexpr size_t kSwSmemBudget = 222 * 1024;
+
+// CTA-pair mode of the h-sweep (MEC_SWEEP_PAIR=1 / 0 forces it on / off)
+bool sweep_pair_mode(const Plan& pl) {
+  if (const char* e = getenv("MEC_SWEEP_PAIR")) return atoi(e) != 0;
+  (void)pl;
+  return false;
+}
 
 int ilog2(int x) {
   int l = 0;
@@ -732,7 +772,7 @@ int ilog2(int x) {
 // The sweep's resources for plan pl, or false when it does not apply (then
 // the one-window-per-tile kernel runs).
 bool sweep_config(const Plan& pl, bool batch_folded, int* n_vres_out, int* n_acc_out, int* ns_out,
-                  int* stages_out) {
+                  int* stages_out, bool pair) {
   if (getenv("MEC_SWEEP") && atoi(getenv("MEC_SWEEP")) == 0) return false;
   if (pl.n_tiles_n != 1 || pl.o_h < 2 || pl.shift >= pl.kdim) return false;  // no window overlap: nothing to share
   if (pl.l_cols > (1LL << 30) || pl.o_h * pl.shift > (1LL << 30)) return false;
@@ -765,7 +805,8 @@ bool sweep_config(const Plan& pl, bool batch_folded, int* n_vres_out, int* n_acc
   int row_bytes = 128;
   while (row_bytes > 32 && (pl.bn * pl.elt) % row_bytes != 0) row_bytes /= 2;
   const size_t epi = static_cast<size_t>(kSwEpiWarps) * 32 * row_bytes;
-  const size_t b_res = static_cast<size_t>(n_vres) * (pl.kdim_pad / pl.bk) * pl.bn * kTileKBytes;
+  // (pair mode: each CTA holds bn / 2 rows of the weights)
+  const size_t b_res = static_cast<size_t>(n_vres) * (pl.kdim_pad / pl.bk) * (pair ? pl.bn / 2 : pl.bn) * kTileKBytes;
   const size_t fixed = b_res + epi + 66 * 8 + 64;
   if (fixed + 2 * kSwAtomBytes > kSwSmemBudget) return false;
   const int stages = static_cast<int>(std::min<size_t>(8, (kSwSmemBudget - fixed) / kSwAtomBytes));
@@ -780,7 +821,10 @@ bool sweep_config(const Plan& pl, bool batch_folded, int* n_vres_out, int* n_acc
 cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st, int* launches) {
   int n_vres, n_acc, ns, stages;
   if (a.fused && !fused_eligible(pl)) return cudaErrorNotSupported;
-  if (!sweep_config(pl, a.batch_folded, &n_vres, &n_acc, &ns, &stages)) return cudaErrorNotSupported;
+  if (!sweep_config(pl, a.batch_folded, &n_vres, &n_acc, &ns, &stages, false)) return cudaErrorNotSupported;
+  // CTA pairs: the 2-SM TS MMA needs N a multiple of 32
+  const bool pair = sweep_pair_mode(pl) && pl.bn % 32 == 0;
+  if (pair && !sweep_config(pl, a.batch_folded, &n_vres, &n_acc, &ns, &stages, true)) return cudaErrorNotSupported;
   const bool tf32 = pl.dt == MEC_DTYPE_TF32;
   const int out_elt = pl.elt;
   CUtensorMap tmA, tmB, tmO;
@@ -820,7 +864,7 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   {  // B: Kt, n_var x kc_pad rows of kdim_pad (K-major)
     const uint64_t dims[2] = {static_cast<uint64_t>(pl.kdim_pad), static_cast<uint64_t>(pl.n_var * pl.kc_pad)};
     const uint64_t strides[1] = {static_cast<uint64_t>(pl.kdim_pad) * pl.elt};
-    const uint32_t box[2] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(pl.bn)};
+    const uint32_t box[2] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(pair ? pl.bn / 2 : pl.bn)};
     cudaError_t e = encode_tiled(&tmB, tf32, 2, a.Kt, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
@@ -859,7 +903,7 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   p.n_acc = n_acc;
   p.a_col0 = static_cast<uint32_t>(((n_acc * pl.bn + 31) / 32) * 32);
   p.guard_col = p.a_col0 + static_cast<uint32_t>(32 * ns);
-  p.idesc = ptx::instr_desc(tf32, kBM, pl.bn);
+  p.idesc = ptx::instr_desc(tf32, pair ? 2 * kBM : kBM, pl.bn);
   p.col_shift = pl.elt == 2 ? 1 : 0;
   p.out_hnwc = a.out_hnwc;
   p.dbg = getenv("MEC_SWEEP_DBG") ? atoi(getenv("MEC_SWEEP_DBG")) : 0;
@@ -914,14 +958,17 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   // h-chunk size H: minimise (waves) x (bytes one item moves: its stream of
   // atoms, its O rows and a fixed pipeline fill), ties to fewer items
   const int64_t tiles = n_mt * groups;
-  const int sms = num_sms();
+  p.n_tiles = tiles;
+  // pair mode: items are (h chunk, pair of CTA tiles), one per pair of SMs
+  const int64_t work_tiles = pair ? (tiles + 1) / 2 : tiles;
+  const int sms = pair ? std::max(1, num_sms() / 2) : num_sms();
   const double o_row_bytes = static_cast<double>(kBM) * pl.bn * out_elt;
   double best = 1e300;
   int64_t best_H = pl.o_h;
   int64_t best_n = 1;
   for (int64_t n_hc = 1; n_hc <= pl.o_h; ++n_hc) {
     const int64_t H = (pl.o_h + n_hc - 1) / n_hc;  // the largest chunk
-    const int64_t items = n_hc * tiles;
+    const int64_t items = n_hc * work_tiles;
     const int64_t waves = (items + sms - 1) / sms;
     const double atoms = static_cast<double>((H - 1) * pl.shift + pl.kdim + pl.avec) / pl.bk + 1.0;
     const double cost = static_cast<double>(waves) * (atoms * kSwAtomBytes + H * o_row_bytes + 4.0 * kSwAtomBytes);
@@ -937,26 +984,48 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   }
   p.H = static_cast<int>(best_H);
   p.n_hc = best_n;
-  p.n_items = p.n_hc * tiles;
+  p.n_items = p.n_hc * work_tiles;
 
-  const size_t b_res = static_cast<size_t>(n_vres) * p.nb_atoms * pl.bn * kTileKBytes;
+  const size_t b_res = static_cast<size_t>(n_vres) * p.nb_atoms * (pair ? pl.bn / 2 : pl.bn) * kTileKBytes;
   const size_t smem = kSmemAlign + static_cast<size_t>(stages) * kSwAtomBytes + b_res +
                       static_cast<size_t>(kSwEpiWarps) * p.stage_out_bytes + 66 * 8 + 16;
   if (smem > kSwSmemBudget + kSmemAlign + 2048) return cudaErrorInvalidConfiguration;
-  const int64_t grid = std::min<int64_t>(p.n_items, sms);
-  auto kern = tf32 ? sweep_gemm_kernel<true> : sweep_gemm_kernel<false>;
+  auto kern = tf32 ? (pair ? sweep_gemm_kernel<true, true> : sweep_gemm_kernel<true, false>)
+                   : (pair ? sweep_gemm_kernel<false, true> : sweep_gemm_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kSwThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = getenv("MEC_NO_PDL") ? 0 : 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 2;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = pair ? attr + 1 : attr;
+  cfg.numAttrs = 0;
+  int64_t grid = std::min<int64_t>(p.n_items, sms);
+  if (pair) {
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * sms));
+    int max_clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
+      cudaGetLastError();
+      max_clusters = sms;
+    }
+    grid = 2 * std::min<int64_t>(p.n_items, max_clusters);
+    // the PDL attribute next to the cluster one
+    if (!getenv("MEC_NO_PDL")) {
+      cfg.attrs = attr;
+      cfg.numAttrs = 2;
+    }
+  } else if (!getenv("MEC_NO_PDL")) {
+    cfg.numAttrs = 1;
+  }
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
   e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmO, p);
   if (e != cudaSuccess) return e;
   if (launches) ++*launches;
