@@ -444,6 +444,7 @@ size_t workspace_need(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, co
 // Prepare the weight operand (Alg.2 l.7: K as a (k_h k_w i_c) x k_c matrix,
 // K-major, zero padded, shifted copies) into Kt with a prep-only launch.
 cudaError_t prepare_weights(const Resolved& r, const void* K, void* Kt, cudaStream_t st, int* launches) {
+  if (r.gemm == 3 && wide_reads_k(r.pc)) return cudaSuccess;  // reads K directly
   return launch_lower(r.pc, nullptr, nullptr, r.pc.pitch, K, Kt, st, launches, r.gather_kt);
 }
 
@@ -462,8 +463,10 @@ cudaError_t run_conv(const Resolved& r, const void* I, const void* K, void* O, v
   // (the fused path skips L: only the weight operand is prepared)
   unsigned char* wide_scratch = static_cast<unsigned char*>(L) + pc.off_wide;
   const size_t wide_bytes = r.ws_need - pc.off_wide - 1024;
-  cudaError_t e = launch_lower(pc, I, path == MEC_PATH_FUSED ? nullptr : L, pc.pitch, kt_ready ? nullptr : K,
-                               kt_ready ? nullptr : Kt, st, launches, r.gather_kt,
+  // the CTA-pair kernel reads K directly (MN-major B): no weight prep then
+  const bool prep = !kt_ready && !(r.gemm == 3 && wide_reads_k(pc));
+  cudaError_t e = launch_lower(pc, I, path == MEC_PATH_FUSED ? nullptr : L, pc.pitch, prep ? K : nullptr,
+                               prep ? Kt : nullptr, st, launches, r.gather_kt,
                                r.gemm == 3 ? reinterpret_cast<uint32_t*>(wide_scratch) : nullptr,
                                r.gemm == 3 ? wide_zero_words(pc) : 0u);
   if (e != cudaSuccess) return e;
@@ -472,6 +475,7 @@ cudaError_t run_conv(const Resolved& r, const void* I, const void* K, void* O, v
   ga.L = path == MEC_PATH_FUSED ? I : L;
   ga.fused = path == MEC_PATH_FUSED;
   ga.Kt = Kt;
+  ga.K = K;
   ga.O = O;
   ga.rows_per_tile = opt->rows_per_tile;
   if (path == MEC_PATH_FUSED) {  // batch-folded tiles of windows of I

@@ -100,6 +100,8 @@ cudaError_t launch_lower(const Plan& p, const void* I, void* L, int64_t pitch, c
 struct GemmArgs {
   const void* L;
   const void* Kt;
+  const void* K;      // the caller's K (k_h, k_w, i_c, k_c): K_mat row-major, read directly as an
+                      // MN-major B operand by kernels that need no prepared Kt (wide_gemm.cu)
   void* O;
   bool batch_folded;
   bool out_hnwc;
@@ -135,6 +137,8 @@ cudaError_t launch_sweep_gemm(const Plan& p, const GemmArgs& a, cudaStream_t st,
 // reduction.  Solution A with flat rows (o_w < 32) only.
 bool wide_eligible(const Plan& p, bool batch_folded, bool fused);
 bool wide_preferred(const Plan& p);  // tensor-bound (AI >= 0.8 ridge) or MEC_WIDE
+// the CTA-pair kernel reads the weights straight from K (MN-major B, no Kt)
+bool wide_reads_k(const Plan& p);
 // scratch (counters + fp32 partials) for split `split` (0 = automatic)
 size_t wide_scratch_bytes(const Plan& p, int split);
 // words of the scratch that must be zero when the kernel starts

@@ -806,6 +806,34 @@ __device__ __forceinline__ void mma_ss_atom_pair_elect(uint32_t tmem_d, uint64_t
   }
 #undef MEC_PAIR_ATOM
 }
+// As mma_ss_atom_pair_elect with B advanced by b_step (16-byte units) per
+// 32-byte K step instead of 2 (an MN-major B: one K step = 16 bf16 / 8 tf32
+// K rows = b_step x 16 bytes further on).
+template <bool kTF32>
+__device__ __forceinline__ void mma_ss_atom_pair_bstep_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                             uint32_t b_step, uint32_t idesc, uint32_t accumulate) {
+#define MEC_PAIR_ATOM_BS(KIND)                                                                          \
+  asm volatile(                                                                                         \
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3, s;\n\t"                                 \
+      "setp.ne.b32 p, %5, 0;\n\t"                                                                       \
+      "cvt.u64.u32 s, %3;\n\t"                                                                           \
+      "add.u64 a1, %1, 2;\n\tadd.u64 a2, %1, 4;\n\tadd.u64 a3, %1, 6;\n\t"                                 \
+      "add.u64 b1, %2, s;\n\tadd.u64 b2, b1, s;\n\tadd.u64 b3, b2, s;\n\t"                               \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                                 \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], %1, %2, %4, p;\n\t"                              \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], a1, b1, %4, 1;\n\t"                              \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], a2, b2, %4, 1;\n\t"                              \
+      "@e tcgen05.mma.cta_group::2.kind::" KIND " [%0], a3, b3, %4, 1;\n\t}" ::"r"(tmem_d),              \
+      "l"(adesc), "l"(bdesc), "r"(b_step), "r"(idesc), "r"(accumulate)                                  \
+      : "memory")
+  if constexpr (kTF32) {
+    MEC_PAIR_ATOM_BS("tf32");
+  } else {
+    MEC_PAIR_ATOM_BS("f16");
+  }
+#undef MEC_PAIR_ATOM_BS
+}
+
 // Whole-warp call (pair leader): commit the pair's prior MMAs to the mbarrier
 // at the same shared offset in every CTA of `cta_mask` (multicast arrive).
 __device__ __forceinline__ void mma_commit_pair_elect(uint64_t* bar, uint16_t cta_mask) {
@@ -841,12 +869,27 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// MN-major operand (N contiguous) in the 128-byte-swizzle canonical layout a
+// TMA load of {128 bytes of N, K rows} boxes with CU_TENSOR_MAP_SWIZZLE_128B
+// produces: 8 K-rows of 128 B form a 1 KB swizzle atom (SBO = 1024 B between
+// consecutive groups of 8 K rows), and consecutive 128-byte N chunks are
+// lbo_bytes apart (LBO: one box).
+__device__ __forceinline__ uint64_t smem_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
 // Instruction descriptor (kind::f16 / kind::tf32): D fp32 [4,6)=1,
 // A/B format [7,10)/[10,13) (1 = BF16, 2 = TF32), both K-major (bits 15,16 = 0),
 // N>>3 at [17,23), M>>4 at [24,29).
-__host__ __device__ constexpr uint32_t instr_desc(bool tf32, uint32_t M, uint32_t N) {
-  return (1u << 4) | ((tf32 ? 2u : 1u) << 7) | ((tf32 ? 2u : 1u) << 10) | ((N >> 3) << 17) |
-         ((M >> 4) << 24);
+__host__ __device__ constexpr uint32_t instr_desc(bool tf32, uint32_t M, uint32_t N, bool b_mn = false) {
+  return (1u << 4) | ((tf32 ? 2u : 1u) << 7) | ((tf32 ? 2u : 1u) << 10) | ((b_mn ? 1u : 0u) << 16) |
+         ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
 }  // namespace ptx

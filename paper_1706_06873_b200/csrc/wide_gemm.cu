@@ -80,6 +80,11 @@ struct WideParams {
   int stages;
   uint32_t stage_bytes, a_bytes, b_half_bytes;
   uint32_t idesc;
+  // weights read straight from K (MN-major B): each CTA's N/2
+  // columns come as b_chunks TMA boxes of chunk_n columns x bk K rows
+  bool b_mn;
+  int b_chunks, chunk_n;
+  uint32_t b_chunk_bytes, b_kstep16;
 };
 
 struct Unit {
@@ -168,14 +173,25 @@ __global__ void __launch_bounds__(kWideThreads, 1)
         const int v = static_cast<int>((xw % p.avec) / p.delta_step);
         const int32_t y0 = static_cast<int32_t>(c.mt * kPairM + rank * kBM);
         const int32_t brow = static_cast<int32_t>(v * p.kc_pad + c.ng * p.n_sub * p.bn + rank * (p.bn / 2));
+        // MN-major: B rows = K_mat rows of the box's columns, shifted by the
+        // window's delta (negative rows / rows past kdim: TMA zero fill)
+        const int32_t bcol = static_cast<int32_t>(c.ng * p.n_sub * p.bn + rank * (p.bn / 2));
+        const int32_t bdelta = static_cast<int32_t>(v * p.delta_step);
         for (int a = c.a0; a < c.a1; ++a) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&full[stage], tx);
           unsigned char* dA = smem + static_cast<size_t>(stage) * p.stage_bytes;
           const uint32_t fb = full0 + static_cast<uint32_t>(stage) * 8u;
           ptx::tma_load_2d_pair(dA, &tmA, fb, x0 + a * p.bk, y0, hintA);
-          for (int sb = 0; sb < p.n_sub; ++sb)
-            ptx::tma_load_2d_pair(dA + p.a_bytes + sb * p.b_half_bytes, &tmB, fb, a * p.bk, brow + sb * p.bn, hintB);
+          if (p.b_mn) {
+            for (int sb = 0; sb < p.n_sub; ++sb)
+              for (int cb = 0; cb < p.b_chunks; ++cb)
+                ptx::tma_load_2d_pair(dA + p.a_bytes + sb * p.b_half_bytes + cb * p.b_chunk_bytes, &tmB, fb,
+                                      bcol + sb * p.bn + cb * p.chunk_n, a * p.bk - bdelta, hintB);
+          } else {
+            for (int sb = 0; sb < p.n_sub; ++sb)
+              ptx::tma_load_2d_pair(dA + p.a_bytes + sb * p.b_half_bytes, &tmB, fb, a * p.bk, brow + sb * p.bn, hintB);
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -187,6 +203,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
     // ===================== MMA issuer (pair leader) =====================
     if (leader) {
       const uint64_t desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smem));
+      const uint64_t bmn0 = ptx::smem_desc_sw128_mn(ptx::smem_u32(smem) + p.a_bytes, p.b_chunk_bytes);
       const uint32_t a_to_b = p.a_bytes >> 4, b_to_b = p.b_half_bytes >> 4;
       int stage = 0;
       uint32_t phase = 0;
@@ -202,11 +219,20 @@ __global__ void __launch_bounds__(kWideThreads, 1)
         for (int a = c.a0; a < c.a1; ++a) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint64_t ad = desc0 + (static_cast<uint32_t>(stage) * p.stage_bytes >> 4);
-          ptx::mma_ss_atom_pair_elect<kTF32>(d, ad, ad + a_to_b, p.idesc, a != c.a0 ? 1u : 0u);
-          if (p.n_sub == 2)
-            ptx::mma_ss_atom_pair_elect<kTF32>(d + static_cast<uint32_t>(p.bn), ad, ad + a_to_b + b_to_b, p.idesc,
-                                               a != c.a0 ? 1u : 0u);
+          const uint32_t soff = static_cast<uint32_t>(stage) * p.stage_bytes >> 4;
+          const uint64_t ad = desc0 + soff;
+          if (p.b_mn) {
+            const uint64_t bd = bmn0 + soff;
+            ptx::mma_ss_atom_pair_bstep_elect<kTF32>(d, ad, bd, p.b_kstep16, p.idesc, a != c.a0 ? 1u : 0u);
+            if (p.n_sub == 2)
+              ptx::mma_ss_atom_pair_bstep_elect<kTF32>(d + static_cast<uint32_t>(p.bn), ad, bd + b_to_b,
+                                                       p.b_kstep16, p.idesc, a != c.a0 ? 1u : 0u);
+          } else {
+            ptx::mma_ss_atom_pair_elect<kTF32>(d, ad, ad + a_to_b, p.idesc, a != c.a0 ? 1u : 0u);
+            if (p.n_sub == 2)
+              ptx::mma_ss_atom_pair_elect<kTF32>(d + static_cast<uint32_t>(p.bn), ad, ad + a_to_b + b_to_b, p.idesc,
+                                                 a != c.a0 ? 1u : 0u);
+          }
           ptx::mma_commit_pair_elect(&empty[stage], 0x3);
           __syncwarp();
           if (++stage == S) {
@@ -457,6 +483,23 @@ bool wide_eligible(const Plan& pl, bool batch_folded, bool fused) {
   return true;
 }
 
+// The weights straight from K as an MN-major B operand (no prepared Kt, so the
+// lowering launch does no weight prep): each CTA's N/2 columns must be whole
+// 128-byte boxes.  Opt-in (MEC_WIDE_KMN=1): measured on B200 it is correct
+// but slower -- the GEMM with MN-major B runs 8-15% longer (cv5 b1024 384 vs
+// 332 us, cv12 b1024 103 vs 89 us: twice the B boxes per atom, N-contiguous
+// smem reads) while the saved weight prep was only ~2.5 us of the lowering
+// launch (its prep CTAs overlap the lowering CTAs).  bf16 only: tf32
+// MN-major B in the plain 128-byte swizzle gave wrong products (CUTLASS pairs
+// 32-bit MN-major operands with the 128B_BASE32B swizzle).
+bool wide_reads_k(const Plan& pl) {
+  const char* e = getenv("MEC_WIDE_KMN");
+  if (e == nullptr || atoi(e) == 0) return false;
+  if (pl.elt != 2) return false;
+  const int chunk_n = kTileKBytes / pl.elt;
+  return (pl.bn / 2) % chunk_n == 0 && (pl.s.k_c * pl.elt) % 16 == 0;
+}
+
 // Tensor-bound: the two-kernel GEMM's arithmetic intensity (SURVEY 8(d):
 // (#L + #K + #O) elt bytes) above ~0.8 of the ridge (251 F/B bf16, 126 tf32).
 bool wide_preferred(const Plan& pl) {
@@ -516,7 +559,12 @@ cudaError_t launch_wide_gemm(const Plan& pl, const GemmArgs& a, void* scratch, s
   if (scratch == nullptr || scratch_bytes < g.cnt_bytes + g.part_bytes) return cudaErrorNotSupported;
   p.cnt = static_cast<uint32_t*>(scratch);
   p.part = reinterpret_cast<float*>(static_cast<unsigned char*>(scratch) + g.cnt_bytes);
-  p.idesc = ptx::instr_desc(tf32, kPairM, pl.bn);
+  p.b_mn = wide_reads_k(pl) && a.K != nullptr;
+  p.chunk_n = kTileKBytes / pl.elt;
+  p.b_chunks = p.b_mn ? (pl.bn / 2) / p.chunk_n : 0;
+  p.b_chunk_bytes = static_cast<uint32_t>(kTileKBytes * pl.bk);                 // 128 B x bk K rows
+  p.b_kstep16 = static_cast<uint32_t>((32 / pl.elt) * kTileKBytes) >> 4;      // one 32-byte K step of K rows
+  p.idesc = ptx::instr_desc(tf32, kPairM, pl.bn, p.b_mn);
   auto kern = tf32 ? wide_gemm_kernel<true> : wide_gemm_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -549,7 +597,14 @@ cudaError_t launch_wide_gemm(const Plan& pl, const GemmArgs& a, void* scratch, s
     e = encode_tiled(&tmA, tf32, 2, a.L, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
-  {
+  if (p.b_mn) {
+    // K_mat = K viewed as (k_h k_w i_c) x k_c row-major (Alg.2 l.7: no copy)
+    const uint64_t dims[2] = {static_cast<uint64_t>(pl.s.k_c), static_cast<uint64_t>(pl.kdim_src)};
+    const uint64_t strides[1] = {static_cast<uint64_t>(pl.s.k_c) * pl.elt};
+    const uint32_t box[2] = {static_cast<uint32_t>(p.chunk_n), static_cast<uint32_t>(pl.bk)};
+    e = encode_tiled(&tmB, tf32, 2, a.K, dims, strides, box);
+    if (e != cudaSuccess) return e;
+  } else {
     const uint64_t dims[2] = {static_cast<uint64_t>(pl.kdim_pad), static_cast<uint64_t>(pl.n_var * pl.kc_pad)};
     const uint64_t strides[1] = {static_cast<uint64_t>(pl.kdim_pad) * pl.elt};
     const uint32_t box[2] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(pl.bn / 2)};

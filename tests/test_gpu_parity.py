@@ -909,3 +909,23 @@ def test_C2_pair_sweep_full_batch_sampled(cuda_ok, dtype):
     for n in (0, 37, 63):
         I = synth.input_images(cfg, n, 1, kind, seed)
         check_O(O[n:n + 1], oracle.direct_conv(I, K, 1, 1, n_threads=8), dtype, 576)
+
+
+@pytest.mark.parametrize("name,batch", [("cv12", 3), ("cv5", 2), ("cv1", 2)])
+def test_wide_pair_kernel_weights_from_K(cuda_ok, name, batch):
+    """Opt-in variant (MEC_WIDE_KMN=1): the CTA-pair kernel reads the weights
+    straight from K as an MN-major B operand (no prepared Kt; negative rows of
+    a delta-shifted window are TMA zero fill) -- within tolerance of the oracle."""
+    i_h, i_w, i_c, k_h, k_w, k_c, s = synth.TABLE2[name]
+    shape = (batch, i_h, i_w, i_c, k_h, k_w, k_c)
+    I, K = make_inputs(shape, "bf16", seed=6300 + batch)
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    os.environ["MEC_WIDE_KMN"] = "1"
+    try:
+        O, g = mec.conv_forward(to_dev(I, "bf16"), to_dev(K, "bf16"), s, s, path=MEC_PATH_SOLUTION_A,
+                                gemm_kernel=3, return_gemm=True)
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("MEC_WIDE_KMN", None)
+    assert g == 3
+    check_O(O, ref, "bf16", k_h * k_w * i_c)
