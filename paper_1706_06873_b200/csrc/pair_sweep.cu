@@ -73,7 +73,9 @@ struct PsParams {
   // the A atom and, for each open row, that row's weight atom (b_open slots)
   bool b_stream;
   int b_open;
-  uint32_t stage_bytes;  // A (16 KB) [+ b_open x b_half_bytes]
+  int aps;               // stream atoms per pipeline stage (one full/empty handshake and commit each)
+  uint32_t slot_bytes;   // one atom of a stage: A (16 KB) [+ b_open x b_half_bytes]
+  uint32_t stage_bytes;  // aps x slot_bytes
   uint32_t idesc;
   bool a_evict_first;    // (experiments: MEC_PS_EVICT_FIRST=1) L2 evict-first hint on the L stream
 };
@@ -101,7 +103,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <bool kTF32>
+template <bool kTF32, int kAps>
 __global__ void __launch_bounds__(kPsThreads, 1)
     pair_sweep_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const PsParams p) {
@@ -173,19 +175,29 @@ __global__ void __launch_bounds__(kPsThreads, 1)
         const int n_stream = (rows - 1) * p.sa + p.na;
         const CTile t = ctile(p, 2 * pt + rank);
         const int32_t x0 = static_cast<int32_t>(h0 * p.shift);
+        int k = 0;  // atom slot within the current stage
         for (int j = 0; j < n_stream; ++j) {
           // streamed weights: the open rows r_lo..r_hi of this atom each need weight atom j - r sa
           const int r_hi = min(rows - 1, j / p.sa);
           const int r_lo = j >= p.na ? (j - p.na) / p.sa + 1 : 0;
-          const uint32_t nb = p.b_stream ? static_cast<uint32_t>(r_hi - r_lo + 1) : 0u;
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2u * (p.a_bytes + nb * p.b_half_bytes));
-          unsigned char* dA = smem + static_cast<size_t>(stage) * p.stage_bytes;
           const uint32_t fb = full0 + static_cast<uint32_t>(stage) * 8u;
-          for (uint32_t k = 0; k < nb; ++k)
-            ptx::tma_load_2d_pair(dA + kBM * kTileKBytes + k * p.b_half_bytes, &tmB, fb,
-                                  (j - (r_lo + static_cast<int>(k)) * p.sa) * p.bk,
-                                  static_cast<int32_t>(rank * (p.bn / 2)), hintB);
+          if (k == 0) {  // a new stage: its bytes (up to aps atoms), one expect_tx
+            uint32_t bytes = 0;
+            const int na_s = min(kAps, n_stream - j);
+            for (int kk = 0; kk < na_s; ++kk) {
+              const int jj = j + kk;
+              const int hi = min(rows - 1, jj / p.sa);
+              const int lo = jj >= p.na ? (jj - p.na) / p.sa + 1 : 0;
+              bytes += p.a_bytes + (p.b_stream ? static_cast<uint32_t>(hi - lo + 1) * p.b_half_bytes : 0u);
+            }
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2u * bytes);
+          }
+          unsigned char* dA = smem + static_cast<size_t>(stage) * p.stage_bytes + static_cast<size_t>(k) * p.slot_bytes;
+          if (p.b_stream)
+            for (int r = r_lo; r <= r_hi; ++r)
+              ptx::tma_load_2d_pair(dA + kBM * kTileKBytes + (r - r_lo) * p.b_half_bytes, &tmB, fb,
+                                    (j - r * p.sa) * p.bk, static_cast<int32_t>(rank * (p.bn / 2)), hintB);
           const int32_t x = x0 + j * p.bk;
           if (p.ipt == 1) {
             ptx::tma_load_3d_pair(dA, &tmA, fb, x, static_cast<int32_t>(t.w0), static_cast<int32_t>(t.n0), hintA);
@@ -194,9 +206,12 @@ __global__ void __launch_bounds__(kPsThreads, 1)
               ptx::tma_load_3d_pair(dA + s * p.slot * kTileKBytes, &tmA, fb, x, 0, static_cast<int32_t>(t.n0 + s),
                                     hintA);
           }
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
+          if (++k == kAps || j == n_stream - 1) {
+            k = 0;
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -207,7 +222,7 @@ __global__ void __launch_bounds__(kPsThreads, 1)
       const uint64_t adesc0 = ptx::smem_desc_sw128(ptx::smem_u32(smem));
       const uint64_t bdesc0 = ptx::smem_desc_sw128(ptx::smem_u32(smemB));
       const uint32_t a_stage16 = p.stage_bytes >> 4, b16 = p.b_half_bytes >> 4;
-      const uint32_t a_to_b16 = (kBM * kTileKBytes) >> 4;
+      const uint32_t a_to_b16 = (kBM * kTileKBytes) >> 4, slot16 = p.slot_bytes >> 4;
       if (!p.b_stream) ptx::mbar_wait(bfull, 0);
       int stage = 0;
       uint32_t phase = 0;
@@ -216,6 +231,7 @@ __global__ void __launch_bounds__(kPsThreads, 1)
         const int64_t hc = it % p.n_hc;
         const int rows = static_cast<int>(p.o_h - hc * p.H < p.H ? p.o_h - hc * p.H : p.H);
         const int n_stream = (rows - 1) * p.sa + p.na;
+        int k = 0;  // atom slot within the current stage
         for (int j = 0; j < n_stream; ++j) {
           // open rows: r sa <= j < r sa + na
           const int r_hi = min(rows - 1, j / p.sa);
@@ -223,27 +239,31 @@ __global__ void __launch_bounds__(kPsThreads, 1)
           // a row starting here needs its accumulator drained (row r_hi starts iff j == r_hi sa)
           if (j == r_hi * p.sa) {
             const uint32_t q = row_seq + static_cast<uint32_t>(r_hi);
-            ptx::mbar_wait_cluster(&tempty[q % p.n_acc], ((q / p.n_acc) & 1u) ^ 1u);
+            ptx::mbar_wait(&tempty[q % p.n_acc], ((q / p.n_acc) & 1u) ^ 1u);
           }
-          ptx::mbar_wait(&full[stage], phase);
+          if (k == 0) ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint64_t ad = adesc0 + static_cast<uint32_t>(stage) * a_stage16;
+          const uint64_t ad = adesc0 + static_cast<uint32_t>(stage) * a_stage16 + static_cast<uint32_t>(k) * slot16;
           for (int r = r_lo; r <= r_hi; ++r) {
             const int a = j - r * p.sa;  // the row's window atom
             const uint32_t q = row_seq + static_cast<uint32_t>(r);
-            // weights: resident atom a, or the stage's slot r - r_lo
+            // weights: resident atom a, or the atom slot's weight part r - r_lo
             const uint64_t bd = p.b_stream ? ad + a_to_b16 + static_cast<uint32_t>(r - r_lo) * b16
                                            : bdesc0 + static_cast<uint32_t>(a) * b16;
             ptx::mma_ss_atom_pair_elect<kTF32>(tmem_base + (q % p.n_acc) * static_cast<uint32_t>(p.bn), ad, bd,
                                                p.idesc, a != 0 ? 1u : 0u);
           }
-          ptx::mma_commit_pair_elect(&empty[stage], 0x3);
+          const bool stage_end = ++k == kAps || j == n_stream - 1;
+          if (stage_end) ptx::mma_commit_pair_elect(&empty[stage], 0x3);  // one release per stage of aps atoms
           if (j - r_lo * p.sa == p.na - 1)  // the oldest open row is complete
             ptx::mma_commit_pair_elect(&tfull[(row_seq + static_cast<uint32_t>(r_lo)) % p.n_acc], 0x3);
           __syncwarp();
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
+          if (stage_end) {
+            k = 0;
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
         row_seq += static_cast<uint32_t>(rows);
@@ -355,7 +375,8 @@ struct PsGeo {
   int ipt, slot;
   int64_t mt_per_img, n_ctile, n_pt;
   int sa, na, n_acc, stages;
-  uint32_t a_bytes, b_half_bytes, stage_bytes;
+  uint32_t a_bytes, b_half_bytes, stage_bytes, slot_bytes;
+  int aps;
   bool b_stream;
   int b_open;
   size_t smem;
@@ -390,8 +411,15 @@ bool ps_geo(const Plan& pl, bool batch_folded, PsGeo* g) {
   g->b_open = open;
   if (g->b_stream) b_res = 0;
   g->a_bytes = static_cast<uint32_t>(g->ipt == 1 ? kBM * kTileKBytes : g->ipt * g->slot * kTileKBytes);
-  g->stage_bytes = static_cast<uint32_t>(kBM * kTileKBytes + (g->b_stream ? open * g->b_half_bytes : 0));
+  g->slot_bytes = static_cast<uint32_t>(kBM * kTileKBytes + (g->b_stream ? open * g->b_half_bytes : 0));
   const size_t fixed = kSmemAlign + b_res + 8 * kPsStageOut + 32 * 8 + 64;
+  // atoms per stage: 1 (one full/empty handshake and commit per atom).  2-3
+  // atoms per stage (MEC_PS_APS, experiments) measured slower on B200: C2 tf32
+  // 701 -> 767 / 795 us, cv4 b128 936 -> 1258 / 1233 us (fewer stages in
+  // flight; the per-atom commits are not the bottleneck here)
+  g->aps = 1;
+  if (const char* e = getenv("MEC_PS_APS")) g->aps = std::max(1, std::min(3, atoi(e)));
+  g->stage_bytes = static_cast<uint32_t>(g->aps) * g->slot_bytes;
   const size_t stage = g->stage_bytes;
   if (fixed + 2 * stage > kPsSmemBudget) return false;
   g->stages = static_cast<int>(std::min<size_t>(12, (kPsSmemBudget - fixed) / stage));
@@ -435,9 +463,16 @@ cudaError_t launch_pair_sweep(const Plan& pl, const GemmArgs& a, cudaStream_t st
   p.b_stream = g.b_stream;
   p.b_open = g.b_open;
   p.stage_bytes = g.stage_bytes;
+  p.slot_bytes = g.slot_bytes;
+  p.aps = g.aps;
   p.a_evict_first = getenv("MEC_PS_EVICT_FIRST") && atoi(getenv("MEC_PS_EVICT_FIRST")) != 0;
   p.idesc = ptx::instr_desc(tf32, 2 * kBM, pl.bn);
-  auto kern = tf32 ? pair_sweep_kernel<true> : pair_sweep_kernel<false>;
+  // atoms per stage as a template parameter: the 1-atom instance keeps the
+  // per-atom loop free of stage bookkeeping (a runtime aps cost ~30% there)
+  auto kern = tf32 ? (g.aps == 1 ? pair_sweep_kernel<true, 1> : g.aps == 2 ? pair_sweep_kernel<true, 2>
+                                                                           : pair_sweep_kernel<true, 3>)
+                   : (g.aps == 1 ? pair_sweep_kernel<false, 1> : g.aps == 2 ? pair_sweep_kernel<false, 2>
+                                                                            : pair_sweep_kernel<false, 3>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};

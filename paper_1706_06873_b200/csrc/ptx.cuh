@@ -65,8 +65,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// As mbar_wait, with cluster-scope acquire: for barriers that a peer CTA of
-// the cluster arrives on (remote mbarrier.arrive.release.cluster).
+// As mbar_wait, with cluster-scope acquire.  Not used on hot paths: a
+// cluster-scope acquire makes ptxas emit an L1 invalidation (CCTL.IVALL) per
+// probe -- the pair kernels' accumulator waits with it ran 20-60% slower (pair
+// sweep cv4 b128 915 -> 1477 us).  The tcgen05 fences around the barrier
+// order the TMEM accesses, as CUTLASS's cluster barriers do with plain waits.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   asm volatile(

@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
         // n_sub = 1: accumulators alternate (i & 1); n_sub = 2: one set of 2 x bn columns
         const int acc = p.n_sub == 1 ? static_cast<int>(i & 1) : 0;
         const int64_t use = p.n_sub == 1 ? (i >> 1) : i;  // uses of this accumulator so far
-        ptx::mbar_wait_cluster(&tempty[acc], (static_cast<uint32_t>(use) & 1u) ^ 1u);
+        ptx::mbar_wait(&tempty[acc], (static_cast<uint32_t>(use) & 1u) ^ 1u);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + static_cast<uint32_t>(acc * p.bn);
         for (int a = c.a0; a < c.a1; ++a) {
