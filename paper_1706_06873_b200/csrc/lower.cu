@@ -132,6 +132,10 @@ struct LowerParams {
   // counters), cleared by the last CTA of this launch
   uint32_t* zero_words;
   uint32_t n_zero;
+  // row-copy path (lower_rows_kernel): 16-byte vectors per strip / per L row
+  uint32_t vps, vpr, vps_magic;
+  int64_t n_rows;          // i_n o_w rows of L
+  int rows_per_cta;
 };
 
 template <typename T>
@@ -736,6 +740,67 @@ __global__ void __launch_bounds__(512) lower_kernel(const LowerParams p) {
 
 // Direct fallback for input rows too wide to stage in shared memory: every
 // thread copies one L element from global.  (Not used by any BASELINE config.)
+// Row-copy lowering for strips that are whole 16-byte vectors (i_c elt a
+// multiple of 16: C2, C3, cv4-cv12).  Alg.2 l.4-6: L[n,w,h,:,:] = I[n,h,s_w
+// w : s_w w + k_w,:] -- every strip is one contiguous run of k_w i_c elements
+// of I, so each 16-byte vector of L is one 16-byte vector of I: a CTA copies
+// whole rows (n, w) of L (i_h strips) straight from global to global, a warp
+// reading and writing 512 contiguous bytes per instruction.  No shared
+// memory, no barrier: many independent loads in flight per SM (the staged
+// band kernel waited for its band before writing).  The k_w / s_w-fold
+// re-reads of I (neighbouring w share pixels) are served by L2.  Zero
+// padding (NEXT-4): vectors of pixels outside the unpadded image are zeros.
+// Blocks past the L rows prepare the weight operand (as lower_kernel).
+template <typename T>
+__global__ void __launch_bounds__(256) lower_rows_kernel(const LowerParams p) {
+  constexpr uint32_t VEC = 16 / sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem[];
+  ptx::griddep_launch_dependents();
+  if (p.zero_words != nullptr && blockIdx.x == gridDim.x - 1)
+    for (uint32_t i = threadIdx.x; i < p.n_zero; i += blockDim.x) p.zero_words[i] = 0u;
+  const int64_t row_blocks = (p.n_rows + p.rows_per_cta - 1) / p.rows_per_cta;
+  if (static_cast<int64_t>(blockIdx.x) >= row_blocks) {
+    const int64_t n_prep = gridDim.x - row_blocks;
+    const int64_t n_tiles = prep_units<T>(p);
+    for (int64_t t = blockIdx.x - row_blocks; t < n_tiles; t += n_prep) prep_unit<T>(p, t, smem);
+    return;
+  }
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * p.rows_per_cta;
+  const int64_t r1 = min(p.n_rows, r0 + p.rows_per_cta);
+  const uint4* I4 = reinterpret_cast<const uint4*>(p.I);
+  for (int64_t row = r0; row < r1; ++row) {
+    const int64_t n = row / p.o_w, w = row - n * p.o_w;
+    uint4* dst = reinterpret_cast<uint4*>(p.L + static_cast<size_t>(row * p.pitch) * sizeof(T));
+    // vector u of the row: strip h = u / vps, vector j = u mod vps of the strip
+    for (uint32_t u0 = threadIdx.x; u0 < p.vpr; u0 += 4 * blockDim.x) {
+      uint4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t u = u0 + k * blockDim.x;
+        v[k] = make_uint4(0u, 0u, 0u, 0u);
+        if (u < p.vpr) {
+          const uint32_t h = __umulhi(u, p.vps_magic), j = u - h * p.vps;
+          if (!p.padded) {
+            const int64_t e = ((n * p.i_h + h) * p.iwc + static_cast<int64_t>(w) * p.wstep) / VEC + j;
+            v[k] = __ldg(I4 + e);
+          } else {
+            // padded image: row h - pad_h, element column w s_w i_c + j VEC - pad_w i_c
+            const int64_t y = static_cast<int64_t>(h) - p.pad_h;
+            const int64_t xc = static_cast<int64_t>(w) * p.wstep + static_cast<int64_t>(j) * VEC - p.pad_wc;
+            if (y >= 0 && y < p.src_h && xc >= 0 && xc < p.src_iwc)
+              v[k] = __ldg(I4 + ((n * p.src_h + y) * p.src_iwc + xc) / VEC);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t u = u0 + k * blockDim.x;
+        if (u < p.vpr) dst[u] = v[k];
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) lower_direct_kernel(const T* __restrict__ I, T* __restrict__ L,
                                                            int64_t i_n, int64_t i_h, int64_t i_w,
@@ -863,6 +928,39 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
     return cudaGetLastError();
   }
 
+  // Row-copy path (lower_rows_kernel): every strip a whole number of 16-byte
+  // vectors at 16-byte aligned addresses on both sides (MEC_LOWER_ROWS=0: the
+  // staged band kernel below)
+  {
+    const uint32_t vecn = static_cast<uint32_t>(16 / pl.elt);
+    const bool rows_ok = !spad && p.kwc % vecn == 0 && p.wstep % vecn == 0 && p.iwc % vecn == 0 &&
+                         pitch % vecn == 0 && (!p.padded || (p.src_iwc % vecn == 0 && p.pad_wc % vecn == 0)) &&
+                         reinterpret_cast<uintptr_t>(I) % 16 == 0 && reinterpret_cast<uintptr_t>(L) % 16 == 0 &&
+                         s.i_h * (p.kwc / vecn) < (1LL << 31) && s.i_n * pl.o_w < (1LL << 40) &&
+                         // the magic-number division u / vps is exact for u vps < 2^32
+                         static_cast<uint64_t>(s.i_h) * (p.kwc / vecn) * (p.kwc / vecn) < (1ull << 32);
+    const char* er = getenv("MEC_LOWER_ROWS");
+    if (rows_ok && (er == nullptr || atoi(er) != 0)) {
+      LowerParams q = p;
+      q.vps = p.kwc / vecn;
+      q.vpr = static_cast<uint32_t>(s.i_h) * q.vps;
+      q.vps_magic = static_cast<uint32_t>((1ull << 32) / q.vps + 1);
+      q.n_rows = s.i_n * pl.o_w;
+      // rows per CTA: ~8 vectors per thread (one unrolled trip of 4 x 256 x 2)
+      q.rows_per_cta = static_cast<int>(std::max<int64_t>(1, 2048 / q.vpr));
+      if (const char* e = getenv("MEC_LOWER_ROWS_PER_CTA")) q.rows_per_cta = std::max(1, atoi(e));
+      const int64_t row_blocks = (q.n_rows + q.rows_per_cta - 1) / q.rows_per_cta;
+      const int64_t grid = row_blocks + prep_blocks;
+      if (grid > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
+      const size_t rsmem = (q.prep64 && prep_blocks > 0) ? kPrep64Smem : 64;
+      if (pl.elt == 2)
+        lower_rows_kernel<uint16_t><<<static_cast<unsigned>(grid), 256, rsmem, st>>>(q);
+      else
+        lower_rows_kernel<uint32_t><<<static_cast<unsigned>(grid), 256, rsmem, st>>>(q);
+      if (launches) ++*launches;
+      return cudaGetLastError();
+    }
+  }
   const int64_t row_bytes = static_cast<int64_t>(p.iwc) * pl.elt;
   const int64_t max_smem = 96 * 1024;
   bool use_smem = row_bytes + 64 <= max_smem && s.k_w * s.i_c < (1 << 20) && p.iwc < (1u << 24);
