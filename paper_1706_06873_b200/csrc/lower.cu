@@ -779,7 +779,8 @@ __global__ void __launch_bounds__(256) lower_rows_kernel(const LowerParams p) {
         const uint32_t u = u0 + k * blockDim.x;
         v[k] = make_uint4(0u, 0u, 0u, 0u);
         if (u < p.vpr) {
-          const uint32_t h = __umulhi(u, p.vps_magic), j = u - h * p.vps;
+          // (vps == 1: the magic number 2^32 + 1 does not fit; h = u)
+          const uint32_t h = p.vps == 1 ? u : __umulhi(u, p.vps_magic), j = u - h * p.vps;
           if (!p.padded) {
             const int64_t e = ((n * p.i_h + h) * p.iwc + static_cast<int64_t>(w) * p.wstep) / VEC + j;
             v[k] = __ldg(I4 + e);
@@ -797,6 +798,69 @@ __global__ void __launch_bounds__(256) lower_rows_kernel(const LowerParams p) {
         const uint32_t u = u0 + k * blockDim.x;
         if (u < p.vpr) dst[u] = v[k];
       }
+    }
+  }
+}
+
+// Row-gather lowering for strips that are not whole 16-byte vectors (i_c = 3:
+// AlexNet conv1 / cv1-cv3, cv7).  Each thread writes one 16-byte vector of an
+// L row (n, w): its VEC elements e come from strip h = e / (k_w i_c), element
+// j = e mod (k_w i_c), i.e. I[n, h, s_w w + j / i_c, j mod i_c] (Alg.2 l.4-6) --
+// consecutive within a strip, a vector spanning at most two strips.  Element
+// loads (a warp's loads fall in a few contiguous runs of I: L1/L2 hits for the
+// k_w / s_w-fold re-reads), one 16-byte store.  Rows past l_cols in the
+// pitched L (pitch padding) are written with whatever the clamped gather
+// reads (never read by a GEMM: the weight rows there are zero).
+template <typename T>
+__global__ void __launch_bounds__(256) lower_rows_gather_kernel(const LowerParams p) {
+  constexpr uint32_t VEC = 16 / sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem[];
+  ptx::griddep_launch_dependents();
+  if (p.zero_words != nullptr && blockIdx.x == gridDim.x - 1)
+    for (uint32_t i = threadIdx.x; i < p.n_zero; i += blockDim.x) p.zero_words[i] = 0u;
+  const int64_t row_blocks = (p.n_rows + p.rows_per_cta - 1) / p.rows_per_cta;
+  if (static_cast<int64_t>(blockIdx.x) >= row_blocks) {
+    const int64_t n_prep = gridDim.x - row_blocks;
+    const int64_t n_tiles = prep_units<T>(p);
+    for (int64_t t = blockIdx.x - row_blocks; t < n_tiles; t += n_prep) prep_unit<T>(p, t, smem);
+    return;
+  }
+  const T* Ie = reinterpret_cast<const T*>(p.I);
+  const uint32_t lcols = static_cast<uint32_t>(p.i_h) * p.kwc;  // valid elements of an L row
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * p.rows_per_cta;
+  const int64_t r1 = min(p.n_rows, r0 + p.rows_per_cta);
+  for (int64_t row = r0; row < r1; ++row) {
+    const int64_t n = row / p.o_w, w = row - n * p.o_w;
+    T* dst = reinterpret_cast<T*>(p.L) + static_cast<size_t>(row * p.pitch);
+    const T* src_row = Ie + n * p.i_h * p.iwc + static_cast<int64_t>(w) * p.wstep;  // strip h at + h iwc
+    for (uint32_t u = threadIdx.x; u < p.vpr; u += blockDim.x) {
+      uint32_t e = u * VEC;
+      // first element's strip and offset (magic division by kwc, exact for e < 2^20)
+      uint32_t h = __umulhi(e, p.kwc_magic), j = e - h * p.kwc;
+      if (p.kwc == 1) { h = e; j = 0; }
+      T val[VEC];
+#pragma unroll
+      for (uint32_t k = 0; k < VEC; ++k) {
+        if (e + k < lcols) {
+          val[k] = __ldg(src_row + static_cast<int64_t>(h) * p.iwc + j);
+        } else {
+          val[k] = T(0);
+        }
+        if (++j == p.kwc) {
+          j = 0;
+          ++h;
+        }
+      }
+      uint4 o;
+      if constexpr (sizeof(T) == 2) {
+        o.x = static_cast<uint32_t>(val[0]) | (static_cast<uint32_t>(val[1]) << 16);
+        o.y = static_cast<uint32_t>(val[2]) | (static_cast<uint32_t>(val[3]) << 16);
+        o.z = static_cast<uint32_t>(val[4]) | (static_cast<uint32_t>(val[5]) << 16);
+        o.w = static_cast<uint32_t>(val[6]) | (static_cast<uint32_t>(val[7]) << 16);
+      } else {
+        o = make_uint4(val[0], val[1], val[2], val[3]);
+      }
+      reinterpret_cast<uint4*>(dst)[u] = o;
     }
   }
 }
@@ -957,6 +1021,34 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
         lower_rows_kernel<uint16_t><<<static_cast<unsigned>(grid), 256, rsmem, st>>>(q);
       else
         lower_rows_kernel<uint32_t><<<static_cast<unsigned>(grid), 256, rsmem, st>>>(q);
+      if (launches) ++*launches;
+      return cudaGetLastError();
+    }
+  }
+  // Row-gather path (lower_rows_gather_kernel) for the other unpadded layouts
+  // with 16-byte aligned L rows.  Opt-in (MEC_LOWER_GATHER=1): measured slower
+  // than the staged aligned-copies kernel below (AlexNet conv1 b32 22.9 vs
+  // 15.9 us, cv3 b128 85 vs 55 us) -- one element load per 2-4 bytes of L.
+  {
+    const uint32_t vecn = static_cast<uint32_t>(16 / pl.elt);
+    const char* eg = getenv("MEC_LOWER_GATHER");
+    const bool g_ok = !spad && !p.padded && pitch % vecn == 0 && reinterpret_cast<uintptr_t>(L) % 16 == 0 &&
+                      reinterpret_cast<uintptr_t>(I) % sizeof(uint16_t) == 0 && pl.l_cols < (1LL << 20) &&
+                      s.i_n * pl.o_w < (1LL << 40);
+    if (g_ok && eg != nullptr && atoi(eg) != 0) {
+      LowerParams q = p;
+      q.vpr = static_cast<uint32_t>((pl.l_cols + vecn - 1) / vecn);  // vectors covering l_cols (<= pitch)
+      q.n_rows = s.i_n * pl.o_w;
+      q.rows_per_cta = static_cast<int>(std::max<int64_t>(1, 1024 / q.vpr));
+      if (const char* e = getenv("MEC_LOWER_ROWS_PER_CTA")) q.rows_per_cta = std::max(1, atoi(e));
+      const int64_t row_blocks = (q.n_rows + q.rows_per_cta - 1) / q.rows_per_cta;
+      const int64_t grid = row_blocks + prep_blocks;
+      if (grid > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
+      const size_t rsmem = (q.prep64 && prep_blocks > 0) ? kPrep64Smem : 64;
+      if (pl.elt == 2)
+        lower_rows_gather_kernel<uint16_t><<<static_cast<unsigned>(grid), 256, rsmem, st>>>(q);
+      else
+        lower_rows_gather_kernel<uint32_t><<<static_cast<unsigned>(grid), 256, rsmem, st>>>(q);
       if (launches) ++*launches;
       return cudaGetLastError();
     }
