@@ -26,9 +26,9 @@ if has cfgs; then
   for c in cv4 cv5 cv6 cv11 cv12; do $B --config C4_$c --batch 1024 --no-fused-alt --steps 5 >> gpurun_out/bench_cfgs.json 2>> gpurun_out/bench_cfgs.err; done
 fi
 if has ncu; then
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-tf32 --no-tf32-peak > /dev/null 2>&1
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2_tf32.csv python bench.py --config C2_tf32 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-tf32-peak > /dev/null 2>&1
-  K='regex:lower_kernel|sweep_gemm|window_gemm|wide_gemm|pair_sweep'
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-tf32 --no-tf32-peak --no-fused-alt > /dev/null 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c2_tf32.csv python bench.py --config C2_tf32 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-tf32-peak --no-fused-alt > /dev/null 2>&1
+  K='regex:lower_kernel|lower_rows|sweep_gemm|window_gemm|wide_gemm|pair_sweep'
   NB="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-fused-alt --no-tf32 --no-tf32-peak"
   for spec in "C2:" "C2_tf32:" "C1:" "C3:" "C4_cv5:--batch 128" "C4_cv6:--batch 128" "C4_cv11:--batch 128" "C4_cv12:--batch 128" "C4_cv8:--batch 128"; do
     c=${spec%%:*}; extra=${spec#*:}

@@ -33,11 +33,12 @@ KEYS = [
 
 
 def short(name):
-    for k in ("lower_kernel", "window_gemm_kernel", "sweep_gemm_kernel", "wide_gemm_kernel", "pair_sweep_kernel",
+    for k in ("lower_rows_kernel", "lower_rows_gather_kernel", "lower_kernel", "window_gemm_kernel", "sweep_gemm_kernel", "wide_gemm_kernel", "pair_sweep_kernel",
               "copy16_kernel", "block_permute_kernel", "flush_kernel", "synth_kernel", "fused"):
         if k in name:
             # every window-GEMM kernel is the "window_gemm" stage of bench.py
-            return {"lower_kernel": "mec_lower", "window_gemm_kernel": "window_gemm",
+            return {"lower_kernel": "mec_lower", "lower_rows_kernel": "mec_lower", "lower_rows_gather_kernel": "mec_lower",
+                    "window_gemm_kernel": "window_gemm",
                     "sweep_gemm_kernel": "window_gemm", "wide_gemm_kernel": "window_gemm",
                     "pair_sweep_kernel": "window_gemm",
                     "copy16_kernel": "sola_copy", "block_permute_kernel": "sola_transpose"}.get(k, k)
