@@ -648,6 +648,25 @@ __device__ __forceinline__ void mma_ts_row_elect(uint32_t tmem_d, uint32_t a_tme
 #undef MEC_TS_ROW_BODY
 }
 
+// Whole-warp call: one elected lane copies a 128-row x 128-byte SW128 K-major
+// atom from shared memory (descriptor sdesc) into TMEM columns taddr ..
+// taddr + 31 (row m -> lane m, 2 bf16 / 1 fp32 per 32-bit column): 4 x
+// tcgen05.cp.128x256b of its 32-byte K chunks (descriptor start + 32 B each).
+// Copies and MMAs issued by one thread execute in issue order.
+__device__ __forceinline__ void tmem_cp_atom_elect(uint32_t taddr, uint64_t sdesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b64 d1, d2, d3;\n\t.reg .b32 t1, t2, t3;\n\t"
+      "add.u64 d1, %1, 2;\n\tadd.u64 d2, %1, 4;\n\tadd.u64 d3, %1, 6;\n\t"
+      "add.u32 t1, %0, 8;\n\tadd.u32 t2, %0, 16;\n\tadd.u32 t3, %0, 24;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t"
+      "@e tcgen05.cp.cta_group::1.128x256b [t1], d1;\n\t"
+      "@e tcgen05.cp.cta_group::1.128x256b [t2], d2;\n\t"
+      "@e tcgen05.cp.cta_group::1.128x256b [t3], d3;\n\t}" ::"r"(taddr),
+      "l"(sdesc)
+      : "memory");
+}
+
 // Whole-warp call: one elected lane commits (arrives on `bar` when done).
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
   asm volatile(

@@ -129,6 +129,9 @@ struct SweepParams {
   uint32_t stage_out_bytes;
   uint32_t backoff_ns;  // copier / epilogue waits: nanosleep between probes (0: spin)
   int n_iss;  // MMA issuer warps (1 or 2)
+  // A into the TMEM ring by tcgen05.cp issued from the MMA thread (DESIGN.md
+  // 6.2b): no copier warps; the copies and the MMAs execute in issue order
+  bool cp;
   // CTA-pair mode (kPair kernels): CTA tiles are dealt in
   // pairs (CTA rank r takes tile 2 pt + r); n_tiles = n_mt groups
   int64_t n_tiles;
@@ -374,7 +377,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     ptx::tma_prefetch_desc(&tmO);
     for (int i = 0; i < S; ++i) {
       ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&empty[i], kSwCopyWarps);
+      ptx::mbar_init(&empty[i], p.cp ? 1 : kSwCopyWarps);  // cp mode: one tcgen05.commit per atom
     }
     // (pair mode: the leader's ring barriers count both CTAs' copier warps)
     for (int i = 0; i < p.ns; ++i) ptx::mbar_init(&afull[i], kSwCopyWarps * (kPair ? 2 : 1));
@@ -455,6 +458,82 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         }
       }
     }
+  } else if (p.cp && warp == 1 && leader) {
+    // ===================== MMA issuer with tcgen05.cp (cp mode) =====================
+    // One thread copies each landed atom from its shared-memory stage into the
+    // TMEM ring (4 x tcgen05.cp.128x256b of the SW128 atom, + the guard copy
+    // of slot 0) and issues the rows.  Copies and MMAs of one thread execute
+    // in issue order, so a ring slot is rewritten only after the MMAs issued
+    // before (the rows that read its previous atom) have read it: no slot
+    // counters.  Atoms are copied just before the first row that needs them.
+    const uint64_t b_desc0 = ptx::smem_desc_sw128(ptx::smem_u32(smemB));
+    const uint64_t a_sdesc0 = ptx::smem_desc_sw128(ptx::smem_u32(smemA));
+    const uint32_t b_tile16 = b_tile_bytes >> 4;
+    const uint32_t bvar16 = b_tile16 * static_cast<uint32_t>(p.nb_atoms);
+    const int kcl = p.kchunk_log2, cs = p.col_shift, bkl = p.bk_log2;
+    const int ns = p.ns, shift = p.shift, mmask = p.mvec - 1;
+    const int kdim_r = p.kdim + (1 << kcl) - 1;
+    const uint32_t ring0 = tmem_base + p.a_col0, ring_cols = static_cast<uint32_t>(32 * ns);
+    const bool no_mma = (p.dbg & 2) != 0;
+    if (t_begin < p.n_items) ptx::mbar_wait(bfull, 0);
+    int stage = 0, ring = 0;  // next atom's smem stage and TMEM ring slot
+    uint32_t sphase = 0;
+    uint32_t q = 0;  // global sequence number of the item's row 0
+    for (int64_t t = t_begin; t < p.n_items; t += t_step) {
+      const SwItem it = sw_decode(p, t, kPair, rank);
+      const int slot0 = ring;  // ring slot of the item's atom 0
+      int cp_next = 0;         // next atom of the item to copy
+      auto copy_atom = [&]() {
+        ptx::mbar_wait(&full[stage], sphase);
+        ptx::tc_fence_after();
+        const uint64_t src = a_sdesc0 + (static_cast<uint32_t>(stage * kSwAtomBytes) >> 4);
+        if (!(p.dbg & 4)) {
+          ptx::tmem_cp_atom_elect(ring0 + static_cast<uint32_t>(ring * 32), src);
+          if (ring == 0) ptx::tmem_cp_atom_elect(tmem_base + p.guard_col, src);  // guard
+        }
+        ptx::mma_commit_elect(&empty[stage]);  // the stage is free once the copies have read it
+        __syncwarp();
+        if (++stage == p.stages) {
+          stage = 0;
+          sphase ^= 1u;
+        }
+        if (++ring == ns) ring = 0;
+        ++cp_next;
+      };
+      int o = it.off0;
+      for (int r = 0; r < it.nrows; ++r, o += shift) {
+        const int d = o & mmask;
+        const int a = o - d;  // stream element of the row's first step
+        const int nk = (kdim_r + d) >> kcl;
+        const int n_full = (nk + 3) >> 2;
+        const int last = (a + (n_full << (kcl + 2)) - 1) >> bkl;  // last atom the row reads
+        while (cp_next <= last) copy_atom();
+        const uint32_t g = q + static_cast<uint32_t>(r);
+        const int acc = p.n_acc == 2 ? static_cast<int>(g & 1u) : 0;
+        const uint32_t acc_use = p.n_acc == 2 ? (g >> 1) : g;
+        ptx::mbar_wait(&tempty[acc], (acc_use & 1u) ^ 1u);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * p.bn);
+        int s0 = slot0 + (a >> bkl);
+        while (s0 >= ns) s0 -= ns;
+        const uint32_t col = ring0 + static_cast<uint32_t>(s0 * 32) + (static_cast<uint32_t>(a & ((1 << bkl) - 1)) >> cs);
+        const uint64_t bvar = b_desc0 + static_cast<uint32_t>(d >> p.ds_log2) * bvar16;
+        if (n_full > 0 && !no_mma)
+          // every atom the row needs is copied (issued before these MMAs): no waits in the loop
+          ptx::mma_ts_row_elect<kTF32, kPair>(d_tmem, col, ring0 + ring_cols, ring_cols, static_cast<uint32_t>(bvar),
+                                              b_tile16, p.idesc, n_full, a, kcl + 2, bkl, ptx::smem_u32(full), 0, 0u,
+                                              1 << 30, ns);
+        if constexpr (kPair) ptx::mma_commit_pair_elect(&tfull[acc], 0x3);
+        else ptx::mma_commit_elect(&tfull[acc]);
+        __syncwarp();
+      }
+      while (cp_next < it.n_a) copy_atom();  // atoms no row reads (the stream's rounding): release them
+      ring = slot0 + it.n_a;
+      while (ring >= ns) ring -= ns;
+      q += static_cast<uint32_t>(it.nrows);
+    }
+  } else if (p.cp && (warp == 1 || warp == kSwMma2Warp || warp < kSwFirstEpiWarp)) {
+    // (cp mode: no copier warps, no second issuer)
   } else if ((warp == 1 || (warp == kSwMma2Warp && p.n_iss > 1)) && leader) {
     // ===================== MMA issuer(s) =====================
     // Issuer mi takes the rows with global sequence number g = mi (mod
@@ -912,9 +991,13 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   // (measured: 2 issuers win where the accumulators are 64 columns -- C2
   // 434->397 us, C3 127->117 us, cv3 106->95 us, cv7 255->250 us -- and lose
   // ~4-7% at k_c = 96, C1 / cv1, whose TMEM ring has 2 slots fewer)
+  // cp mode (MEC_SWEEP_CP=1 / 0): the MMA thread copies the atoms into TMEM
+  // itself (tcgen05.cp), one issuer; not with CTA pairs (one cta_group per kernel)
+  p.cp = !pair && getenv("MEC_SWEEP_CP") && atoi(getenv("MEC_SWEEP_CP")) != 0;
   p.n_iss = (2 * pl.shift < pl.kdim && pl.bn <= 64 && n_acc == 2) ? 2 : 1;
   if (const char* e = getenv("MEC_SWEEP_ISSUERS"))  // (experiments; 2 needs 2 shift < kdim, 2 accumulators)
     p.n_iss = (atoi(e) >= 2 && 2 * pl.shift < pl.kdim && n_acc == 2) ? 2 : 1;
+  if (p.cp) p.n_iss = 1;
   p.backoff_ns = getenv("MEC_SWEEP_BACKOFF") ? static_cast<uint32_t>(atoi(getenv("MEC_SWEEP_BACKOFF"))) : 0u;
   // epilogue: pass width = 128 / 64 / 32 bytes per row, dividing bn
   int row_bytes = 128;

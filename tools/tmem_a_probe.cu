@@ -99,10 +99,11 @@ __global__ void __launch_bounds__(128, 1) probe(float* out_mma, uint32_t* out_cp
     if (lane == 0) {
       const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(atomA));
       for (int k = 0; k < 4; ++k) tmem_cp_128x256b(tmem + 128 + 8 * k, ad + 2 * k);
-      // and an MMA reading the copied A at column offset 2 (elements 4..19)
+      // and an MMA reading the copied A at column offset 2 (elements 4..19);
+      // the_off = 1: at column 0 instead (the 4-column rule: offsets 1-3 trap)
       asm volatile(
           "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, 0;" ::"r"(tmem + 64),
-          "r"(tmem + 130), "l"(bdesc), "r"(ptx::instr_desc(false, 128, 32))
+          "r"(tmem + (the_off == 1 ? 128 : 130)), "l"(bdesc), "r"(ptx::instr_desc(false, 128, 32))
           : "memory");
       ptx::mma_commit(&bar);
     }
@@ -169,6 +170,58 @@ __global__ void __launch_bounds__(128, 1) probe(float* out_mma, uint32_t* out_cp
     }
     ph ^= 1;
   }
+  // mode 7 / 8: tcgen05.cp from a NON-swizzled K-major atom laid out as
+  // [16-byte K chunk c][row m][16 B] (8x16 B core matrices contiguous: SBO =
+  // 128 B between 8-row groups, LBO = 2048 B between K chunks), copy k takes
+  // chunks 2k, 2k+1 (start + 4096 k) -> TMEM columns 128 + 8k; then an MMA on
+  // the copied A (columns 128.., K elements 0..15).  Mode 8: throughput.
+  if (mode == 7 || mode == 8) {
+    unsigned char* atomN = smem + 16384 + 12288;  // 16 KB
+    for (int i = threadIdx.x; i < 128 * 64; i += blockDim.x) {
+      const int r = i / 64, k = i % 64;
+      *reinterpret_cast<uint16_t*>(atomN + (k / 8) * 2048 + r * 16 + (k % 8) * 2) = bf16_bits(a_val(r, k));
+    }
+    ptx::fence_proxy_async_smem();
+    __syncthreads();
+    if (warp == 0 && lane == 0) {
+      auto ndesc = [&](uint32_t addr) {
+        uint64_t d = 0;
+        d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+        d |= static_cast<uint64_t>(2048 >> 4) << 16;  // LBO: next K core-matrix column
+        d |= static_cast<uint64_t>(128 >> 4) << 32;   // SBO: next 8-row group
+        d |= static_cast<uint64_t>(1) << 46;          // version
+        return d;                                     // layout 0 = no swizzle
+      };
+      const uint32_t base = ptx::smem_u32(atomN);
+      const long long t0 = clock64();
+      const int reps = mode == 8 ? 256 : 1;
+      for (int it = 0; it < reps; ++it)
+        for (int k = 0; k < 4; ++k) tmem_cp_128x256b(tmem + 128 + 8 * k, ndesc(base + 4096 * k));
+      if (mode == 7)
+        asm volatile(
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, 0;" ::"r"(tmem + 64),
+            "r"(tmem + 128), "l"(bdesc), "r"(ptx::instr_desc(false, 128, 32))
+            : "memory");
+      ptx::mma_commit(&bar);
+      ptx::mbar_wait(&bar, ph);
+      cyc[2] = clock64() - t0;
+    }
+    __syncwarp();
+    ptx::mbar_wait(&bar, ph);
+    ph ^= 1;
+    ptx::tc_fence_after();
+    if (mode == 7) {
+      uint32_t v[16];
+      for (int h = 0; h < 2; ++h) {
+        ptx::tmem_ld_32x32b_x16(tmem + lane_base + 128 + 16 * h, v);
+        ptx::tmem_ld_wait();
+        for (int j = 0; j < 16; ++j) out_cp[m * 32 + 16 * h + j] = v[j];
+        ptx::tmem_ld_32x32b_x16(tmem + lane_base + 64 + 16 * h, v);
+        ptx::tmem_ld_wait();
+        for (int j = 0; j < 16; ++j) out_cpmma[m * 32 + 16 * h + j] = __uint_as_float(v[j]);
+      }
+    }
+  }
   // tcgen05.cp throughput: 1024 copies of 128x256b (4 KB each)
   if (mode == 4 && warp == 0) {
     const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(atomA));
@@ -202,7 +255,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&d_cp, 128 * 32 * 4);
   cudaMalloc(&d_cpmma, 128 * 32 * 4);
   cudaMalloc(&d_cyc, 3 * 8);
-  const int smem = 16384 + 12288 + 1024;
+  const int smem = 16384 + 12288 + 16384 + 1024;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaMemset(d_mma, 0xff, kOffs * 128 * 32 * 4);
   probe<<<1, 128, smem>>>(d_mma, d_cp, d_cpmma, d_cyc, mode, the_off);
@@ -231,6 +284,36 @@ int main(int argc, char** argv) {
     printf("TS MMA A column offset %3d (elements %3d..): %s (%d/4096 wrong)\n", offs[o], 2 * offs[o],
            bad ? "MISMATCH" : "exact", bad);
   }
+  if (mode == 7) {
+    int bad = 0;
+    auto bits = [](float f) {
+      uint32_t u;
+      memcpy(&u, &f, 4);
+      return u >> 16;
+    };
+    for (int mm = 0; mm < 128; ++mm)
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t ex = bits(a_val(mm, 2 * j)) | (bits(a_val(mm, 2 * j + 1)) << 16);
+        if (h_cp[mm * 32 + j] != ex) {
+          if (bad < 4) printf("  cp lane %d col %d: got %08x want %08x\n", mm, j, h_cp[mm * 32 + j], ex);
+          ++bad;
+        }
+      }
+    printf("tcgen05.cp 128x256b from a no-swizzle K-major atom: %s (%d/4096 wrong)\n", bad ? "MISMATCH" : "exact", bad);
+    bad = 0;
+    for (int mm = 0; mm < 128; ++mm)
+      for (int n = 0; n < 32; ++n) {
+        float ref = 0;
+        for (int k = 0; k < 16; ++k) ref += a_val(mm, k) * b_val(n, k);
+        if (h_cpmma[mm * 32 + n] != ref) ++bad;
+      }
+    printf("MMA on the cp'd A: %s (%d wrong)\n", bad ? "MISMATCH" : "exact", bad);
+    return 0;
+  }
+  if (mode == 8) {
+    printf("tcgen05.cp 128x256b (no swizzle): %.1f cyc each (4 KB)\n", cyc[2] / 1024.0);
+    return 0;
+  }
   if (mode != 1) goto timing;
   {
   int bad = 0;
@@ -253,7 +336,7 @@ int main(int argc, char** argv) {
   for (int mm = 0; mm < 128; ++mm)
     for (int n = 0; n < 32; ++n) {
       float ref = 0;
-      for (int k = 0; k < 16; ++k) ref += a_val(mm, 4 + k) * b_val(n, k);
+      for (int k = 0; k < 16; ++k) ref += a_val(mm, (the_off == 1 ? 0 : 4) + k) * b_val(n, k);
       if (h_cpmma[mm * 32 + n] != ref) ++bad;
     }
   printf("MMA on cp'd A at column offset 2: %s (%d wrong)\n", bad ? "MISMATCH" : "exact", bad);
