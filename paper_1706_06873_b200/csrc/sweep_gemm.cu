@@ -79,8 +79,22 @@ extern "C" int mec_sweep_trace_enable(void** dev_buf_out, size_t* bytes_out) {
 namespace mec {
 namespace {
 
-constexpr int kSwCopyWarps = 4;
-constexpr int kSwEpiWarps = 8;
+// copier warps in groups of 4 (one per 32-row quarter; groups take alternate
+// atoms) and epilogue warps in groups of 4 (groups take alternate rows).
+// Default 1 copier group + 2 epilogue groups; 2 + 1 (-DMEC_SW_COPY_GROUPS=2
+// -DMEC_SW_EPI_GROUPS=1) measured slower: C2 GEMM 319 vs 315 us, cv3 b128
+// 125 vs 89 us, cv7 391 vs 241 us (one epilogue group cannot keep up with
+// short windows).
+#ifndef MEC_SW_COPY_GROUPS
+#define MEC_SW_COPY_GROUPS 1
+#endif
+#ifndef MEC_SW_EPI_GROUPS
+#define MEC_SW_EPI_GROUPS 2
+#endif
+constexpr int kSwCopyGroups = MEC_SW_COPY_GROUPS;
+constexpr int kSwEpiGroups = MEC_SW_EPI_GROUPS;
+constexpr int kSwCopyWarps = 4 * kSwCopyGroups;
+constexpr int kSwEpiWarps = 4 * kSwEpiGroups;
 constexpr int kSwFirstCopyWarp = 2;
 constexpr int kSwFirstEpiWarp = kSwFirstCopyWarp + kSwCopyWarps;
 // MMA issuer warps (rows dealt round-robin, p.n_iss = 1 or 2; the second is
@@ -88,7 +102,7 @@ constexpr int kSwFirstEpiWarp = kSwFirstCopyWarp + kSwCopyWarps;
 // with the other's MMAs (single-warp issue is latency-bound).
 constexpr int kSwMaxIssuers = 2;
 constexpr int kSwMma2Warp = kSwFirstEpiWarp + kSwEpiWarps;
-constexpr int kSwThreads = 32 * (kSwMma2Warp + 1);  // 480
+constexpr int kSwThreads = 32 * (kSwMma2Warp + 1);  // 480 (2 copier groups + 1 epilogue group, or 1 + 2)
 constexpr int kSwAtomBytes = kBM * kTileKBytes;                   // 16 KB: 128 rows x 128 B
 constexpr int kSwMaxRing = 16;
 constexpr int kSwMaxAcc = 8;
@@ -377,15 +391,15 @@ __global__ void __launch_bounds__(kSwThreads, 1)
     ptx::tma_prefetch_desc(&tmO);
     for (int i = 0; i < S; ++i) {
       ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&empty[i], p.cp ? 1 : kSwCopyWarps);  // cp mode: one tcgen05.commit per atom
+      ptx::mbar_init(&empty[i], p.cp ? 1 : 4);  // one copier group; cp mode: one tcgen05.commit per atom
     }
     // (pair mode: the leader's ring barriers count both CTAs' copier warps)
-    for (int i = 0; i < p.ns; ++i) ptx::mbar_init(&afull[i], kSwCopyWarps * (kPair ? 2 : 1));
+    for (int i = 0; i < p.ns; ++i) ptx::mbar_init(&afull[i], 4 * (kPair ? 2 : 1));
     rows_done[0] = 0;
     rows_done[1] = 0;
     for (int i = 0; i < p.n_acc; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], kPair ? 8 : 4);  // the 4 warps of one epilogue group (x 2 CTAs)
+      ptx::mbar_init(&tempty[i], kPair ? 8 : 4);  // the 4 warps of an epilogue group (x 2 CTAs)
     }
     ptx::mbar_init(bfull, 1);
     ptx::fence_mbar_init();
@@ -700,6 +714,7 @@ __global__ void __launch_bounds__(kSwThreads, 1)
   } else if (warp < kSwFirstEpiWarp) {
     // ===================== copiers: smem atom -> TMEM ring =====================
     const int quarter = warp & 3;
+    const uint32_t cgroup = static_cast<uint32_t>((warp - kSwFirstCopyWarp) >> 2);  // atoms cseq = cgroup mod groups
     const int m = 32 * quarter + lane;  // tile row = TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>(32 * quarter) << 16;
     const uint32_t a_smem = ptx::smem_u32(smemA) + static_cast<uint32_t>(m * kTileKBytes);
@@ -717,6 +732,14 @@ __global__ void __launch_bounds__(kSwThreads, 1)
       // fr, and fo = the first element of row fr + 1
       int fr = 0, fo = it.off0 + p.shift;
       for (int i = 0; i < it.n_a; ++i, ++cseq) {
+        if (kSwCopyGroups > 1 && cseq % kSwCopyGroups != cgroup) {  // another group's atom
+          if (++stage == S) {
+            stage = 0;
+            sphase ^= 1u;
+          }
+          if (++slot == p.ns) slot = 0;
+          continue;
+        }
         if (p.backoff_ns) ptx::mbar_wait_backoff(&full[stage], sphase, p.backoff_ns);
         else ptx::mbar_wait(&full[stage], sphase);
         if (warp == kSwFirstCopyWarp && lane == 0) SW_TRACE(cseq, 1);
@@ -803,13 +826,13 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         const uint32_t qr = q + static_cast<uint32_t>(r);
         const uint32_t al = static_cast<uint32_t>(p.n_acc - 1);  // log2(n_acc), n_acc = 1 or 2
         const int acc = static_cast<int>(qr & al);
-        if (acc != group) continue;  // (n_acc = 1: group 0 takes every row)
+        if (kSwEpiGroups > 1 && acc != group) continue;  // (n_acc = 1 or one group: group 0 takes every row)
         if (p.backoff_ns) ptx::mbar_wait_backoff(&tfull[acc], (qr >> al) & 1u, p.backoff_ns);
         else ptx::mbar_wait(&tfull[acc], (qr >> al) & 1u);
         ptx::tc_fence_after();
         // row qr's MMAs are complete: its A atoms may be overwritten
         if (lane == 0 && ((warp - kSwFirstEpiWarp) & 3) == 0)
-          ptx::st_release_shared_u32(ptx::smem_u32(&rows_done[group]), (qr >> al) + 1u);
+          ptx::st_release_shared_u32(ptx::smem_u32(&rows_done[acc]), (qr >> al) + 1u);
         sw_store_row<kTF32>(p, &tmO, it.h0 + r, it.mt, it.g, quarter, lane,
                             tmem_base + lane_base + static_cast<uint32_t>(acc * p.bn), stg, stg_gen, &tempty[acc],
                             it.valid, kPair ? tempty0 + static_cast<uint32_t>(acc) * 8u : 0u);
@@ -832,6 +855,16 @@ __global__ void __launch_bounds__(kSwThreads, 1)
 }
 
 constexpr size_t kSwSmemBudget = 222 * 1024;
+constexpr int kSwMaxStages = 8;  // the barrier block holds 8 full + 8 empty barriers
+
+// epilogue pass width in bytes of an output row (128, 64 or 32, dividing
+// bn elt); MEC_SWEEP_EPI_BYTES caps it (experiments: less staging, more stages)
+int sweep_epi_row_bytes(const Plan& pl) {
+  int row_bytes = 128;
+  if (const char* e = getenv("MEC_SWEEP_EPI_BYTES")) row_bytes = std::max(32, std::min(128, atoi(e)));
+  while (row_bytes > 32 && (pl.bn * pl.elt) % row_bytes != 0) row_bytes /= 2;
+  return row_bytes;
+}
 
 // CTA-pair mode of the h-sweep (MEC_SWEEP_PAIR=1 / 0 forces it on / off)
 bool sweep_pair_mode(const Plan& pl) {
@@ -881,14 +914,14 @@ bool sweep_config(const Plan& pl, bool batch_folded, int* n_vres_out, int* n_acc
     ns = std::min(kSwMaxRing, (512 - kSwGuardCols - ((pl.bn + 31) / 32) * 32) / 32);
   }
   if (ns < span) return false;
-  int row_bytes = 128;
-  while (row_bytes > 32 && (pl.bn * pl.elt) % row_bytes != 0) row_bytes /= 2;
+  int row_bytes = sweep_epi_row_bytes(pl);
   const size_t epi = static_cast<size_t>(kSwEpiWarps) * 32 * row_bytes;
   // (pair mode: each CTA holds bn / 2 rows of the weights)
   const size_t b_res = static_cast<size_t>(n_vres) * (pl.kdim_pad / pl.bk) * (pair ? pl.bn / 2 : pl.bn) * kTileKBytes;
   const size_t fixed = b_res + epi + 66 * 8 + 64;
   if (fixed + 2 * kSwAtomBytes > kSwSmemBudget) return false;
-  const int stages = static_cast<int>(std::min<size_t>(8, (kSwSmemBudget - fixed) / kSwAtomBytes));
+  int stages = static_cast<int>(std::min<size_t>(kSwMaxStages, (kSwSmemBudget - fixed) / kSwAtomBytes));
+  if (const char* e = getenv("MEC_SWEEP_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));  // (experiments)
   (void)batch_folded;
   *n_vres_out = n_vres;
   *n_acc_out = n_acc;
@@ -1000,8 +1033,7 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   if (p.cp) p.n_iss = 1;
   p.backoff_ns = getenv("MEC_SWEEP_BACKOFF") ? static_cast<uint32_t>(atoi(getenv("MEC_SWEEP_BACKOFF"))) : 0u;
   // epilogue: pass width = 128 / 64 / 32 bytes per row, dividing bn
-  int row_bytes = 128;
-  while (row_bytes > 32 && (pl.bn * out_elt) % row_bytes != 0) row_bytes /= 2;
+  const int row_bytes = sweep_epi_row_bytes(pl);
   p.pw = row_bytes / out_elt;
   p.n_pass = pl.bn / p.pw;
   p.tma_store = ((pl.s.k_c * out_elt) % 16 == 0) && (reinterpret_cast<uintptr_t>(a.O) % 16 == 0) &&
