@@ -793,6 +793,20 @@ __device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const void* des
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar_cluster), "r"(x), "r"(y), "r"(z), "l"(cache_hint)
       : "memory");
 }
+// As tma_load_2d_pair, multicast to the CTAs of cta_mask (same shared offset in
+// each); bar_cta is this CTA's own (shared::cta) address of the barrier, with
+// the pair bit cleared so each destination pair's LEADER barrier counts the
+// bytes (the CUTLASS SM100 2-SM multicast convention).
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* smem_dst, const void* desc, uint32_t bar_cta, uint16_t cta_mask,
+                                                    int32_t x, int32_t y, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar_cta & 0xFEFFFFFFu), "h"(cta_mask), "r"(x), "r"(y),
+      "l"(cache_hint)
+      : "memory");
+}
+
 // TMEM allocation for a CTA pair: executed by the same warp in both CTAs.
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_result, uint32_t cols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_result)),
