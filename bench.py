@@ -68,8 +68,9 @@ def parse(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tf32", action="store_true", help="skip the tf32 variant of the config")
     ap.add_argument("--no-tf32-peak", action="store_true", help="skip the in-run tf32 peak measurement")
-    ap.add_argument("--e2e-chunks", type=int, default=4,
-                    help="image chunks of the e2e host-buffer call (copies pipelined with the kernels)")
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="image chunks of the e2e host-buffer call (copies pipelined with the kernels; "
+                         "0 = mec.auto_chunks: ~48 MB of copies per chunk, 4-16)")
     ap.add_argument("--no-flush", action="store_true", help="(diagnostic) do not flush L2")
     ap.add_argument("--no-fused-alt", action="store_true",
                     help="with --path auto, skip measuring the fused path alongside (north_star (3))")
@@ -456,7 +457,8 @@ def measure(args, cfg, rw, rank, ws, dev, peaks, peak_src, tf32_peak, primary=Tr
         I_h = I.cpu().pin_memory()
         K_h = K.cpu().pin_memory()
         O_h = torch.empty(O.shape, dtype=O.dtype).pin_memory()
-        nch = max(1, min(args.e2e_chunks, I.shape[0]))
+        nch = (max(1, min(args.e2e_chunks, I.shape[0])) if args.e2e_chunks > 0
+               else mec.auto_chunks(I.shape[0], (I.numel() + O.numel()) * I.element_size()))
         scratch = torch.empty(mec.host_scratch_bytes(*I.shape, *K.shape[:2], K.shape[3], s_h, s_w, I.dtype, nch),
                               dtype=torch.uint8, device=dev)
         eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
