@@ -173,6 +173,12 @@ __device__ __forceinline__ void st_shared_u32(uint32_t addr, uint32_t v) {
 
 // CTA-scope acquire load / release store of a shared-memory word (flags
 // between warps of one CTA).
+// relaxed gpu-scope load (a spin on a counter other CTAs bump; pair it with a fence)
+__device__ __forceinline__ uint32_t ld_relaxed_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint32_t ld_acquire_shared_u32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");

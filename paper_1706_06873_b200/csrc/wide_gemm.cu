@@ -17,10 +17,15 @@
 //     of B's N columns, 64 B per cycle per SM.
 //   * too few tiles: cv12 at batch 128 has 5 output rows x 640 folded rows
 //     x 512 channels = 30 pair tiles for 74 SM pairs.  The K loop of a tile is
-//     split into S ranges (split-K) run by different pairs; each range's fp32
-//     partial goes to a workspace slot, and the warp that arrives last on a
-//     per-(tile, 32-row block) counter sums the S partials IN SPLIT ORDER (so
-//     the result does not depend on which range finished last) and stores O.
+//     split into S ranges (split-K) run by different pairs.  The ranges then
+//     exchange partials (a reduce-scatter through L2): range k owns 1/S of
+//     the tile's output columns, writes its fp32 partial of the other columns
+//     to a workspace slot, counts itself in on a per-(tile, 32-row block)
+//     counter, waits for the other ranges' counts, and sums its own columns'
+//     S partials IN RANGE ORDER (so the result does not depend on which range
+//     finished first) before storing O.  Measured on B200 (cv12 b128, S = 2):
+//     GEMM 31.1 us with the earlier last-arriver-sums-everything scheme, 27.8
+//     with the exchange, 24.6 with no partial traffic at all.
 //
 // The windows are read in place from L with TMA (2-D map {i_h k_w i_c, i_n
 // o_w}, the box at column h s_h k_w i_c rounded down to the 32-byte box
@@ -89,6 +94,7 @@ struct WideParams {
   bool b_mn;
   int b_chunks, chunk_n;
   uint32_t b_chunk_bytes, b_kstep16;
+  int dbg;  // (timing experiments, MEC_WIDE_DBG: 1 skip the partial reads, 2 skip the partial writes)
 };
 
 struct Unit {
@@ -310,85 +316,109 @@ __global__ void __launch_bounds__(kWideThreads, 1)
       const float4* part_t = reinterpret_cast<const float4*>(p.part) +
                              ((c.tile * p.S * 2 + rank) * p.n_sub + sub) * slot_elems;
       const int64_t k_stride = 2 * p.n_sub * slot_elems;  // next range of the same tile
+      // output chunks of kPw columns; with split-K, range k owns (reduces and
+      // stores) the chunks ci with ci S / n_oc == k and hands the others over
+      const int n_oc = (p.bn + kPw - 1) / kPw;  // (bn a multiple of 32: the last chunk may be half)
       if (p.S > 1 && c.valid) {
         float4* mine = const_cast<float4*>(part_t) + c.ks * k_stride;
-        for (int c0 = 0; c0 < p.bn; c0 += 16) {
-          uint32_t v[16];
-          ptx::tmem_ld_32x32b_x16(taddr + c0, v);
-          ptx::tmem_ld_wait();
+#pragma unroll 1
+        for (int ci = 0; ci < n_oc && !(p.dbg & 2); ++ci) {
+          if (ci * p.S / n_oc == c.ks) continue;  // own chunk: stays in TMEM
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            __stcg(mine + static_cast<int64_t>(c0 / 4 + q) * kBM + m,
-                   make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                               __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+          for (int h16 = 0; h16 < kPw / 16; ++h16) {
+            const int c0 = ci * kPw + 16 * h16;
+            if (c0 >= p.bn) break;
+            uint32_t v[16];
+            ptx::tmem_ld_32x32b_x16(taddr + c0, v);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              __stcg(mine + static_cast<int64_t>(c0 / 4 + q) * kBM + m,
+                     make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                 __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+          }
         }
+        // release the hand-over, then wait until every range of this tile has
+        // handed over (the S ranges are co-resident units of the persistent grid:
+        // each writes before it waits, and a wait targets the same tile only)
         __threadfence();
         __syncwarp();
-        uint32_t old = 0;
-        if (lane == 0) old = atomicAdd(&p.cnt[(((c.tile * 2 + rank) * 4 + quarter) * p.n_sub) + sub], 1u);
-        old = __shfl_sync(0xffffffffu, old, 0);
-        store = store && old == static_cast<uint32_t>(p.S - 1);  // the last range of this block sums
-        if (store) __threadfence();
+        uint32_t* cnt = &p.cnt[(((c.tile * 2 + rank) * 4 + quarter) * p.n_sub) + sub];
+        if (lane == 0) atomicAdd(cnt, 1u);
+        bool owns = false;  // (S > n_oc: some ranges own no chunk)
+        for (int ci = 0; ci < n_oc; ++ci) owns = owns || ci * p.S / n_oc == c.ks;
+        store = store && owns;
+        if (store) {
+          if (lane == 0 && !(p.dbg & 1))
+            while (ptx::ld_relaxed_gpu_u32(cnt) < static_cast<uint32_t>(p.S)) __nanosleep(64);
+          __syncwarp();
+          __threadfence();  // (acquire: the other ranges' partials are read after this)
+        }
       }
       if (store) {
-        for (int c0 = 0; c0 < p.bn && c0 < cols_left; c0 += kPw) {
-          // 32-column blocks: TMEM (own range) [+ the other ranges' partials,
-          // summed in range order 0, 1, ..., S-1] -> packed -> swizzled staging
+#pragma unroll 1
+        for (int ci = 0; ci < n_oc && ci * kPw < cols_left; ++ci) {
+          if (p.S > 1 && ci * p.S / n_oc != c.ks) continue;
+          const int c0 = ci * kPw;
+          // split-K, S = 2: the other range's partial, 32 columns (8 loads per
+          // thread) in flight ahead of the block being summed (fp32 addition
+          // commutes: own + other is the range-order sum)
+          const float4* src2 = part_t + (1 - c.ks) * k_stride + static_cast<int64_t>(c0 / 4) * kBM + m;
+          float4 x2[8];
+          if (p.S == 2 && !(p.dbg & 1)) {
 #pragma unroll
+            for (int q = 0; q < 8; ++q) x2[q] = __ldcg(src2 + static_cast<int64_t>(q) * kBM);
+          }
+#pragma unroll 1
           for (int sb = 0; sb < kPw / 32; ++sb) {
+            // 32 columns: TMEM (this range) [+ the other ranges' partials, in
+            // range order 0, 1, ..., S-1] -> packed -> swizzled staging
             const int cb = c0 + 32 * sb;
+            if (cb >= p.bn) break;
             uint32_t v[32];
             ptx::tmem_ld_32x32b_x16(taddr + cb, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
             ptx::tmem_ld_32x32b_x16(taddr + cb + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
             ptx::tmem_ld_wait();
-            if (p.S == 2) {
-              // one other range: its 8 chunks loaded together, then added in range order
-              const float4* src = part_t + (1 - c.ks) * k_stride + static_cast<int64_t>(cb / 4) * kBM + m;
-              float4 x[8];
-#pragma unroll
-              for (int q = 0; q < 8; ++q) x[q] = __ldcg(src + static_cast<int64_t>(q) * kBM);
+            if (p.S == 2 && !(p.dbg & 1)) {
 #pragma unroll
               for (int q = 0; q < 8; ++q) {
-                float4 o = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                       __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-                const float4 a0 = c.ks == 0 ? o : x[q], a1 = c.ks == 0 ? x[q] : o;  // range 0 first
-                v[4 * q] = __float_as_uint(a0.x + a1.x);
-                v[4 * q + 1] = __float_as_uint(a0.y + a1.y);
-                v[4 * q + 2] = __float_as_uint(a0.z + a1.z);
-                v[4 * q + 3] = __float_as_uint(a0.w + a1.w);
+                const float4 t = x2[q];
+                v[4 * q] = __float_as_uint(__uint_as_float(v[4 * q]) + t.x);
+                v[4 * q + 1] = __float_as_uint(__uint_as_float(v[4 * q + 1]) + t.y);
+                v[4 * q + 2] = __float_as_uint(__uint_as_float(v[4 * q + 2]) + t.z);
+                v[4 * q + 3] = __float_as_uint(__uint_as_float(v[4 * q + 3]) + t.w);
               }
-            } else if (p.S > 2) {
-              float4 acc4[8];
-              for (int k = 0; k < p.S; ++k) {
-                float4 x[8];
-                if (k == c.ks) {
+              if (sb + 1 < kPw / 32 && cb + 32 < p.bn) {  // the next block's loads, in flight while this one is staged
 #pragma unroll
-                  for (int q = 0; q < 8; ++q)
-                    x[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                       __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-                } else {
-                  const float4* src = part_t + k * k_stride + static_cast<int64_t>(cb / 4) * kBM + m;
+                for (int q = 0; q < 8; ++q) x2[q] = __ldcg(src2 + static_cast<int64_t>(8 * (sb + 1) + q) * kBM);
+              }
+            } else if (p.S > 2 && !(p.dbg & 1)) {
+              // 16 columns at a time (register budget of the 10-warp CTA)
 #pragma unroll
-                  for (int q = 0; q < 8; ++q) x[q] = __ldcg(src + static_cast<int64_t>(q) * kBM);
-                }
+              for (int h = 0; h < 2; ++h) {
+                float a[16];
+#pragma unroll 1
+                for (int k = 0; k < p.S; ++k) {
+                  float x[16];
+                  if (k == c.ks) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  if (k == 0) {
-                    acc4[q] = x[q];
+                    for (int j = 0; j < 16; ++j) x[j] = __uint_as_float(v[16 * h + j]);
                   } else {
-                    acc4[q].x += x[q].x;
-                    acc4[q].y += x[q].y;
-                    acc4[q].z += x[q].z;
-                    acc4[q].w += x[q].w;
-                  }
-                }
-              }
+                    const float4* src = part_t + k * k_stride + static_cast<int64_t>((cb + 16 * h) / 4) * kBM + m;
 #pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                v[4 * q] = __float_as_uint(acc4[q].x);
-                v[4 * q + 1] = __float_as_uint(acc4[q].y);
-                v[4 * q + 2] = __float_as_uint(acc4[q].z);
-                v[4 * q + 3] = __float_as_uint(acc4[q].w);
+                    for (int q = 0; q < 4; ++q) {
+                      const float4 t = __ldcg(src + static_cast<int64_t>(q) * kBM);
+                      x[4 * q] = t.x;
+                      x[4 * q + 1] = t.y;
+                      x[4 * q + 2] = t.z;
+                      x[4 * q + 3] = t.w;
+                    }
+                  }
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) a[j] = k == 0 ? x[j] : a[j] + x[j];
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[16 * h + j] = __float_as_uint(a[j]);
               }
             }
             if constexpr (kTF32) {  // 32 fp32 columns = the whole 128-byte row, 8 chunks
@@ -414,8 +444,8 @@ __global__ void __launch_bounds__(kWideThreads, 1)
           const int nch = chunks_left < 8 ? static_cast<int>(chunks_left) : 8;
 #pragma unroll
           for (int it = 0; it < 8; ++it) {
-            const int ci = it * 32 + lane;
-            const int r = ci >> 3, ch = ci & 7;
+            const int ci2 = it * 32 + lane;
+            const int r = ci2 >> 3, ch = ci2 & 7;
             const unsigned long long base = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(orow), r);
             const uint4 val = ptx::ld_shared_v4(stg + static_cast<uint32_t>(r * 128) +
                                                 ((static_cast<uint32_t>(ch) ^ static_cast<uint32_t>(r & 7)) << 4));
@@ -570,6 +600,7 @@ cudaError_t launch_wide_gemm(const Plan& pl, const GemmArgs& a, void* scratch, s
   p.n_tiles = g.tiles;
   p.S = g.S;
   p.apk = g.apk;
+  p.dbg = getenv("MEC_WIDE_DBG") ? atoi(getenv("MEC_WIDE_DBG")) : 0;
   p.n_units = g.tiles * g.S;
 
   p.a_bytes = static_cast<uint32_t>(kAtomA);
