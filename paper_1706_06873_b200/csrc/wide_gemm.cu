@@ -679,7 +679,18 @@ cudaError_t launch_wide_gemm(const Plan& pl, const GemmArgs& a, void* scratch, s
     if (e != cudaSuccess) return e;
   }
   // (the counters were zeroed by the lowering launch: launch_lower's zero_words)
-  const int64_t clusters = std::min<int64_t>(max_clusters, p.n_groups);
+  int64_t clusters = std::min<int64_t>(max_clusters, p.n_groups);
+  if (p.S > 1 && clusters < p.n_groups && clusters < 2 * p.S) {
+    // the split-K exchange waits on the other ranges of a tile: with fewer
+    // resident pairs than 2 S - 1 a pair could wait on a range it would only
+    // run itself later (each pair takes units in increasing order, a tile's
+    // ranges are S consecutive units) -- run unsplit
+    p.S = 1;
+    p.apk = g.n_atoms;
+    p.n_units = g.tiles;
+    p.n_groups = ((p.n_hm + p.mc - 1) / p.mc) * g.n_ng;
+    clusters = std::min<int64_t>(max_clusters, p.n_groups);
+  }
   cfg.gridDim = dim3(static_cast<unsigned>(2 * p.mc * clusters));
   cfg.numAttrs = getenv("MEC_NO_PDL") ? 1 : 2;
   e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, p);
