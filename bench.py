@@ -56,7 +56,8 @@ def parse(argv=None):
     ap.add_argument("--batch", type=int, default=None, help="override the global batch i_n")
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
                     help="strong: shard the global batch over the ranks; weak: a full batch per rank")
-    ap.add_argument("--path", choices=["auto", "A", "B", "fused"], default="auto")
+    ap.add_argument("--path", choices=["auto", "A", "B", "fused", "fastest"], default="auto",
+                    help="auto: the paper's Alg.2 l.8 choice (the headline); fastest: MEC_PATH_FASTEST")
     ap.add_argument("--sola-fix", choices=["epilogue", "literal"], default="epilogue")
     ap.add_argument("--T", type=int, default=100)
     ap.add_argument("--rows-per-tile", type=int, default=0,
@@ -319,7 +320,7 @@ def measure(args, cfg, rw, rank, ws, dev, peaks, peak_src, tf32_peak, primary=Tr
 
     import synth
     from paper_1706_06873_b200 import dist, mec
-    from paper_1706_06873_b200._lib import (MEC_PATH_AUTO, MEC_PATH_FUSED, MEC_PATH_SOLUTION_A,
+    from paper_1706_06873_b200._lib import (MEC_PATH_AUTO, MEC_PATH_FASTEST, MEC_PATH_FUSED, MEC_PATH_SOLUTION_A,
                                             MEC_PATH_SOLUTION_B, MEC_SOLA_FIX_EPILOGUE, MEC_SOLA_FIX_LITERAL,
                                             MecError)
 
@@ -334,7 +335,7 @@ def measure(args, cfg, rw, rank, ws, dev, peaks, peak_src, tf32_peak, primary=Tr
     i_n, i_h, i_w, i_c, k_h, k_w, k_c = w["shape"]
     s_h, s_w = cfg["s_h"], cfg["s_w"]
     path = {"auto": MEC_PATH_AUTO, "A": MEC_PATH_SOLUTION_A, "B": MEC_PATH_SOLUTION_B,
-            "fused": MEC_PATH_FUSED}[args.path]
+            "fused": MEC_PATH_FUSED, "fastest": MEC_PATH_FASTEST}[args.path]
     fix = MEC_SOLA_FIX_EPILOGUE if args.sola_fix == "epilogue" else MEC_SOLA_FIX_LITERAL
     K_steps = args.steps
 

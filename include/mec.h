@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define MEC_ABI_VERSION 5
+#define MEC_ABI_VERSION 6
 
 typedef enum {
   MEC_OK = 0,
@@ -67,10 +67,15 @@ typedef enum {
   MEC_PATH_AUTO = 0,       /* Alg.2 l.8: A iff o_w <= T and #O <= #L, else B */
   MEC_PATH_SOLUTION_A = 1, /* batch-folded */
   MEC_PATH_SOLUTION_B = 2, /* per-image */
-  MEC_PATH_FUSED = 3       /* lowering fused into the GEMM: each K-atom of a window tile is
+  MEC_PATH_FUSED = 3,      /* lowering fused into the GEMM: each K-atom of a window tile is
                               read as a TMA box of I, L is never written (needs i_c elt a
                               multiple of 128 B and s_w <= 2; else MEC_ERR_UNSUPPORTED).
                               Never chosen by MEC_PATH_AUTO (which follows Alg.2 l.8). */
+  MEC_PATH_FASTEST = 4     /* MEC_PATH_FUSED where its TMA-box variant runs as the h-sweep
+                              and the layer is not tensor-bound (measured faster on B200:
+                              VGG conv1_2 b64 301 vs 563 us, ResNet-50 3x3 b256 101 vs 159,
+                              cv8 / cv9 1.25-1.6x), else MEC_PATH_AUTO's choice.  Not a
+                              paper rule: the paper's path (Alg.2 l.8) is MEC_PATH_AUTO. */
 } mec_path_t;
 
 /* How Solution A reaches n-h-w-c (Alg.2 l.13-19). */

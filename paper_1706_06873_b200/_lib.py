@@ -26,6 +26,7 @@ MEC_PATH_AUTO = 0
 MEC_PATH_SOLUTION_A = 1
 MEC_PATH_SOLUTION_B = 2
 MEC_PATH_FUSED = 3
+MEC_PATH_FASTEST = 4  # fused h-sweep where measured faster, else MEC_PATH_AUTO (include/mec.h)
 # mec_sola_fix_t
 MEC_SOLA_FIX_EPILOGUE = 0
 MEC_SOLA_FIX_LITERAL = 1

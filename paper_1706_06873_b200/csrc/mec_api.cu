@@ -392,11 +392,22 @@ mec_status_t resolve(const mec_shape_t* s, int s_h, int s_w, mec_dtype_t dt, con
   mec_status_t st = make_plan(s, s_h, s_w, dt, &r->p, opt->pad_h, opt->pad_w);
   if (st != MEC_OK) return st;
   const Plan& p = r->p;
-  if (opt->path < MEC_PATH_AUTO || opt->path > MEC_PATH_FUSED) return MEC_ERR_INVALID_ARG;
+  if (opt->path < MEC_PATH_AUTO || opt->path > MEC_PATH_FASTEST) return MEC_ERR_INVALID_ARG;
   if (opt->sola_fix < MEC_SOLA_FIX_EPILOGUE || opt->sola_fix > MEC_SOLA_FIX_NONE) return MEC_ERR_INVALID_ARG;
   if (opt->rows_per_tile < 0) return MEC_ERR_INVALID_ARG;
   const int T = opt->T > 0 ? opt->T : MEC_DEFAULT_T;
   int path = opt->path;
+  if (path == MEC_PATH_FASTEST) {
+    // the fused TMA-box variant on the h-sweep, where the layer is not
+    // tensor-bound (measured faster there; the one-window and
+    // gather variants are not)
+    int nv, na, ns, stg;
+    const bool paper_wide = wide_preferred(p) && wide_eligible(p, select_path_plan(p, T) != MEC_PATH_SOLUTION_B, false);
+    const bool fused_sweep = fused_eligible(p) && !paper_wide && opt->rows_per_tile == 0 &&
+                             (opt->gemm_kernel == 0 || opt->gemm_kernel == 2) &&
+                             sweep_config(p, true, &nv, &na, &ns, &stg, false);
+    path = fused_sweep ? MEC_PATH_FUSED : MEC_PATH_AUTO;
+  }
   if (path == MEC_PATH_AUTO) path = select_path_plan(p, T);
   if (path == MEC_PATH_FUSED && !fused_eligible(p) && !gather_eligible(p)) return MEC_ERR_UNSUPPORTED;
   // Solution A's literal format fix repurposes L as auxiliary space,

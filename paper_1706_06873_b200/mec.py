@@ -15,7 +15,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import (MEC_DTYPE_BF16, MEC_DTYPE_TF32, MEC_PATH_AUTO, MEC_PATH_FUSED,  # noqa: F401
+from ._lib import (MEC_DTYPE_BF16, MEC_DTYPE_TF32, MEC_PATH_AUTO, MEC_PATH_FASTEST, MEC_PATH_FUSED,  # noqa: F401
                    MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B, MEC_SOLA_FIX_EPILOGUE,
                    MEC_SOLA_FIX_LITERAL, MEC_SOLA_FIX_NONE, MEC_DEFAULT_T, MecError)
 

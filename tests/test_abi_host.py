@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(_lib.EXPORTED)
     for s in declared:
         assert hasattr(L, s), s
-    assert L.mec_abi_version() == 5
+    assert L.mec_abi_version() == 6
 
 
 def test_status_strings():

@@ -201,6 +201,40 @@ def test_fused_path(cuda_ok, name, batch, dtype):
     assert torch.equal(OF, O2)
 
 
+# (layer, batch, dtype, the path MEC_PATH_FASTEST resolves to): the fused h-sweep on the
+# HBM-bound wide-channel layers; the paper's Alg.2 l.8 choice on the tensor-bound ones,
+# the 3-channel ones (no TMA-box fused variant) and tf32 VGG conv1_2 (window past the ring)
+FASTEST_CASES = [("vgg16_conv1_2", 2, "bf16", "fused"), ("cv9", 3, "bf16", "fused"), ("cv8", 1, "bf16", "fused"),
+                 ("cv12", 5, "bf16", "paper"), ("cv3", 2, "bf16", "paper"), ("vgg16_conv1_2", 1, "tf32", "paper")]
+
+
+@pytest.mark.parametrize("name,batch,dtype,want", FASTEST_CASES)
+def test_fastest_path(cuda_ok, name, batch, dtype, want):
+    """MEC_PATH_FASTEST: the fused path where its TMA-box h-sweep applies and the
+    layer is not tensor-bound, else MEC_PATH_AUTO's Alg.2 l.8 choice; either way
+    within tolerance of the oracle and equal to the explicitly requested path."""
+    from paper_1706_06873_b200._lib import MEC_PATH_AUTO, MEC_PATH_FASTEST, MEC_PATH_FUSED
+    if name == "vgg16_conv1_2":
+        i_h, i_w, i_c, k_h, k_w, k_c, s = 226, 226, 64, 3, 3, 64, 1
+    else:
+        i_h, i_w, i_c, k_h, k_w, k_c, s = synth.TABLE2[name]
+    shape = (batch, i_h, i_w, i_c, k_h, k_w, k_c)
+    I, K = make_inputs(shape, dtype, seed=4300 + batch + len(name))
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    O, chosen = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_FASTEST, return_path=True)
+    paper = mec.select_path(shape, s, s)
+    assert chosen == (MEC_PATH_FUSED if want == "fused" else paper)
+    O2 = mec.conv_forward(Id, Kd, s, s, path=chosen)
+    torch.cuda.synchronize()
+    check_O(O, ref, dtype, k_h * k_w * i_c)
+    assert torch.equal(O, O2)
+    if want == "paper":
+        O3 = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_AUTO)
+        torch.cuda.synchronize()
+        assert torch.equal(O, O3)
+
+
 @pytest.mark.parametrize("shape,s", [((4, 56, 56, 256, 1, 1, 64), 1), ((3, 28, 28, 192, 1, 1, 64), 1),
                                      ((2, 30, 33, 64, 3, 3, 96), 2), ((2, 17, 140, 128, 2, 3, 48), 1)])
 def test_fused_path_misc(cuda_ok, shape, s):
