@@ -123,6 +123,7 @@ struct LowerParams {
   uint32_t delta16;   // (i_w - k_w) i_c elt mod 16
   int wcls;           // column-class period 16 / gcd(wstep_b, 16)
   uint32_t raw_bytes;   // smem bytes per raw band buffer (two, double-buffered)
+  int n_raw;            // raw band buffers: 2 (persistent CTAs, next band prefetched) or 1 (one band per CTA)
   int64_t total_bands;  // i_n bands (the persistent CTAs loop over them)
   bool prep_first;      // plain path: weight-prep CTAs before the lowering CTAs (large K)
   bool prep64;          // weight prep in 64 x 64 tiles with 16-byte vectors (bf16, k_c % 8 == 0)
@@ -314,7 +315,7 @@ __device__ __forceinline__ void lower_copies(const LowerParams& p, unsigned char
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   const uint32_t s_base = ptx::smem_u32(smem);
   const uint32_t raw0 = s_base + 128 + 32;  // raw buffer b at raw0 + b raw_bytes (32 B slack before)
-  const uint32_t cps = s_base + 128 + 2 * p.raw_bytes;
+  const uint32_t cps = s_base + 128 + static_cast<uint32_t>(p.n_raw) * p.raw_bytes;
   const int64_t nb = p.total_bands;
   const int64_t b0 = cta, bstep = p.n_lower_blocks;
 #ifdef MEC_TRACE
@@ -1187,8 +1188,14 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
       // measured slower on B200 -- AlexNet conv1 22.4 vs 16.5 us, cv3 b128
       // 114 vs 63 us: the output loop is instruction-bound, not store-bound
       p.direct = getenv("MEC_LOWER_DIRECT") && atoi(getenv("MEC_LOWER_DIRECT")) != 0;
-      smem = 128 + 2 * static_cast<size_t>(p.raw_bytes) + (p.direct ? 0 : csmem);
       p.total_bands = p.n_lower_blocks;
+      // one band per CTA: one raw buffer, more CTAs per SM, the block scheduler
+      // balances (measured on B200: cv1 b128 39.5 -> 36.4 us, cv3 b128 54.7 ->
+      // 51.0, AlexNet conv1 unchanged); MEC_LOWER_ONE_BAND=0: persistent CTAs
+      // with a prefetched second band (round 1)
+      const bool one_band = !(getenv("MEC_LOWER_ONE_BAND") && atoi(getenv("MEC_LOWER_ONE_BAND")) == 0);
+      p.n_raw = one_band ? 1 : 2;
+      smem = 128 + static_cast<size_t>(p.n_raw) * p.raw_bytes + (p.direct ? 0 : csmem);
       // persistent CTAs: as many as are co-resident (each loops over bands,
       // prefetching the next band's rows while it writes the current one)
       int occ = 0;
@@ -1202,7 +1209,7 @@ cudaError_t launch_lower(const Plan& pl, const void* I, void* L, int64_t pitch, 
       // equal band counts per CTA (a ragged last round of bands left most CTAs
       // idle while a quarter of them processed a second band: measured)
       const int64_t slots = static_cast<int64_t>(occ) * num_sms();
-      const int64_t per = (p.total_bands + slots - 1) / slots;
+      const int64_t per = one_band ? 1 : (p.total_bands + slots - 1) / slots;
       p.n_lower_blocks = (p.total_bands + per - 1) / per;
     }
   }
