@@ -44,6 +44,26 @@
 #include "ptx.cuh"
 #include "tma_host.h"
 
+#ifdef MEC_TRACE
+// Debug-only cycle accounting (tools/trace_pair_sweep.py, -DMEC_TRACE build):
+// per CTA [0] MMA warp cycles waiting for a free accumulator, [1] waiting for
+// landed atoms, [2] MMA warp total, [3] producer cycles waiting for a free
+// stage, [4] producer total, [5] atoms issued, [6] rows, [7] SM id
+__device__ unsigned long long* g_ps_trace = nullptr;
+extern "C" int mec_pair_sweep_trace_enable(void** dev_buf_out, size_t* bytes_out) {
+  const size_t bytes = static_cast<size_t>(512) * 8 * 8;
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, bytes) != cudaSuccess) return 1;
+  cudaMemset(buf, 0, bytes);
+  if (cudaMemcpyToSymbol(g_ps_trace, &buf, sizeof(buf)) != cudaSuccess) return 2;
+  *dev_buf_out = buf;
+  *bytes_out = bytes;
+  return 0;
+}
+#define PS_CLK(v) const long long v = clock64()
+#define PS_ADD(acc, t0) acc += clock64() - (t0)
+#endif
+
 namespace mec {
 namespace {
 
@@ -168,6 +188,10 @@ __global__ void __launch_bounds__(kPsThreads, 1)
       }
       int stage = 0;
       uint32_t phase = 0;
+#ifdef MEC_TRACE
+      long long c_pwait = 0, n_atoms = 0;
+      const long long c_p0 = clock64();
+#endif
       for (int64_t it = pair; it < p.n_items; it += n_pairs) {
         const int64_t pt = it / p.n_hc, hc = it - pt * p.n_hc;
         const int64_t h0 = hc * p.H;
@@ -190,7 +214,13 @@ __global__ void __launch_bounds__(kPsThreads, 1)
               const int lo = jj >= p.na ? (jj - p.na) / p.sa + 1 : 0;
               bytes += p.a_bytes + (p.b_stream ? static_cast<uint32_t>(hi - lo + 1) * p.b_half_bytes : 0u);
             }
+#ifdef MEC_TRACE
+            PS_CLK(tw0);
+#endif
             ptx::mbar_wait(&empty[stage], phase ^ 1);
+#ifdef MEC_TRACE
+            PS_ADD(c_pwait, tw0);
+#endif
             if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2u * bytes);
           }
           unsigned char* dA = smem + static_cast<size_t>(stage) * p.stage_bytes + static_cast<size_t>(k) * p.slot_bytes;
@@ -206,6 +236,9 @@ __global__ void __launch_bounds__(kPsThreads, 1)
               ptx::tma_load_3d_pair(dA + s * p.slot * kTileKBytes, &tmA, fb, x, 0, static_cast<int32_t>(t.n0 + s),
                                     hintA);
           }
+#ifdef MEC_TRACE
+          ++n_atoms;
+#endif
           if (++k == kAps || j == n_stream - 1) {
             k = 0;
             if (++stage == S) {
@@ -215,6 +248,14 @@ __global__ void __launch_bounds__(kPsThreads, 1)
           }
         }
       }
+#ifdef MEC_TRACE
+      if (g_ps_trace != nullptr && blockIdx.x < 512) {
+        unsigned long long* e = g_ps_trace + static_cast<size_t>(blockIdx.x) * 8;
+        e[3] = static_cast<unsigned long long>(c_pwait);
+        e[4] = static_cast<unsigned long long>(clock64() - c_p0);
+        e[5] = static_cast<unsigned long long>(n_atoms);
+      }
+#endif
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (pair leader) =====================
@@ -224,39 +265,81 @@ __global__ void __launch_bounds__(kPsThreads, 1)
       const uint32_t a_stage16 = p.stage_bytes >> 4, b16 = p.b_half_bytes >> 4;
       const uint32_t a_to_b16 = (kBM * kTileKBytes) >> 4, slot16 = p.slot_bytes >> 4;
       if (!p.b_stream) ptx::mbar_wait(bfull, 0);
+      // Division-free bookkeeping (the MMA warp's scalar code was the limit:
+      // 80-90% of its time issuing at ~2x the MMA time per atom, trace build):
+      // the open rows r_lo..r_hi, the atom at which the next row starts and the
+      // one after which the oldest completes, and the accumulators of the
+      // oldest and the next row (rows complete in order; all rows of an item
+      // complete before the next item's first row starts)
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t row_seq = 0;  // rows started so far by this CTA pair (accumulator rotation)
+      const int sa = p.sa, na = p.na;
+      const uint32_t n_acc = static_cast<uint32_t>(p.n_acc), bn = static_cast<uint32_t>(p.bn);
+      uint32_t acc_lo = 0, acc_next = 0, tph_next = 0;
+#ifdef MEC_TRACE
+      long long c_tempty = 0, c_full = 0;
+      uint32_t rows_total = 0;
+      const long long c_m0 = clock64();
+#endif
       for (int64_t it = pair; it < p.n_items; it += n_pairs) {
         const int64_t hc = it % p.n_hc;
         const int rows = static_cast<int>(p.o_h - hc * p.H < p.H ? p.o_h - hc * p.H : p.H);
-        const int n_stream = (rows - 1) * p.sa + p.na;
+        const int n_stream = (rows - 1) * sa + na;
+#ifdef MEC_TRACE
+        rows_total += static_cast<uint32_t>(rows);
+#endif
         int k = 0;  // atom slot within the current stage
+        int r_lo = 0, r_hi = -1;
+        int next_start = 0;  // atom at which row r_hi + 1 starts
+        int lo_start = 0;    // atom at which row r_lo started (its window atom = j - lo_start)
         for (int j = 0; j < n_stream; ++j) {
-          // open rows: r sa <= j < r sa + na
-          const int r_hi = min(rows - 1, j / p.sa);
-          const int r_lo = j >= p.na ? (j - p.na) / p.sa + 1 : 0;
-          // a row starting here needs its accumulator drained (row r_hi starts iff j == r_hi sa)
-          if (j == r_hi * p.sa) {
-            const uint32_t q = row_seq + static_cast<uint32_t>(r_hi);
-            ptx::mbar_wait(&tempty[q % p.n_acc], ((q / p.n_acc) & 1u) ^ 1u);
+          if (j == next_start) {
+            if (r_hi + 1 < rows) {
+              // row r_hi + 1 starts here: its accumulator must be drained
+              ++r_hi;
+#ifdef MEC_TRACE
+              PS_CLK(t0);
+#endif
+              ptx::mbar_wait(&tempty[acc_next], tph_next ^ 1u);
+#ifdef MEC_TRACE
+              PS_ADD(c_tempty, t0);
+#endif
+              if (++acc_next == n_acc) {
+                acc_next = 0;
+                tph_next ^= 1u;
+              }
+            }
+            next_start += sa;
           }
+#ifdef MEC_TRACE
+          PS_CLK(t1);
+#endif
           if (k == 0) ptx::mbar_wait(&full[stage], phase);
+#ifdef MEC_TRACE
+          PS_ADD(c_full, t1);
+#endif
           ptx::tc_fence_after();
           const uint64_t ad = adesc0 + static_cast<uint32_t>(stage) * a_stage16 + static_cast<uint32_t>(k) * slot16;
+          // rows r_lo..r_hi: window atom a = j - r sa, accumulator acc_lo + (r - r_lo);
+          // weights: the atom slot's weight part r - r_lo (streamed) or resident atom a
+          int a = j - lo_start;
+          uint32_t acc = acc_lo;
+          uint64_t bd = p.b_stream ? ad + a_to_b16 : bdesc0 + static_cast<uint32_t>(a) * b16;
+          const int64_t bstep = p.b_stream ? static_cast<int64_t>(b16) : -static_cast<int64_t>(sa) * b16;
           for (int r = r_lo; r <= r_hi; ++r) {
-            const int a = j - r * p.sa;  // the row's window atom
-            const uint32_t q = row_seq + static_cast<uint32_t>(r);
-            // weights: resident atom a, or the atom slot's weight part r - r_lo
-            const uint64_t bd = p.b_stream ? ad + a_to_b16 + static_cast<uint32_t>(r - r_lo) * b16
-                                           : bdesc0 + static_cast<uint32_t>(a) * b16;
-            ptx::mma_ss_atom_pair_elect<kTF32>(tmem_base + (q % p.n_acc) * static_cast<uint32_t>(p.bn), ad, bd,
-                                               p.idesc, a != 0 ? 1u : 0u);
+            ptx::mma_ss_atom_pair_elect<kTF32>(tmem_base + acc * bn, ad, bd, p.idesc, a != 0 ? 1u : 0u);
+            if (++acc == n_acc) acc = 0;
+            a -= sa;
+            bd += static_cast<uint64_t>(bstep);
           }
           const bool stage_end = ++k == kAps || j == n_stream - 1;
           if (stage_end) ptx::mma_commit_pair_elect(&empty[stage], 0x3);  // one release per stage of aps atoms
-          if (j - r_lo * p.sa == p.na - 1)  // the oldest open row is complete
-            ptx::mma_commit_pair_elect(&tfull[(row_seq + static_cast<uint32_t>(r_lo)) % p.n_acc], 0x3);
+          if (j - lo_start == na - 1) {  // the oldest open row is complete
+            ptx::mma_commit_pair_elect(&tfull[acc_lo], 0x3);
+            ++r_lo;
+            lo_start += sa;
+            if (++acc_lo == n_acc) acc_lo = 0;
+          }
           __syncwarp();
           if (stage_end) {
             k = 0;
@@ -266,8 +349,19 @@ __global__ void __launch_bounds__(kPsThreads, 1)
             }
           }
         }
-        row_seq += static_cast<uint32_t>(rows);
       }
+#ifdef MEC_TRACE
+      if (lane == 0 && g_ps_trace != nullptr && blockIdx.x < 512) {
+        unsigned long long* e = g_ps_trace + static_cast<size_t>(blockIdx.x) * 8;
+        e[0] = static_cast<unsigned long long>(c_tempty);
+        e[1] = static_cast<unsigned long long>(c_full);
+        e[2] = static_cast<unsigned long long>(clock64() - c_m0);
+        e[6] = rows_total;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        e[7] = smid;
+      }
+#endif
     }
   } else {
     // ===================== epilogue (warps 2..9: two groups, alternate rows) =====================
