@@ -408,6 +408,46 @@ __global__ void __launch_bounds__(kPsThreads, 1)
         }
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                static_cast<uint32_t>(acc * p.bn);
+        if (!kTF32 && p.bn == 128 && cols_left >= 128) {
+          // bf16, N = 128 (cv8): the whole row out of TMEM first, packed to
+          // bf16 (64 registers), then the accumulator is released BEFORE the
+          // stores -- with 4 accumulators for 3 open rows the MMA warp waited
+          // a third of its time for a drained one (trace build)
+          uint32_t pk[64];
+#pragma unroll
+          for (int cb = 0; cb < 128; cb += 32) {
+            uint32_t v[32];
+            ptx::tmem_ld_32x32b_x16(taddr + cb, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+            ptx::tmem_ld_32x32b_x16(taddr + cb + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pk[cb / 2 + e] = pack_bf16x2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(tempty0 + static_cast<uint32_t>(acc) * 8u);
+#pragma unroll
+          for (int c0 = 0; c0 < 128; c0 += kPw) {
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+              const uint32_t* w4 = &pk[c0 / 2 + 4 * ch];
+              ptx::st_shared_v4(my_row_s + ((static_cast<uint32_t>(ch) ^ my_x) << 4), w4[0], w4[1], w4[2], w4[3]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i2 = 0; i2 < 8; ++i2) {
+              const int ci = i2 * 32 + lane;
+              const int rr = ci >> 3, ch = ci & 7;
+              const unsigned long long base = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(orow), rr);
+              const uint4 val = ptx::ld_shared_v4(stg + static_cast<uint32_t>(rr * 128) +
+                                                  ((static_cast<uint32_t>(ch) ^ static_cast<uint32_t>(rr & 7)) << 4));
+              if (base != 0ull)
+                *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(base) + c0 * kOutElt + ch * 16) = val;
+            }
+            __syncwarp();
+          }
+          continue;
+        }
         for (int c0 = 0; c0 < p.bn && c0 < cols_left; c0 += kPw) {
 #pragma unroll
           for (int sb = 0; sb < kPw / 32; ++sb) {
