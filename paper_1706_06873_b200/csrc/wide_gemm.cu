@@ -82,6 +82,7 @@ struct WideParams {
   int n_atoms;     // K atoms per window
   int S, apk;      // split count, atoms per split
   int64_t n_tiles, n_units;
+  int64_t g_full;  // unit groups run as whole tiles before the split ones (0: every tile split S ways)
   // pairs per cluster sharing one multicast of the weights (mc, 1 or 2): a
   // cluster works on `mc` (h, 256-row) tiles of the same N group and K range
   int mc;
@@ -100,14 +101,26 @@ struct WideParams {
 struct Unit {
   int64_t h, mt, tile;
   int ng, ks, a0, a1;
+  int nsplit;  // K ranges of this unit's tile (1: whole tile; p.S: a split tile)
   bool valid;  // false: a cluster's extra pair past the last tile (computes, stores nothing)
 };
 
 // unit group G (one per cluster iteration) -> the unit of pair pp of the cluster
 __device__ __forceinline__ Unit decode_unit(const WideParams& p, int64_t G, int pp) {
   Unit c;
-  const int64_t g2 = G / p.S;
-  c.ks = static_cast<int>(G - g2 * p.S);
+  // the first g_full unit groups are whole tiles (hybrid split: whole waves
+  // of unsplit tiles, then the last partial wave's tiles in p.S ranges)
+  int64_t g2;
+  if (G < p.g_full) {
+    g2 = G;
+    c.ks = 0;
+    c.nsplit = 1;
+  } else {
+    const int64_t gt = (G - p.g_full) / p.S;
+    c.ks = static_cast<int>(G - p.g_full - gt * p.S);
+    g2 = p.g_full + gt;
+    c.nsplit = p.S;
+  }
   // K range fastest, then the N group, then the (h, 256-row tile) combo: the
   // pairs in flight share A windows (same rows, neighbouring h) in L2
   const int64_t hmg = g2 / p.n_ng;
@@ -118,8 +131,8 @@ __device__ __forceinline__ Unit decode_unit(const WideParams& p, int64_t G, int 
   c.h = hm % p.o_h;
   c.mt = hm / p.o_h;
   c.tile = hm * p.n_ng + c.ng;
-  c.a0 = c.ks * p.apk;
-  c.a1 = min(p.n_atoms, c.a0 + p.apk);
+  c.a0 = c.nsplit == 1 ? 0 : c.ks * p.apk;
+  c.a1 = c.nsplit == 1 ? p.n_atoms : min(p.n_atoms, c.a0 + p.apk);
   return c;
 }
 
@@ -319,11 +332,11 @@ __global__ void __launch_bounds__(kWideThreads, 1)
       // output chunks of kPw columns; with split-K, range k owns (reduces and
       // stores) the chunks ci with ci S / n_oc == k and hands the others over
       const int n_oc = (p.bn + kPw - 1) / kPw;  // (bn a multiple of 32: the last chunk may be half)
-      if (p.S > 1 && c.valid) {
+      if (c.nsplit > 1 && c.valid) {
         float4* mine = const_cast<float4*>(part_t) + c.ks * k_stride;
 #pragma unroll 1
         for (int ci = 0; ci < n_oc && !(p.dbg & 2); ++ci) {
-          if (ci * p.S / n_oc == c.ks) continue;  // own chunk: stays in TMEM
+          if (ci * c.nsplit / n_oc == c.ks) continue;  // own chunk: stays in TMEM
 #pragma unroll
           for (int h16 = 0; h16 < kPw / 16; ++h16) {
             const int c0 = ci * kPw + 16 * h16;
@@ -346,11 +359,11 @@ __global__ void __launch_bounds__(kWideThreads, 1)
         uint32_t* cnt = &p.cnt[(((c.tile * 2 + rank) * 4 + quarter) * p.n_sub) + sub];
         if (lane == 0) atomicAdd(cnt, 1u);
         bool owns = false;  // (S > n_oc: some ranges own no chunk)
-        for (int ci = 0; ci < n_oc; ++ci) owns = owns || ci * p.S / n_oc == c.ks;
+        for (int ci = 0; ci < n_oc; ++ci) owns = owns || ci * c.nsplit / n_oc == c.ks;
         store = store && owns;
         if (store) {
           if (lane == 0 && !(p.dbg & 1))
-            while (ptx::ld_relaxed_gpu_u32(cnt) < static_cast<uint32_t>(p.S)) __nanosleep(64);
+            while (ptx::ld_relaxed_gpu_u32(cnt) < static_cast<uint32_t>(c.nsplit)) __nanosleep(64);
           __syncwarp();
           __threadfence();  // (acquire: the other ranges' partials are read after this)
         }
@@ -358,14 +371,14 @@ __global__ void __launch_bounds__(kWideThreads, 1)
       if (store) {
 #pragma unroll 1
         for (int ci = 0; ci < n_oc && ci * kPw < cols_left; ++ci) {
-          if (p.S > 1 && ci * p.S / n_oc != c.ks) continue;
+          if (c.nsplit > 1 && ci * c.nsplit / n_oc != c.ks) continue;
           const int c0 = ci * kPw;
           // split-K, S = 2: the other range's partial, 32 columns (8 loads per
           // thread) in flight ahead of the block being summed (fp32 addition
           // commutes: own + other is the range-order sum)
           const float4* src2 = part_t + (1 - c.ks) * k_stride + static_cast<int64_t>(c0 / 4) * kBM + m;
           float4 x2[8];
-          if (p.S == 2 && !(p.dbg & 1)) {
+          if (c.nsplit == 2 && !(p.dbg & 1)) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) x2[q] = __ldcg(src2 + static_cast<int64_t>(q) * kBM);
           }
@@ -379,7 +392,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
             ptx::tmem_ld_32x32b_x16(taddr + cb, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
             ptx::tmem_ld_32x32b_x16(taddr + cb + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
             ptx::tmem_ld_wait();
-            if (p.S == 2 && !(p.dbg & 1)) {
+            if (c.nsplit == 2 && !(p.dbg & 1)) {
 #pragma unroll
               for (int q = 0; q < 8; ++q) {
                 const float4 t = x2[q];
@@ -392,13 +405,13 @@ __global__ void __launch_bounds__(kWideThreads, 1)
 #pragma unroll
                 for (int q = 0; q < 8; ++q) x2[q] = __ldcg(src2 + static_cast<int64_t>(8 * (sb + 1) + q) * kBM);
               }
-            } else if (p.S > 2 && !(p.dbg & 1)) {
+            } else if (c.nsplit > 2 && !(p.dbg & 1)) {
               // 16 columns at a time (register budget of the 10-warp CTA)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 float a[16];
 #pragma unroll 1
-                for (int k = 0; k < p.S; ++k) {
+                for (int k = 0; k < c.nsplit; ++k) {
                   float x[16];
                   if (k == c.ks) {
 #pragma unroll
@@ -473,6 +486,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
 struct WideGeo {
   int n_sub, n_ng, n_atoms, S, apk;
   int64_t n_mt, tiles;
+  int64_t g_full;  // hybrid split: tiles run whole (whole waves) before the split ones
   size_t cnt_words, cnt_bytes, part_bytes;
 };
 
@@ -492,6 +506,7 @@ WideGeo wide_geo(const Plan& pl, int split) {
   // the pair count is the SM count / 2 here, at plan time and at launch alike,
   // so the workspace sized by the plan always fits the launch
   const int64_t n_pairs = std::max(1, num_sms() / 2);
+  g.g_full = 0;
   if (split > 0) {
     g.S = std::min(split, g.n_atoms);
   } else {
@@ -511,7 +526,30 @@ WideGeo wide_geo(const Plan& pl, int split) {
         g.S = s;
       }
     }
-    if (const char* e = getenv("MEC_WIDE_SPLIT")) g.S = std::max(1, std::min(g.n_atoms, atoi(e)));
+    // hybrid: the whole waves of tiles unsplit, the last partial wave's r
+    // tiles split into floor(n_pairs / r) ranges (one wave of ranges, each
+    // pair at most one): the last wave's time drops from a tile's atoms to a
+    // range's, for one exchange (cv12 b128 measured ~3 us ~ 8 atom-times)
+    g.g_full = 0;
+    const int64_t full = g.tiles / n_pairs * n_pairs, r = g.tiles - full;
+    if (full > 0 && r > 0) {
+      const int st = static_cast<int>(std::min<int64_t>({kMaxSplit, n_pairs / r, std::max(1, g.n_atoms / 4)}));
+      if (st >= 2) {
+        const int a = (g.n_atoms + st - 1) / st;
+        const double t = static_cast<double>(full / n_pairs) * (g.n_atoms * g.n_sub + 3.0) + (a * g.n_sub + 3.0) +
+                         (4.0 + 2.0 * st) * g.n_sub;
+        bool use = t < best_t - 1e-9;
+        if (const char* e = getenv("MEC_WIDE_HYBRID")) use = atoi(e) != 0;
+        if (use) {
+          g.S = st;
+          g.g_full = full;
+        }
+      }
+    }
+    if (const char* e = getenv("MEC_WIDE_SPLIT")) {
+      g.S = std::max(1, std::min(g.n_atoms, atoi(e)));
+      g.g_full = 0;
+    }
   }
   g.apk = (g.n_atoms + g.S - 1) / g.S;
   g.S = (g.n_atoms + g.apk - 1) / g.apk;  // no empty ranges
@@ -601,7 +639,8 @@ cudaError_t launch_wide_gemm(const Plan& pl, const GemmArgs& a, void* scratch, s
   p.S = g.S;
   p.apk = g.apk;
   p.dbg = getenv("MEC_WIDE_DBG") ? atoi(getenv("MEC_WIDE_DBG")) : 0;
-  p.n_units = g.tiles * g.S;
+  p.g_full = g.g_full;
+  p.n_units = g.g_full + (g.tiles - g.g_full) * g.S;
 
   p.a_bytes = static_cast<uint32_t>(kAtomA);
   p.b_half_bytes = static_cast<uint32_t>(pl.bn / 2 * kTileKBytes);
@@ -623,9 +662,10 @@ cudaError_t launch_wide_gemm(const Plan& pl, const GemmArgs& a, void* scratch, s
   p.mc = 1;
   // (one weight copy: the pairs of a cluster may work on different h, whose
   // window alignment would otherwise pick different shifted copies)
-  if (const char* e = getenv("MEC_WIDE_MC")) p.mc = (atoi(e) == 2 && !p.b_mn && pl.n_var == 1) ? 2 : 1;
+  if (const char* e = getenv("MEC_WIDE_MC"))
+    p.mc = (atoi(e) == 2 && !p.b_mn && pl.n_var == 1 && g.g_full == 0) ? 2 : 1;
   p.n_hm = pl.o_h * g.n_mt;
-  p.n_groups = ((p.n_hm + p.mc - 1) / p.mc) * g.n_ng * g.S;
+  p.n_groups = p.g_full + (((p.n_hm + p.mc - 1) / p.mc) * g.n_ng - p.g_full) * g.S;
   p.chunk_n = kTileKBytes / pl.elt;
   p.b_chunks = p.b_mn ? (pl.bn / 2) / p.chunk_n : 0;
   p.b_chunk_bytes = static_cast<uint32_t>(kTileKBytes * pl.bk);                 // 128 B x bk K rows
@@ -680,7 +720,19 @@ cudaError_t launch_wide_gemm(const Plan& pl, const GemmArgs& a, void* scratch, s
   }
   // (the counters were zeroed by the lowering launch: launch_lower's zero_words)
   int64_t clusters = std::min<int64_t>(max_clusters, p.n_groups);
-  if (p.S > 1 && clusters < p.n_groups && clusters < 2 * p.S) {
+  // hybrid split: the split ranges must form one wave of resident pairs
+  // (g_full whole waves before them): else run the plain split model's way
+  const bool hybrid_ok = p.g_full > 0 && clusters == std::max(1, num_sms() / 2) && p.g_full % clusters == 0 &&
+                         p.n_groups - p.g_full <= clusters;
+  if (p.g_full > 0 && !hybrid_ok) {
+    p.g_full = 0;
+    p.S = 1;
+    p.apk = g.n_atoms;
+    p.n_units = g.tiles;
+    p.n_groups = ((p.n_hm + p.mc - 1) / p.mc) * g.n_ng;
+    clusters = std::min<int64_t>(max_clusters, p.n_groups);
+  }
+  if (p.S > 1 && p.g_full == 0 && clusters < p.n_groups && clusters < 2 * p.S) {
     // the split-K exchange waits on the other ranges of a tile: with fewer
     // resident pairs than 2 S - 1 a pair could wait on a range it would only
     // run itself later (each pair takes units in increasing order, a tile's

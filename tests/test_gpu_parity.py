@@ -844,6 +844,35 @@ def test_wide_pair_kernel(cuda_ok, name, batch, split, dtype):
         assert torch.equal(O, O1)
 
 
+@pytest.mark.parametrize("name,batch,forced", [("cv6", 128, None), ("cv11", 136, "1"), ("cv5", 48, "1")])
+def test_wide_pair_kernel_hybrid_split(cuda_ok, monkeypatch, name, batch, forced):
+    """Hybrid split: whole waves of unsplit pair tiles, then the
+    last partial wave's tiles in S ranges that exchange partials (cv6 b128: 100
+    tiles on 74 pairs, S = 2 by the cost model; cv11 b136: 84 tiles, S = 7 forced;
+    cv5 b48: 80 tiles, S = 8 forced).  Sampled images against the oracle,
+    deterministic run to run."""
+    if forced is not None:
+        monkeypatch.setenv("MEC_WIDE_HYBRID", forced)
+    i_h, i_w, i_c, k_h, k_w, k_c, s = synth.TABLE2[name]
+    shape = (batch, i_h, i_w, i_c, k_h, k_w, k_c)
+    seed = 6200 + batch
+    Id = torch.empty(shape[:4], dtype=torch.bfloat16, device="cuda")
+    Kd = torch.empty((k_h, k_w, i_c, k_c), dtype=torch.bfloat16, device="cuda")
+    mec.synth_fill(Id, seed, synth.TENSOR_I, synth.KIND_GRID8)
+    mec.synth_fill(Kd, seed, synth.TENSOR_K, synth.KIND_GRID8)
+    O, g, used = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_SOLUTION_A, return_gemm=True, return_split=True)
+    O2 = mec.conv_forward(Id, Kd, s, s, path=MEC_PATH_SOLUTION_A)
+    torch.cuda.synchronize()
+    assert g == 3 and used >= 2, (g, used)
+    assert torch.equal(O, O2)
+    cfg = dict(i_h=i_h, i_w=i_w, i_c=i_c, k_h=k_h, k_w=k_w, k_c=k_c)
+    K = synth.kernel_tensor(cfg, synth.KIND_GRID8, seed)
+    for n in (0, batch // 2, batch - 1):
+        I = synth.input_images(cfg, n, 1, synth.KIND_GRID8, seed)
+        ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+        check_O(O[n:n + 1], ref, "bf16", k_h * k_w * i_c)
+
+
 def test_wide_pair_kernel_refuses_other_layouts(cuda_ok):
     """Forced CTA-pair kernel where it does not apply (per-image tiles of Solution B,
     k_c not a multiple of 32): MEC_ERR_UNSUPPORTED, not a silent fallback."""

@@ -18,7 +18,7 @@ tdt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
 I = torch.empty((cfg["i_n"], cfg["i_h"], cfg["i_w"], cfg["i_c"]), dtype=tdt, device="cuda")
 K = torch.empty((cfg["k_h"], cfg["k_w"], cfg["i_c"], cfg["k_c"]), dtype=tdt, device="cuda")
 mec.synth_fill(I, 1, 0, 0); mec.synth_fill(K, 1, 1, 0)
-path = {"auto": 0, "A": 1, "B": 2}[args.path]
+path = {"auto": 0, "A": 1, "B": 2, "fused": 3}[args.path]
 for _ in range(3): mec.conv_forward(I, K, cfg["s_h"], cfg["s_w"], path=path)
 torch.cuda.synchronize()
 buf = ctypes.c_void_p(); nbytes = ctypes.c_size_t()
