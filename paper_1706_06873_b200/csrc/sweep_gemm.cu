@@ -131,6 +131,11 @@ struct SweepParams {
   int bn;
   int H;           // output rows of the largest work item (chunks differ by <= 1 row)
   int64_t n_hc, n_items;
+  // balanced split (bal_G > 0): CTA c owns rows [c R / G, (c + 1) R / G) of
+  // the flattened (tile, h) sequence (R = n_tiles o_h), cut at tile
+  // boundaries into at most bal_J items; item t = c + j G is piece j of CTA c
+  int64_t bal_R;
+  int bal_G, bal_J;
   int stages;      // shared-memory A stages (one atom each)
   int ns;          // TMEM A ring slots (32 columns each)
   int n_acc;       // TMEM accumulators (bn columns each)
@@ -169,6 +174,19 @@ struct SwItem {
 __device__ __forceinline__ SwItem sw_decode(const SweepParams& p, int64_t t, bool pair = false,
                                            uint32_t rank = 0) {
   SwItem it;
+  if (!pair && p.bal_G > 0) {
+    const int64_t c = t % p.bal_G, j = t / p.bal_G;
+    const int64_t s = c * p.bal_R / p.bal_G, e = (c + 1) * p.bal_R / p.bal_G;
+    const int64_t tile0 = s / p.o_h;
+    const int64_t start = j == 0 ? s : (tile0 + j) * p.o_h;
+    const int64_t end = min(e, (tile0 + j + 1) * p.o_h);
+    it.valid = true;
+    const int64_t tl = start < end ? start / p.o_h : tile0;
+    it.mt = tl % p.n_mt;
+    it.g = tl / p.n_mt;
+    it.h0 = start < end ? start - tl * p.o_h : 0;
+    it.nrows = start < end ? static_cast<int>(end - start) : 0;
+  } else {
   const int64_t hc = t % p.n_hc;
   t /= p.n_hc;
   if (pair) t = 2 * t + rank;  // pair tile -> this CTA's tile
@@ -179,9 +197,14 @@ __device__ __forceinline__ SwItem sw_decode(const SweepParams& p, int64_t t, boo
   // chunk hc: rows [hc o_h / n_hc, (hc + 1) o_h / n_hc) (sizes differ by <= 1)
   it.h0 = hc * p.o_h / p.n_hc;
   it.nrows = static_cast<int>((hc + 1) * p.o_h / p.n_hc - it.h0);
+  }
   const int64_t xs = it.h0 * p.shift;
   it.x0 = static_cast<int>(xs - xs % p.avec);
   it.off0 = static_cast<int>(xs - it.x0);
+  if (it.nrows == 0) {  // (an empty piece of a balanced split: no atoms, no rows)
+    it.n_a = 0;
+    return it;
+  }
   // the last row's last K step bounds the stream
   const int o_last = it.off0 + (it.nrows - 1) * p.shift;
   const int d_last = o_last & (p.mvec - 1);
@@ -1093,13 +1116,51 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
       best_n = n_hc;
     }
   }
+  // balanced split (not CTA pairs): one CTA per SM, each the same number of
+  // (tile, h) rows, cut at tile boundaries, where the chunked items above
+  // leave SMs idle (C3, cv1-cv3, cv9 at b128: 128 tiles of one chunk for 148
+  // SMs) and the cost model (a CTA's pieces' streams + rows + fills) agrees.
+  // Measured (profiles/r2_sweep_balanced.txt): C3 GEMM 92.3 -> 86.2 us, cv3
+  // b128 90.5 -> 82.5; C1 (two fills per ~6-row CTA) and C2 (chip-wide
+  // DRAM-bound, every SM already busy) gain nothing and keep the chunks.
+  bool balanced = false;
+  int64_t bal_G = 0, bal_J = 0;
+  const int64_t R = tiles * pl.o_h;
+  if (!pair && R >= sms && best_n * work_tiles < sms) {
+    bal_G = sms;
+    const int64_t per = (R + bal_G - 1) / bal_G;
+    bal_J = (per + pl.o_h - 1) / pl.o_h + 1;
+    double worst = 0.0;
+    for (int64_t c = 0; c < bal_G; ++c) {
+      const int64_t s0 = c * R / bal_G, e0 = (c + 1) * R / bal_G;
+      double cost = 0.0;
+      for (int64_t pos = s0; pos < e0;) {
+        const int64_t end = std::min(e0, (pos / pl.o_h + 1) * pl.o_h);
+        const int64_t H = end - pos;
+        const double atoms = static_cast<double>((H - 1) * pl.shift + pl.kdim + pl.avec) / pl.bk + 1.0;
+        cost += atoms * kSwAtomBytes + H * o_row_bytes + 4.0 * kSwAtomBytes;
+        pos = end;
+      }
+      worst = std::max(worst, cost);
+    }
+    balanced = worst < best * 0.999;
+    if (const char* e = getenv("MEC_SWEEP_BALANCED")) balanced = atoi(e) != 0;
+  }
   if (const char* e = getenv("MEC_SWEEP_H")) {
     best_H = std::max<int64_t>(1, std::min<int64_t>(pl.o_h, atoi(e)));
     best_n = (pl.o_h + best_H - 1) / best_H;
+    balanced = false;
   }
   p.H = static_cast<int>(best_H);
   p.n_hc = best_n;
   p.n_items = p.n_hc * work_tiles;
+  if (balanced) {
+    p.bal_R = R;
+    p.bal_G = static_cast<int>(bal_G);
+    p.bal_J = static_cast<int>(bal_J);
+    p.n_items = bal_G * bal_J;
+    p.H = static_cast<int>(std::min<int64_t>(pl.o_h, (R + bal_G - 1) / bal_G));
+  }
 
   const size_t b_res = static_cast<size_t>(n_vres) * p.nb_atoms * (pair ? pl.bn / 2 : pl.bn) * kTileKBytes;
   const size_t smem = kSmemAlign + static_cast<size_t>(stages) * kSwAtomBytes + b_res +

@@ -20,7 +20,7 @@ import torch
 import oracle
 import synth
 from paper_1706_06873_b200 import mec
-from paper_1706_06873_b200._lib import (MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B, MEC_SOLA_FIX_EPILOGUE,
+from paper_1706_06873_b200._lib import (MEC_PATH_FUSED, MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B, MEC_SOLA_FIX_EPILOGUE,
                                         MEC_SOLA_FIX_LITERAL, MEC_SOLA_FIX_NONE, MecError)
 
 pytestmark = pytest.mark.gpu
@@ -172,7 +172,9 @@ def test_multi_row_tiles(cuda_ok, name, batch, rpt, dtype):
     ref = oracle.direct_conv(I, K, s, s, n_threads=8)
     Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
     for path in (MEC_PATH_SOLUTION_A, MEC_PATH_SOLUTION_B):
-        O1 = mec.conv_forward(Id, Kd, s, s, path=path)
+        # (the one-row schedule of the same kernel: the automatic choice may be
+        # the CTA-pair kernel, whose split-K regroups the sums)
+        O1 = mec.conv_forward(Id, Kd, s, s, path=path, gemm_kernel=1)
         OR = mec.conv_forward(Id, Kd, s, s, path=path, rows_per_tile=rpt)
         torch.cuda.synchronize()
         check_O(OR, ref, dtype, k_h * k_w * i_c)
@@ -811,6 +813,49 @@ def test_non_finite_input_documented_behaviour(cuda_ok, path):
     bar = tol("tf32", 72, np.where(nan_ref, 0.0, ref))
     assert np.abs(got[fin] - ref[fin]).max() <= bar
     assert not np.any(nan_got[0])  # the other image is untouched
+
+
+BAL_CASES = [
+    # (name or shape, batch / stride, path)
+    (("cv9", 8), MEC_PATH_SOLUTION_A),     # 4 tiles x 54 rows on 148 CTAs: 1-2 rows each, pieces across tiles
+    (("cv1", 6), MEC_PATH_SOLUTION_A),     # AlexNet conv1 rows (2 weight variants), 3 tiles
+    (("cv3", 3), MEC_PATH_SOLUTION_B),     # 7x7 s2, per-image tiles
+    (((3, 30, 230, 64, 3, 3, 64), 1), MEC_PATH_SOLUTION_B),  # o_w 228: 2 CTA tiles per image
+    (((3, 30, 230, 64, 3, 3, 64), 1), MEC_PATH_FUSED),       # the fused TMA-box variant
+]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("case", range(len(BAL_CASES)))
+def test_sweep_balanced_split(cuda_ok, monkeypatch, case, dtype):
+    """The h-sweep's balanced split (every CTA the same number of (tile, h) rows,
+    cut at tile boundaries) against the chunked items: the same
+    K steps per row, so bit for bit, and the oracle within tolerance."""
+    (what, b), path = BAL_CASES[case]
+    if isinstance(what, str):
+        i_h, i_w, i_c, k_h, k_w, k_c, s = synth.TABLE2[what]
+        shape = (b, i_h, i_w, i_c, k_h, k_w, k_c)
+    else:
+        shape, s = what, b
+    if path == MEC_PATH_FUSED and dtype == "tf32":
+        pytest.skip("fused TMA-box variant: bf16 case is enough here")
+    I, K = make_inputs(shape, dtype, seed=6300 + case)
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    outs = []
+    for bal in ("1", "0"):
+        monkeypatch.setenv("MEC_SWEEP_BALANCED", bal)
+        try:
+            O, g = mec.conv_forward(Id, Kd, s, s, path=path, gemm_kernel=2, return_gemm=True)
+        except MecError:
+            if dtype == "tf32":  # (a tf32 window wider than the TMEM ring: no h-sweep)
+                pytest.skip("h-sweep does not apply to this tf32 window")
+            raise
+        torch.cuda.synchronize()
+        assert g == 2
+        outs.append(O)
+    check_O(outs[0], ref, dtype, shape[4] * shape[5] * shape[3])
+    assert torch.equal(outs[0], outs[1])
 
 
 # ------------------------------- the CTA-pair (cta_group::2) split-K kernel
