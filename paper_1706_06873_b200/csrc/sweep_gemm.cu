@@ -461,6 +461,16 @@ __global__ void __launch_bounds__(kSwThreads, 1)
         const SwItem it = sw_decode(p, t, kPair, rank);
         const int32_t y0 = static_cast<int32_t>(it.mt * kBM);
         const int32_t z0 = static_cast<int32_t>(it.g);
+        // fused: L column x -> input row hh, kernel column b, channel block cb,
+        // advanced by one atom (bk channels; i_c is a multiple of bk) per step
+        // -- no divisions on the per-atom path
+        int f_hh = 0, f_b = 0, f_cb = 0;
+        if (p.fused) {
+          f_hh = it.x0 / p.kwc;
+          const int rem = it.x0 - f_hh * p.kwc;
+          f_b = rem / p.i_c;
+          f_cb = rem - f_b * p.i_c;
+        }
         for (int i = 0; i < it.n_a; ++i, ++pseq) {
           if (pseq < 100) SW_TRACE(300u + pseq, 0);
           ptx::mbar_wait(&empty[stage], pphase ^ 1u);
@@ -470,8 +480,14 @@ __global__ void __launch_bounds__(kSwThreads, 1)
           const int32_t x = it.x0 + i * p.bk;
           if (p.fused) {
             // L column x -> input row hh, kernel column b, channel block cb
-            const int hh = x / p.kwc, rem = x - hh * p.kwc;
-            const int b = rem / p.i_c, cb = rem - b * p.i_c;
+            const int hh = f_hh, b = f_b, cb = f_cb;
+            if ((f_cb += p.bk) == p.i_c) {
+              f_cb = 0;
+              if (++f_b == p.kwc / p.i_c) {
+                f_b = 0;
+                ++f_hh;
+              }
+            }
             const int32_t zy = hh - p.pad_h;  // (padding: TMA zero-fills out-of-bounds pixels and rows)
             if (p.ipt <= 1) {
               ptx::tma_load_4d(dstA, &tmA, &full[stage], cb, y0 * p.s_w + b - p.pad_w, zy, z0, hintA);
