@@ -7,7 +7,7 @@ cd "$(dirname "$0")/.."
 cp gpurun_out/bench_default.json profiles/${T}_bench_default.json
 cp gpurun_out/bench_ref.json profiles/${T}_bench_ref.json
 cp gpurun_out/bench_cfgs.json profiles/${T}_bench_cfgs.json
-for t in memcheck racecheck synccheck; do [ -f gpurun_out/sanitize_$t.log ] && cp gpurun_out/sanitize_$t.log profiles/${T}_sanitize_$t.log; done
+for t in memcheck racecheck synccheck; do [ -f gpurun_out/sanitize_$t.log ] && ! grep -q "is closed on this pool" gpurun_out/sanitize_$t.log && cp gpurun_out/sanitize_$t.log profiles/${T}_sanitize_$t.log; done
 python tools/profile_summary.py --launches gpurun_out/launches_c2.csv --config C2_vgg16_conv1_2 --tag $T
 python tools/profile_summary.py --launches gpurun_out/launches_c2_tf32.csv --config C2_vgg16_conv1_2_tf32 --tag $T
 declare -A NAME=([C2]=C2_vgg16_conv1_2 [C2_tf32]=C2_vgg16_conv1_2_tf32 [C1]=C1_alexnet_conv1
