@@ -187,20 +187,26 @@ __device__ __forceinline__ SwItem sw_decode(const SweepParams& p, int64_t t, boo
     it.h0 = start < end ? start - tl * p.o_h : 0;
     it.nrows = start < end ? static_cast<int>(end - start) : 0;
   } else {
-  const int64_t hc = t % p.n_hc;
-  t /= p.n_hc;
-  if (pair) t = 2 * t + rank;  // pair tile -> this CTA's tile
-  it.valid = t < p.n_tiles;
-  if (!it.valid) t = p.n_tiles - 1;  // (a real tile's coordinates; nothing is stored)
-  it.mt = t % p.n_mt;
-  it.g = t / p.n_mt;
+  // 32-bit index math (items, tiles and rows all fit; 64-bit divisions cost
+  // every role ~1 us per item before its first atom, trace build on C1)
+  uint32_t tt = static_cast<uint32_t>(t);
+  const uint32_t n_hc = static_cast<uint32_t>(p.n_hc), o_h = static_cast<uint32_t>(p.o_h);
+  const uint32_t hc = tt % n_hc;
+  tt /= n_hc;
+  if (pair) tt = 2 * tt + rank;  // pair tile -> this CTA's tile
+  it.valid = tt < static_cast<uint32_t>(p.n_tiles);
+  if (!it.valid) tt = static_cast<uint32_t>(p.n_tiles) - 1;  // (a real tile's coordinates; nothing is stored)
+  const uint32_t n_mt = static_cast<uint32_t>(p.n_mt);
+  it.mt = tt % n_mt;
+  it.g = tt / n_mt;
   // chunk hc: rows [hc o_h / n_hc, (hc + 1) o_h / n_hc) (sizes differ by <= 1)
-  it.h0 = hc * p.o_h / p.n_hc;
-  it.nrows = static_cast<int>((hc + 1) * p.o_h / p.n_hc - it.h0);
+  const uint32_t h0 = hc * o_h / n_hc;
+  it.h0 = h0;
+  it.nrows = static_cast<int>((hc + 1) * o_h / n_hc - h0);
   }
-  const int64_t xs = it.h0 * p.shift;
-  it.x0 = static_cast<int>(xs - xs % p.avec);
-  it.off0 = static_cast<int>(xs - it.x0);
+  const uint32_t xs = static_cast<uint32_t>(it.h0) * static_cast<uint32_t>(p.shift);  // < 2^30 (sweep_config)
+  it.x0 = static_cast<int>(xs - xs % static_cast<uint32_t>(p.avec));
+  it.off0 = static_cast<int>(xs - static_cast<uint32_t>(it.x0));
   if (it.nrows == 0) {  // (an empty piece of a balanced split: no atoms, no rows)
     it.n_a = 0;
     return it;
@@ -257,8 +263,10 @@ __device__ __forceinline__ void sw_store_row(const SweepParams& p, const CUtenso
     if (p.out_hnwc) {
       out_row = h * (p.i_n * p.o_w) + gr;
     } else {
-      const int64_t n = gr / p.o_w, w = gr - n * p.o_w;
-      out_row = (n * p.o_h + h) * p.o_w + w;
+      // (32-bit division: i_n o_w < 2^31, launch_sweep_gemm)
+      const uint32_t n = static_cast<uint32_t>(gr) / static_cast<uint32_t>(p.o_w);
+      const int64_t w = gr - static_cast<int64_t>(n) * p.o_w;
+      out_row = (static_cast<int64_t>(n) * p.o_h + h) * p.o_w + w;
     }
     orow_own = static_cast<unsigned char*>(p.O) + out_row * p.k_c * kOutElt;
   }
@@ -1167,6 +1175,8 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
     best_n = (pl.o_h + best_H - 1) / best_H;
     balanced = false;
   }
+  if (work_tiles * pl.o_h >= (1LL << 31) || pl.s.i_n * pl.o_w >= (1LL << 31))
+    return cudaErrorNotSupported;  // (the kernel's item and row indices are 32-bit)
   p.H = static_cast<int>(best_H);
   p.n_hc = best_n;
   p.n_items = p.n_hc * work_tiles;

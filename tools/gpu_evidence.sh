@@ -4,7 +4,8 @@
 # lines, the ncu launch list of the default command, full ncu captures of the
 # dominant kernels per config, and compute-sanitizer runs.  Every step under
 # its own timeout.   usage: tools/gpu_evidence.sh [parts]   (default: all)
-PARTS=${1:-"tests bench cfgs ncu sanitize"}
+# (compute-sanitizer is closed on this pool since round 2: sanitize only on request)
+PARTS=${1:-"tests bench cfgs ncu"}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv > gpurun_out/smi.csv
 has() { [[ " $PARTS " == *" $1 "* ]]; }
