@@ -106,31 +106,36 @@ struct Unit {
 };
 
 // unit group G (one per cluster iteration) -> the unit of pair pp of the cluster
-__device__ __forceinline__ Unit decode_unit(const WideParams& p, int64_t G, int pp) {
+__device__ __forceinline__ Unit decode_unit(const WideParams& p, int64_t G64, int pp) {
   Unit c;
+  // 32-bit index math (unit groups, tiles and h all fit, launch_wide_gemm):
+  // every role decodes each unit before its first atom
+  const uint32_t G = static_cast<uint32_t>(G64), g_full = static_cast<uint32_t>(p.g_full);
+  const uint32_t S = static_cast<uint32_t>(p.S), n_ng = static_cast<uint32_t>(p.n_ng);
   // the first g_full unit groups are whole tiles (hybrid split: whole waves
   // of unsplit tiles, then the last partial wave's tiles in p.S ranges)
-  int64_t g2;
-  if (G < p.g_full) {
+  uint32_t g2;
+  if (G < g_full) {
     g2 = G;
     c.ks = 0;
     c.nsplit = 1;
   } else {
-    const int64_t gt = (G - p.g_full) / p.S;
-    c.ks = static_cast<int>(G - p.g_full - gt * p.S);
-    g2 = p.g_full + gt;
+    const uint32_t gt = (G - g_full) / S;
+    c.ks = static_cast<int>(G - g_full - gt * S);
+    g2 = g_full + gt;
     c.nsplit = p.S;
   }
   // K range fastest, then the N group, then the (h, 256-row tile) combo: the
   // pairs in flight share A windows (same rows, neighbouring h) in L2
-  const int64_t hmg = g2 / p.n_ng;
-  c.ng = static_cast<int>(g2 - hmg * p.n_ng);
-  int64_t hm = hmg * p.mc + pp;
-  c.valid = hm < p.n_hm;
-  if (!c.valid) hm = p.n_hm - 1;  // (loads a real tile; the epilogue stores nothing)
-  c.h = hm % p.o_h;
-  c.mt = hm / p.o_h;
-  c.tile = hm * p.n_ng + c.ng;
+  const uint32_t hmg = g2 / n_ng;
+  c.ng = static_cast<int>(g2 - hmg * n_ng);
+  uint32_t hm = hmg * static_cast<uint32_t>(p.mc) + static_cast<uint32_t>(pp);
+  const uint32_t n_hm = static_cast<uint32_t>(p.n_hm), o_h = static_cast<uint32_t>(p.o_h);
+  c.valid = hm < n_hm;
+  if (!c.valid) hm = n_hm - 1;  // (loads a real tile; the epilogue stores nothing)
+  c.mt = hm / o_h;
+  c.h = hm - static_cast<uint32_t>(c.mt) * o_h;
+  c.tile = static_cast<int64_t>(hm) * p.n_ng + c.ng;
   c.a0 = c.nsplit == 1 ? 0 : c.ks * p.apk;
   c.a1 = c.nsplit == 1 ? p.n_atoms : min(p.n_atoms, c.a0 + p.apk);
   return c;
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
       // this lane's output row O[n, h, w, ncol0 ...] (n-h-w-c: Alg.2 l.17-19 at store time)
       unsigned char* orow = nullptr;
       if (row < p.rows) {
-        const int64_t n = row / p.o_w, w = row - n * p.o_w;
+        const int64_t n = static_cast<uint32_t>(row) / static_cast<uint32_t>(p.o_w), w = row - n * p.o_w;  // rows < 2^31
         orow = static_cast<unsigned char*>(p.O) + ((((n * p.o_h + c.h) * p.o_w + w) * p.k_c) + ncol0) * kOutElt;
       }
       const int64_t rem = p.rows - r0;
@@ -665,6 +670,7 @@ cudaError_t launch_wide_gemm(const Plan& pl, const GemmArgs& a, void* scratch, s
   if (const char* e = getenv("MEC_WIDE_MC"))
     p.mc = (atoi(e) == 2 && !p.b_mn && pl.n_var == 1 && g.g_full == 0) ? 2 : 1;
   p.n_hm = pl.o_h * g.n_mt;
+  if (p.n_hm * g.n_ng * std::max(1, g.S) >= (1LL << 31)) return cudaErrorNotSupported;  // (32-bit unit decode)
   p.n_groups = p.g_full + (((p.n_hm + p.mc - 1) / p.mc) * g.n_ng - p.g_full) * g.S;
   p.chunk_n = kTileKBytes / pl.elt;
   p.b_chunks = p.b_mn ? (pl.bn / 2) / p.chunk_n : 0;

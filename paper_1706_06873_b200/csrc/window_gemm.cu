@@ -733,6 +733,9 @@ __global__ void __launch_bounds__(kernel_threads<kGather>(), 1)
         int64_t out_row;
         if (p.out_hnwc) {
           out_row = c.h * (p.i_n * p.o_w) + gr;
+        } else if (p.tiles32) {  // (i_n o_w < 2^31 too: a 32-bit division)
+          const int64_t n = static_cast<uint32_t>(gr) / static_cast<uint32_t>(p.o_w), w = gr - n * p.o_w;
+          out_row = (n * p.o_h + c.h) * p.o_w + w;
         } else {
           const int64_t n = gr / p.o_w, w = gr - n * p.o_w;
           out_row = (n * p.o_h + c.h) * p.o_w + w;
@@ -1218,7 +1221,7 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   int64_t per = std::max<int64_t>(1, num_sms() / p.n_combo);
   per = std::min<int64_t>(per, max_tiles);
   p.ctas_per_combo = static_cast<int>(per);
-  p.tiles32 = max_tiles + per < (1LL << 31) && pl.o_h < (1LL << 31);
+  p.tiles32 = max_tiles + per < (1LL << 31) && pl.o_h < (1LL << 31) && pl.s.i_n * pl.o_w < (1LL << 31);
   const int64_t grid = per * p.n_combo;
   auto kern = tf32 ? (gather ? window_gemm_kernel<true, true> : window_gemm_kernel<true, false>)
                    : (gather ? window_gemm_kernel<false, true> : window_gemm_kernel<false, false>);
