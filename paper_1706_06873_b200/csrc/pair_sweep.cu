@@ -82,6 +82,11 @@ struct PsParams {
   int64_t n_pt;          // pair tiles = ceil(n_ctile / 2)
   int H;                 // output rows per chunk (the last chunk may be shorter)
   int64_t n_hc, n_items;
+  // balanced split (bal_P > 0): pair c owns rows [c R / P, (c + 1) R / P) of
+  // the flattened (pair tile, h) sequence (R = n_pt o_h), cut at pair-tile
+  // boundaries into at most bal_J items; item it = c + j P is piece j of pair c
+  int64_t bal_R;
+  int bal_P, bal_J;
   int64_t shift;         // elements
   int bk, sa, na;        // atom width (elements), shift atoms, window atoms (kdim_pad / bk)
   int bn;                // MMA N (k_c rounded up to 16)
@@ -116,6 +121,32 @@ __device__ __forceinline__ CTile ctile(const PsParams& p, int64_t c) {
     t.w0 = 0;
   }
   return t;
+}
+
+// work item it -> pair tile pt, first output row h0 and row count (0: an
+// empty piece of a balanced split)
+__device__ __forceinline__ void ps_item(const PsParams& p, int64_t it, int64_t* pt, int64_t* h0, int* rows) {
+  if (p.bal_P > 0) {
+    const int64_t c = it % p.bal_P, j = it / p.bal_P;
+    const int64_t s = c * p.bal_R / p.bal_P, e = (c + 1) * p.bal_R / p.bal_P;
+    const int64_t tile0 = s / p.o_h;
+    const int64_t start = j == 0 ? s : (tile0 + j) * p.o_h;
+    const int64_t end = min(e, (tile0 + j + 1) * p.o_h);
+    if (start >= end) {
+      *pt = tile0;
+      *h0 = 0;
+      *rows = 0;
+      return;
+    }
+    *pt = start / p.o_h;
+    *h0 = start - *pt * p.o_h;
+    *rows = static_cast<int>(end - start);
+    return;
+  }
+  const int64_t q = it / p.n_hc, hc = it - q * p.n_hc;
+  *pt = q;
+  *h0 = hc * p.H;
+  *rows = static_cast<int>(p.o_h - *h0 < p.H ? p.o_h - *h0 : p.H);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -193,9 +224,10 @@ __global__ void __launch_bounds__(kPsThreads, 1)
       const long long c_p0 = clock64();
 #endif
       for (int64_t it = pair; it < p.n_items; it += n_pairs) {
-        const int64_t pt = it / p.n_hc, hc = it - pt * p.n_hc;
-        const int64_t h0 = hc * p.H;
-        const int rows = static_cast<int>(p.o_h - h0 < p.H ? p.o_h - h0 : p.H);
+        int64_t pt, h0;
+        int rows;
+        ps_item(p, it, &pt, &h0, &rows);
+        if (rows == 0) continue;
         const int n_stream = (rows - 1) * p.sa + p.na;
         const CTile t = ctile(p, 2 * pt + rank);
         const int32_t x0 = static_cast<int32_t>(h0 * p.shift);
@@ -297,8 +329,10 @@ __global__ void __launch_bounds__(kPsThreads, 1)
       const long long c_m0 = clock64();
 #endif
       for (int64_t it = pair; it < p.n_items; it += n_pairs) {
-        const int64_t hc = it % p.n_hc;
-        const int rows = static_cast<int>(p.o_h - hc * p.H < p.H ? p.o_h - hc * p.H : p.H);
+        int64_t pt_, h0_;
+        int rows;
+        ps_item(p, it, &pt_, &h0_, &rows);
+        if (rows == 0) continue;
         const int n_stream = (rows - 1) * sa + na;
 #ifdef MEC_TRACE
         rows_total += static_cast<uint32_t>(rows);
@@ -392,9 +426,10 @@ __global__ void __launch_bounds__(kPsThreads, 1)
     const int64_t cols_left = p.k_c;
     uint32_t row_seq = 0;
     for (int64_t it = pair; it < p.n_items; it += n_pairs) {
-      const int64_t pt = it / p.n_hc, hc = it - pt * p.n_hc;
-      const int64_t h0 = hc * p.H;
-      const int rows = static_cast<int>(p.o_h - h0 < p.H ? p.o_h - h0 : p.H);
+      int64_t pt, h0;
+      int rows;
+      ps_item(p, it, &pt, &h0, &rows);
+      if (rows == 0) continue;
       const CTile t = ctile(p, 2 * pt + rank);
       // this thread's row of the tile: image n, column w
       int64_t n, w;
@@ -656,10 +691,41 @@ cudaError_t launch_pair_sweep(const Plan& pl, const GemmArgs& a, cudaStream_t st
       best_hc = hc;
     }
   }
-  if (const char* e2 = getenv("MEC_PS_CHUNKS")) best_hc = std::max<int64_t>(1, std::min<int64_t>(pl.o_h, atoi(e2)));
+  // balanced split: each pair the same number of (pair tile, h) rows, cut at
+  // pair-tile boundaries (<= 2 pieces when a pair's share is at most one
+  // tile's rows), where the wave model prefers it to the chunks -- no idle
+  // pairs (cv4 / cv8 at b128: 64 pair tiles of one chunk for 74 pairs) and no
+  // partial last wave (C2 tf32); cost = its pieces' streams
+  bool balanced = false;
+  const int64_t R = g.n_pt * pl.o_h, P = max_clusters;
+  if (R >= P) {
+    double worst = 0.0;
+    for (int64_t c = 0; c < P; ++c) {
+      const int64_t s0 = c * R / P, e0 = (c + 1) * R / P;
+      double t = 0.0;
+      for (int64_t pos = s0; pos < e0;) {
+        const int64_t end = std::min(e0, (pos / pl.o_h + 1) * pl.o_h);
+        t += static_cast<double>((end - pos - 1) * g.sa + g.na + 4);
+        pos = end;
+      }
+      worst = std::max(worst, t);
+    }
+    balanced = worst < best_t * 0.999;
+  }
+  if (const char* e3 = getenv("MEC_PS_BALANCED")) balanced = atoi(e3) != 0 && R >= P;
+  if (const char* e2 = getenv("MEC_PS_CHUNKS")) {
+    best_hc = std::max<int64_t>(1, std::min<int64_t>(pl.o_h, atoi(e2)));
+    balanced = false;
+  }
   p.H = static_cast<int>((pl.o_h + best_hc - 1) / best_hc);
   p.n_hc = (pl.o_h + p.H - 1) / p.H;
   p.n_items = g.n_pt * p.n_hc;
+  if (balanced) {
+    p.bal_R = R;
+    p.bal_P = static_cast<int>(P);
+    p.bal_J = static_cast<int>(((R + P - 1) / P + pl.o_h - 1) / pl.o_h + 1);
+    p.n_items = P * p.bal_J;
+  }
   CUtensorMap tmA, tmB;
   {
     // L per image: {i_h k_w i_c, o_w, i_n} (pitched rows); box = 128 rows or one image slot

@@ -1001,6 +1001,30 @@ def test_pair_sweep_kernel(cuda_ok, case, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("case", [0, 2, 3, 6, 7])
+def test_pair_sweep_balanced_split(cuda_ok, monkeypatch, case, dtype):
+    """The pair sweep's balanced split (every pair the same number of (pair tile,
+    h) rows, cut at pair-tile boundaries), forced on these small
+    shapes (1-2 rows per pair, empty pieces): the same K steps per row as the
+    one-window kernel, so bit for bit."""
+    shape, s, path = PS_CASES[case]
+    I, K = make_inputs(shape, dtype, seed=8100 + case)
+    Id, Kd = to_dev(I, dtype), to_dev(K, dtype)
+    if path == "stream":
+        path = MEC_PATH_SOLUTION_B
+        monkeypatch.setenv("MEC_PS_BSTREAM", "1")
+    monkeypatch.setenv("MEC_PS_BALANCED", "1")
+    O, g = mec.conv_forward(Id, Kd, s, s, path=path, gemm_kernel=4, return_gemm=True)
+    torch.cuda.synchronize()
+    assert g == 4
+    O1 = mec.conv_forward(Id, Kd, s, s, path=path, gemm_kernel=1)
+    torch.cuda.synchronize()
+    assert torch.equal(O, O1)
+    ref = oracle.direct_conv(I, K, s, s, n_threads=8)
+    check_O(O, ref, dtype, shape[3] * shape[4] * shape[5])
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
 def test_C2_pair_sweep_full_batch_sampled(cuda_ok, dtype):
     """C2 at b64 through the pair sweep (tf32: the automatic choice)."""
     c = "C2" if dtype == "bf16" else "C2_tf32"
