@@ -103,6 +103,12 @@ struct PsParams {
   uint32_t stage_bytes;  // aps x slot_bytes
   uint32_t idesc;
   bool a_evict_first;    // (experiments: MEC_PS_EVICT_FIRST=1) L2 evict-first hint on the L stream
+  // streamed weights in ONE 3-D TMA box per atom (tmB3: {kdim_pad, kc_pad,
+  // b_open} with the third stride sa atoms): slab z = the weight atom of row
+  // r_hi - z (atom j - r_hi sa + z sa); slabs of rows that are not open (item
+  // start / end) are loaded and not read.  One issue instead of one per open
+  // row: the producer was ~87% busy issuing 5 boxes per cv4 atom
+  bool b3;
 };
 
 // CTA tile c -> the image and first row (w) of each of its rows' slots
@@ -157,7 +163,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 template <bool kTF32, int kAps>
 __global__ void __launch_bounds__(kPsThreads, 1)
     pair_sweep_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const PsParams p) {
+                      const __grid_constant__ CUtensorMap tmB3, const PsParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + kSmemAlign - 1) & ~uintptr_t(kSmemAlign - 1));
@@ -182,6 +188,7 @@ __global__ void __launch_bounds__(kPsThreads, 1)
   if (threadIdx.x == 0) {
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
+    if (p.b3) ptx::tma_prefetch_desc(&tmB3);
     for (int i = 0; i < S; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1);
@@ -246,7 +253,8 @@ __global__ void __launch_bounds__(kPsThreads, 1)
           if (k == 0) {  // a new stage: its bytes (up to aps atoms), one expect_tx
             uint32_t bytes = 0;
             if (kAps == 1) {
-              bytes = p.a_bytes + (p.b_stream ? static_cast<uint32_t>(r_hi - r_lo + 1) * p.b_half_bytes : 0u);
+              bytes = p.a_bytes + (p.b_stream ? static_cast<uint32_t>(p.b3 ? p.b_open : r_hi - r_lo + 1) * p.b_half_bytes
+                                              : 0u);
             } else {
               const int na_s = min(kAps, n_stream - j);
               for (int kk = 0; kk < na_s; ++kk) {
@@ -266,7 +274,10 @@ __global__ void __launch_bounds__(kPsThreads, 1)
             if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2u * bytes);
           }
           unsigned char* dA = smem + static_cast<size_t>(stage) * p.stage_bytes + static_cast<size_t>(k) * p.slot_bytes;
-          if (p.b_stream) {
+          if (p.b3) {
+            ptx::tma_load_3d_pair(dA + kBM * kTileKBytes, &tmB3, fb, (j - r_hi * p.sa) * p.bk,
+                                  static_cast<int32_t>(rank * (p.bn / 2)), 0, hintB);
+          } else if (p.b_stream) {
             for (int r = r_lo; r <= r_hi; ++r)
               ptx::tma_load_2d_pair(dA + kBM * kTileKBytes + (r - r_lo) * p.b_half_bytes, &tmB, fb,
                                     (j - r * p.sa) * p.bk, static_cast<int32_t>(rank * (p.bn / 2)), hintB);
@@ -373,8 +384,11 @@ __global__ void __launch_bounds__(kPsThreads, 1)
           // weights: the atom slot's weight part r - r_lo (streamed) or resident atom a
           int a = j - lo_start;
           uint32_t acc = acc_lo;
-          uint64_t bd = p.b_stream ? ad + a_to_b16 : bdesc0 + static_cast<uint32_t>(a) * b16;
-          const int64_t bstep = p.b_stream ? static_cast<int64_t>(b16) : -static_cast<int64_t>(sa) * b16;
+          // (3-D weight box: row r's slab is z = r_hi - r, so the rows walk it backwards)
+          uint64_t bd = p.b3 ? ad + a_to_b16 + static_cast<uint32_t>(r_hi - r_lo) * b16
+                             : (p.b_stream ? ad + a_to_b16 : bdesc0 + static_cast<uint32_t>(a) * b16);
+          const int64_t bstep = p.b3 ? -static_cast<int64_t>(b16)
+                                     : (p.b_stream ? static_cast<int64_t>(b16) : -static_cast<int64_t>(sa) * b16);
           for (int r = r_lo; r <= r_hi; ++r) {
             ptx::mma_ss_atom_pair_elect<kTF32>(tmem_base + acc * bn, ad, bd, p.idesc, a != 0 ? 1u : 0u);
             if (++acc == n_acc) acc = 0;
@@ -744,10 +758,27 @@ cudaError_t launch_pair_sweep(const Plan& pl, const GemmArgs& a, cudaStream_t st
     e = encode_tiled(&tmB, tf32, 2, a.Kt, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
+  CUtensorMap tmB3;
+  std::memset(&tmB3, 0, sizeof(tmB3));
+  p.b3 = false;
+  if (g.b_stream && !(getenv("MEC_PS_B3") && atoi(getenv("MEC_PS_B3")) == 0) && g.aps == 1) {
+    // Kt as {kdim_pad, kc_pad, b_open}: the third stride is one window shift
+    // (sa atoms); slab z starts z sa atoms further along the same channel row
+    // (past a row's end it reads the next row, or the workspace tail reserved
+    // for it, Plan::bytes_kt -- never an open row's weights)
+    const uint64_t dims[3] = {static_cast<uint64_t>(pl.kdim_pad), static_cast<uint64_t>(pl.kc_pad),
+                              static_cast<uint64_t>(g.b_open)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(pl.kdim_pad) * pl.elt,
+                                 static_cast<uint64_t>(g.sa) * pl.bk * pl.elt};
+    const uint32_t box[3] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(pl.bn / 2),
+                             static_cast<uint32_t>(g.b_open)};
+    if (encode_tiled(&tmB3, tf32, 3, a.Kt, dims, strides, box) == cudaSuccess) p.b3 = true;
+    else cudaGetLastError();
+  }
   const int64_t pairs = std::min<int64_t>(max_clusters, p.n_items);
   cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
   cfg.numAttrs = getenv("MEC_NO_PDL") ? 1 : 2;
-  e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, p);
+  e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmB3, p);
   if (e != cudaSuccess) return e;
   if (launches) ++*launches;
   return cudaGetLastError();
