@@ -331,8 +331,10 @@ __global__ void __launch_bounds__(kWideThreads, 1)
       // split-K slots of this (tile, rank, N sub-tile): chunk-major, 16-byte
       // chunk q of row m at (q * 128 + m) * 16, a warp's store is 512 contiguous bytes
       const int64_t slot_elems = static_cast<int64_t>(n_c4) * kBM;  // float4s per slot
+      // (hybrid split: the split tiles are the ones from g_full on -- tile ==
+      // unit group index with one pair per cluster -- and only they have slots)
       const float4* part_t = reinterpret_cast<const float4*>(p.part) +
-                             ((c.tile * p.S * 2 + rank) * p.n_sub + sub) * slot_elems;
+                             (((c.tile - p.g_full) * p.S * 2 + rank) * p.n_sub + sub) * slot_elems;
       const int64_t k_stride = 2 * p.n_sub * slot_elems;  // next range of the same tile
       // output chunks of kPw columns; with split-K, range k owns (reduces and
       // stores) the chunks ci with ci S / n_oc == k and hands the others over
@@ -560,7 +562,8 @@ WideGeo wide_geo(const Plan& pl, int split) {
   g.S = (g.n_atoms + g.apk - 1) / g.apk;  // no empty ranges
   g.cnt_words = static_cast<size_t>(g.tiles) * 8 * g.n_sub;
   g.cnt_bytes = (g.cnt_words * sizeof(uint32_t) + 1023) / 1024 * 1024;
-  g.part_bytes = g.S > 1 ? static_cast<size_t>(g.tiles) * g.S * kPairM * g.n_sub * pl.bn * sizeof(float) : 0;
+  // partial slots for the split tiles only (hybrid: the tail after g_full)
+  g.part_bytes = g.S > 1 ? static_cast<size_t>(g.tiles - g.g_full) * g.S * kPairM * g.n_sub * pl.bn * sizeof(float) : 0;
   return g;
 }
 
