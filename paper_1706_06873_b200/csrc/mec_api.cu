@@ -167,9 +167,10 @@ void set_window_geometry(Plan* p, int64_t kw_s) {
   p->bytes_L_pitched = static_cast<size_t>(s->i_n * p->o_w * p->pitch) * p->elt;
   p->off_kt = static_cast<size_t>(round_up(static_cast<int64_t>(p->bytes_L_pitched), 1024));
   p->bytes_kt = static_cast<size_t>(std::max(p->n_var * p->kdim_pad, p->kdim_g) * p->kc_pad) * p->elt;
-  // tail: the pair sweep's 3-D weight box reads up to 3 window shifts past the
-  // last channel row's end (slabs of rows that are not open; never used)
-  p->bytes_kt += static_cast<size_t>(4 * p->shift + p->bk) * p->elt;
+  // tail: the pair sweep's 3-D weight box reads up to (open rows - 1) window
+  // shifts past the last channel row's end (slabs of rows that are not open;
+  // never used); open rows <= 7 (at most 8 accumulators, one spare)
+  p->bytes_kt += static_cast<size_t>(8 * p->shift + p->bk) * p->elt;
   p->off_wide = static_cast<size_t>(round_up(static_cast<int64_t>(p->off_kt + p->bytes_kt), 1024));
   p->ws_bytes = p->off_kt + p->bytes_kt + 1024;
 }
