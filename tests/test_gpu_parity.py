@@ -967,6 +967,8 @@ PS_CASES = [
     ((2, 17, 70, 128, 2, 2, 32), 1, MEC_PATH_SOLUTION_B),   # shift = 2 atoms, window 4 atoms
     ((2, 40, 60, 64, 7, 7, 64), 2, MEC_PATH_SOLUTION_B),    # cv4-like: 49-atom window, weights streamed
     ((3, 30, 150, 64, 3, 3, 64), 1, "stream"),              # resident-size weights forced to stream
+    ((1, 20, 40, 64, 7, 7, 64), 1, MEC_PATH_SOLUTION_B),    # 7 open rows, streamed weights: the 3-D weight
+                                                            # box's slabs reach 6 window shifts past K_t
 ]
 
 
