@@ -160,6 +160,9 @@ struct SweepParams {
   bool fused;
   int kwc, i_c, s_w, pad_h, pad_w;
   int dbg;  // (experiments, MEC_SWEEP_DBG) 1: no O stores, 2: no MMAs, 4: no TMEM stores of A
+  // tiles in reverse order: the first wave streams the images the lowering
+  // wrote last, whose L lines are still in L2
+  bool reverse;
 };
 
 struct SwItem {
@@ -175,7 +178,8 @@ __device__ __forceinline__ SwItem sw_decode(const SweepParams& p, int64_t t, boo
                                            uint32_t rank = 0) {
   SwItem it;
   if (!pair && p.bal_G > 0) {
-    const int64_t c = t % p.bal_G, j = t / p.bal_G;
+    const int64_t c0 = t % p.bal_G, j = t / p.bal_G;
+    const int64_t c = p.reverse ? p.bal_G - 1 - c0 : c0;
     const int64_t s = c * p.bal_R / p.bal_G, e = (c + 1) * p.bal_R / p.bal_G;
     const int64_t tile0 = s / p.o_h;
     const int64_t start = j == 0 ? s : (tile0 + j) * p.o_h;
@@ -194,6 +198,7 @@ __device__ __forceinline__ SwItem sw_decode(const SweepParams& p, int64_t t, boo
   const uint32_t hc = tt % n_hc;
   tt /= n_hc;
   if (pair) tt = 2 * tt + rank;  // pair tile -> this CTA's tile
+  else if (p.reverse) tt = static_cast<uint32_t>(p.n_tiles) - 1 - tt;
   it.valid = tt < static_cast<uint32_t>(p.n_tiles);
   if (!it.valid) tt = static_cast<uint32_t>(p.n_tiles) - 1;  // (a real tile's coordinates; nothing is stored)
   const uint32_t n_mt = static_cast<uint32_t>(p.n_mt);
@@ -1066,6 +1071,9 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   p.col_shift = pl.elt == 2 ? 1 : 0;
   p.out_hnwc = a.out_hnwc;
   p.dbg = getenv("MEC_SWEEP_DBG") ? atoi(getenv("MEC_SWEEP_DBG")) : 0;
+  // (measured: C2 GEMM 309 -> 307.5 us, cv7 b128 232.7 -> 230.3 us, C3 equal;
+  // profiles/r2_sweep_reverse.txt.  MEC_SWEEP_REV=0: forward order)
+  p.reverse = !a.fused && !(getenv("MEC_SWEEP_REV") && atoi(getenv("MEC_SWEEP_REV")) == 0);
   // two issuers need every atom read by both issuers' rows (windows of rows
   // h and h + 2 overlap), else an issuer could lag a slot by two fills
   // (measured: 2 issuers win where the accumulators are 64 columns -- C2
