@@ -993,7 +993,14 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
   const int out_elt = pl.elt;
   CUtensorMap tmA, tmB, tmO;
   // row tiling: as window_gemm.cu
-  const bool flat = !a.fused && a.batch_folded && pl.o_w < 32;
+  // flat batch-folded rows (n o_w + w, 128 per tile, one TMA box per atom)
+  // for o_w < 32, and for o_w <= 64 where the window shift is 16-byte aligned
+  // (one weight copy): measured C3 GEMM 85.3 -> 79.0 us, cv9 b128 51.4 -> 46.2,
+  // while AlexNet conv1's shape (two weight copies) kept image slots (C1 22.5
+  // vs 24.8 us; profiles/r2_sweep_flat_rows.txt).  MEC_SWEEP_FLAT64=0: slots.
+  const bool flat64 = pl.o_w <= 64 && pl.shift % (16 / pl.elt) == 0 &&
+                      !(getenv("MEC_SWEEP_FLAT64") && atoi(getenv("MEC_SWEEP_FLAT64")) == 0);
+  const bool flat = !a.fused && a.batch_folded && (pl.o_w < 32 || flat64);
   int slot = 128, ipt = 1;
   if (!flat && pl.o_w <= 128) {
     slot = static_cast<int>((pl.o_w + 31) / 32 * 32);
