@@ -963,7 +963,11 @@ cudaError_t launch_window_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t s
   CUtensorMap tmA, tmB, tmO;
   // Row tiling (see GemmParams): Solution A with o_w < 32 folds flat (a
   // 32-row epilogue block then spans several images); otherwise image slots.
-  const bool flat = !a.fused && a.batch_folded && pl.o_w < 32;
+  // (as the h-sweep: flat rows also for o_w <= 64 with a 16-byte aligned
+  // window shift; MEC_SWEEP_FLAT64=0: image slots)
+  const bool flat64 = pl.o_w <= 64 && pl.shift % (16 / pl.elt) == 0 &&
+                      !(getenv("MEC_SWEEP_FLAT64") && atoi(getenv("MEC_SWEEP_FLAT64")) == 0);
+  const bool flat = !a.fused && a.batch_folded && (pl.o_w < 32 || flat64);
   int slot = 128, ipt = 1;
   const bool gather = a.fused && !fused_eligible(pl);
   if (!flat && pl.o_w <= 128) {
