@@ -502,18 +502,14 @@ __global__ void __launch_bounds__(kSwThreads, 1)
               }
             }
             const int32_t zy = hh - p.pad_h;  // (padding: TMA zero-fills out-of-bounds pixels and rows)
-            if (p.ipt <= 1) {
-              ptx::tma_load_4d(dstA, &tmA, &full[stage], cb, y0 * p.s_w + b - p.pad_w, zy, z0, hintA);
-            } else {
-              for (int j = 0; j < p.ipt; ++j)
-                ptx::tma_load_4d(dstA + j * p.slot * kTileKBytes, &tmA, &full[stage], cb, b - p.pad_w, zy,
-                                 z0 * p.ipt + j, hintA);
-            }
+            // (ipt > 1: one box of ipt images x `slot` pixels -- the box's
+            // last extent is ipt; images >= i_n and pixels >= the width: zero fill)
+            ptx::tma_load_4d(dstA, &tmA, &full[stage], cb, (p.ipt <= 1 ? y0 * p.s_w : 0) + b - p.pad_w, zy,
+                             p.ipt <= 1 ? z0 : z0 * p.ipt, hintA);
           } else if (p.ipt <= 1) {
             ptx::tma_load_3d(dstA, &tmA, &full[stage], x, y0, z0, hintA);
-          } else {  // one box of `slot` rows per image of the tile (images >= i_n: zero fill)
-            for (int j = 0; j < p.ipt; ++j)
-              ptx::tma_load_3d(dstA + j * p.slot * kTileKBytes, &tmA, &full[stage], x, 0, z0 * p.ipt + j, hintA);
+          } else {  // one box of ipt images x `slot` rows (images >= i_n, rows >= o_w: zero fill)
+            ptx::tma_load_3d(dstA, &tmA, &full[stage], x, 0, z0 * p.ipt, hintA);
           }
           SW_TRACE(pseq, 0);
           if (pseq < 100) SW_TRACE(300u + pseq, 2);
@@ -1019,7 +1015,8 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
                                  static_cast<uint64_t>(pl.src_w * pl.s.i_c) * pl.elt,
                                  static_cast<uint64_t>(pl.src_h * pl.src_w * pl.s.i_c) * pl.elt};
     const uint32_t rows_box = static_cast<uint32_t>(ipt > 1 ? slot : kBM);
-    const uint32_t box[4] = {static_cast<uint32_t>(pl.bk), rows_box * static_cast<uint32_t>(pl.s_w), 1, 1};
+    const uint32_t box[4] = {static_cast<uint32_t>(pl.bk), rows_box * static_cast<uint32_t>(pl.s_w), 1,
+                             static_cast<uint32_t>(ipt)};
     const uint32_t es[4] = {1, static_cast<uint32_t>(pl.s_w), 1, 1};
     cudaError_t e = encode_tiled_strided(&tmA, tf32, 4, a.L, dims, strides, box, es);
     if (e != cudaSuccess) return e;
@@ -1028,7 +1025,8 @@ cudaError_t launch_sweep_gemm(const Plan& pl, const GemmArgs& a, cudaStream_t st
                               static_cast<uint64_t>(flat ? 1 : pl.s.i_n)};
     const uint64_t strides[2] = {static_cast<uint64_t>(pl.pitch) * pl.elt,
                                  static_cast<uint64_t>(pl.pitch) * pl.elt * rows};
-    const uint32_t box[3] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(ipt > 1 ? slot : kBM), 1};
+    const uint32_t box[3] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(ipt > 1 ? slot : kBM),
+                             static_cast<uint32_t>(ipt)};
     cudaError_t e = encode_tiled(&tmA, tf32, 3, a.L, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
