@@ -286,9 +286,8 @@ __global__ void __launch_bounds__(kPsThreads, 1)
           if (p.ipt == 1) {
             ptx::tma_load_3d_pair(dA, &tmA, fb, x, static_cast<int32_t>(t.w0), static_cast<int32_t>(t.n0), hintA);
           } else {
-            for (int s = 0; s < p.ipt; ++s)
-              ptx::tma_load_3d_pair(dA + s * p.slot * kTileKBytes, &tmA, fb, x, 0, static_cast<int32_t>(t.n0 + s),
-                                    hintA);
+            // one box of ipt images x slot rows (images >= i_n, rows >= o_w: zero fill)
+            ptx::tma_load_3d_pair(dA, &tmA, fb, x, 0, static_cast<int32_t>(t.n0), hintA);
           }
 #ifdef MEC_TRACE
           ++n_atoms;
@@ -747,7 +746,8 @@ cudaError_t launch_pair_sweep(const Plan& pl, const GemmArgs& a, cudaStream_t st
                               static_cast<uint64_t>(pl.s.i_n)};
     const uint64_t strides[2] = {static_cast<uint64_t>(pl.pitch) * pl.elt,
                                  static_cast<uint64_t>(pl.pitch) * pl.elt * pl.o_w};
-    const uint32_t box[3] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(g.ipt == 1 ? kBM : g.slot), 1};
+    const uint32_t box[3] = {static_cast<uint32_t>(pl.bk), static_cast<uint32_t>(g.ipt == 1 ? kBM : g.slot),
+                             static_cast<uint32_t>(g.ipt)};
     e = encode_tiled(&tmA, tf32, 3, a.L, dims, strides, box);
     if (e != cudaSuccess) return e;
   }
