@@ -752,6 +752,9 @@ __global__ void __launch_bounds__(512) lower_kernel(const LowerParams p) {
 // re-reads of I (neighbouring w share pixels) are served by L2.  Zero
 // padding (NEXT-4): vectors of pixels outside the unpadded image are zeros.
 // Blocks past the L rows prepare the weight operand (as lower_kernel).
+#ifndef MEC_ROWS_UNROLL
+#define MEC_ROWS_UNROLL 4  // 16-byte vectors in flight per thread (row-copy lowering)
+#endif
 template <typename T>
 __global__ void __launch_bounds__(256) lower_rows_kernel(const LowerParams p) {
   constexpr uint32_t VEC = 16 / sizeof(T);
@@ -773,10 +776,10 @@ __global__ void __launch_bounds__(256) lower_rows_kernel(const LowerParams p) {
     const int64_t n = row / p.o_w, w = row - n * p.o_w;
     uint4* dst = reinterpret_cast<uint4*>(p.L + static_cast<size_t>(row * p.pitch) * sizeof(T));
     // vector u of the row: strip h = u / vps, vector j = u mod vps of the strip
-    for (uint32_t u0 = threadIdx.x; u0 < p.vpr; u0 += 4 * blockDim.x) {
-      uint4 v[4];
+    for (uint32_t u0 = threadIdx.x; u0 < p.vpr; u0 += MEC_ROWS_UNROLL * blockDim.x) {
+      uint4 v[MEC_ROWS_UNROLL];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < MEC_ROWS_UNROLL; ++k) {
         const uint32_t u = u0 + k * blockDim.x;
         v[k] = make_uint4(0u, 0u, 0u, 0u);
         if (u < p.vpr) {
@@ -795,7 +798,7 @@ __global__ void __launch_bounds__(256) lower_rows_kernel(const LowerParams p) {
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < MEC_ROWS_UNROLL; ++k) {
         const uint32_t u = u0 + k * blockDim.x;
         if (u < p.vpr) dst[u] = v[k];
       }
