@@ -525,6 +525,15 @@ def measure(args, cfg, rw, rank, ws, dev, peaks, peak_src, tf32_peak, primary=Tr
             "traffic_source": nk.get("source"),
             "all_kernels": {k: {"ms": v[0], "bound": v[1], "achieved": v[2], "unit": v[4],
                                 "frac": v[2] / v[3], "algorithmic_per_launch": v[5]} for k, v in kernels.items()}}
+    # the same fraction against the nominal B200 figures SURVEY 8(d) asks to
+    # report beside the measured ones (north_star: "~8 TB/s"; 2.25 PF/s dense
+    # bf16, tf32 half), and against the sustained bf16 measurement
+    nom = 8000.0 if bound == "hbm" else (2250.0 if dtype_name == "bf16" else 1125.0)
+    roof["nominal"] = {"peak": nom, "unit": unit, "frac": ach / nom,
+                       "source": "B200 nominal: HBM 8 TB/s, dense bf16 2.25 PF/s (tf32 x 1/2)"}
+    if bound == "tensor" and peaks.get("bf16_tflops_sustained"):
+        sus = peaks["bf16_tflops_sustained"] * (1.0 if dtype_name == "bf16" else 0.5)
+        roof["frac_of_sustained"] = ach / sus
     g_flops_rate = flops / (mean_gemm * 1e-3) / 1e12
     tpu = {"gemm_tflops": g_flops_rate, "of_dense_peak": g_flops_rate / tc, "peak_tflops": tc,
            "peak_source": f"{tc_src} ({peak_src})",
